@@ -1,0 +1,166 @@
+// Device-side building blocks for the sm_100a data plane: bf16 packing,
+// mbarrier + 1-D bulk-copy (TMA engine) ring primitives, ldmatrix/mma.sync
+// fragments, cache-global loads for data produced by other CTAs in the same
+// launch, and a self-resetting grid barrier for persistent kernels.
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#define MESH_DEV __device__ __forceinline__
+
+namespace meshgpu {
+
+// ---------------------------------------------------------------- bf16 utils
+MESH_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+MESH_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xffff0000u); }
+MESH_DEV float bf16_to_f(uint16_t v) { return __uint_as_float(uint32_t(v) << 16); }
+// Round-to-nearest-even fp32 -> bf16 (matches the CPU oracle's rounding).
+MESH_DEV uint16_t f_to_bf16(float f) {
+    return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+MESH_DEV uint32_t pack_bf16x2(float lo, float hi) {
+    return uint32_t(f_to_bf16(lo)) | (uint32_t(f_to_bf16(hi)) << 16);
+}
+
+// ------------------------------------------------------- cache-global loads
+// Data written by other CTAs during the same launch must bypass L1.
+MESH_DEV float ldcg_f32(const float* p) { return __ldcg(p); }
+MESH_DEV int ldcg_i32(const int* p) { return __ldcg(p); }
+MESH_DEV uint4 ldcg_u4(const void* p) { return __ldcg(reinterpret_cast<const uint4*>(p)); }
+MESH_DEV uint2 ldcg_u2(const void* p) { return __ldcg(reinterpret_cast<const uint2*>(p)); }
+MESH_DEV uint32_t ldcg_u32(const void* p) { return __ldcg(reinterpret_cast<const unsigned int*>(p)); }
+
+// ------------------------------------------------------------------ mbarrier
+MESH_DEV uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+MESH_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count));
+}
+MESH_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory"); }
+MESH_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+MESH_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+MESH_DEV bool mbar_try_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, p;\n\t}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+MESH_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+    while (!mbar_try_wait(bar, parity)) {
+    }
+}
+
+// 1-D bulk copy global -> shared through the TMA engine, completing on `bar`.
+MESH_DEV void bulk_g2s(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+// Same, with an L2 evict-first policy for streamed-once weights.
+MESH_DEV void bulk_g2s_evict_first(void* smem_dst, const void* gsrc, uint32_t bytes, uint64_t* bar,
+                                   uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+            smem_u32(smem_dst)),
+        "l"(gsrc), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+MESH_DEV uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;\n" : "=l"(pol));
+    return pol;
+}
+
+// ------------------------------------------------------------ tensor cores
+MESH_DEV void ldmatrix_x4(uint32_t smem_addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                          uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(smem_addr));
+}
+MESH_DEV void ldmatrix_x2(uint32_t smem_addr, uint32_t& r0, uint32_t& r1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];\n"
+                 : "=r"(r0), "=r"(r1)
+                 : "r"(smem_addr));
+}
+MESH_DEV void ldmatrix_x2_trans(uint32_t smem_addr, uint32_t& r0, uint32_t& r1) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0,%1}, [%2];\n"
+                 : "=r"(r0), "=r"(r1)
+                 : "r"(smem_addr));
+}
+MESH_DEV void ldmatrix_x4_trans(uint32_t smem_addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
+                                uint32_t& r3) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+                 : "r"(smem_addr));
+}
+// D = A(16x16, row) * B(16x8, col) + D ; bf16 inputs, fp32 accumulate.
+MESH_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
+                             uint32_t b0, uint32_t b1) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+MESH_DEV void named_bar_sync(int id, int nthreads) {
+    asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// ------------------------------------------------------------ grid barrier
+// Sense-reversing barrier over all CTAs of a persistent launch. `count` returns
+// to 0 after every barrier and `gen` only ever increments, so the pair needs no
+// reset between launches. Called by ONE thread per CTA after a CTA-level sync.
+MESH_DEV void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int nblocks) {
+    unsigned int my_gen;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(my_gen) : "l"(gen) : "memory");
+    __threadfence();
+    unsigned int old = atomicAdd(count, 1u);
+    if (old == nblocks - 1) {
+        atomicExch(count, 0u);
+        __threadfence();
+        asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(gen), "r"(my_gen + 1) : "memory");
+    } else {
+        unsigned int cur;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(cur) : "l"(gen) : "memory");
+        } while (cur == my_gen);
+    }
+    __threadfence();
+}
+
+// ------------------------------------------------ weight tiling (T16 x SW128)
+// Weight matrices [N][K] bf16 live in HBM as 16-row tiles; each tile is K/64
+// blocks of 16 rows x 64 columns (2 KB) with the 128-byte swizzle, so a tile is
+// contiguous and any run of blocks can be fetched with one bulk copy and read
+// conflict-free by ldmatrix (and is the canonical SW128 K-major UMMA layout).
+MESH_DEV uint32_t sw128_off(int r, int c) {  // byte offset of (r, c) inside a 16x64 block
+    return uint32_t(r) * 128u + ((uint32_t((c >> 3) ^ (r & 7))) << 4) + uint32_t(c & 7) * 2u;
+}
+__host__ __device__ inline size_t tiled_index(int row, int col, int K) {
+    // element index (not bytes) of logical (row, col) in the tiled layout
+    size_t tile = size_t(row >> 4), kb = size_t(col >> 6);
+    int r = row & 15, c = col & 63;
+    size_t block = tile * size_t(K >> 6) + kb;
+    size_t inblock = size_t(r) * 64 + size_t((((c >> 3) ^ (r & 7)) << 3) + (c & 7));
+    return block * 1024 + inblock;
+}
+
+}  // namespace meshgpu

@@ -1,0 +1,1285 @@
+// Host side of the B200 data plane behind include/mesh_gpu.h.
+//
+//  * KV pool: every instance reserves a virtual range (cuMemAddressReserve)
+//    and maps 2 MiB physical granules from a per-device free list; block b of
+//    the instance lives at va + b * block_bytes, so GROW = map granules (no
+//    copy) and SHRINK = move live blocks above the new high-water mark into
+//    the lowest free slots (batched block-copy kernel), rewrite the block
+//    tables, unmap the tail. Ops are applied physically when ISSUED, so the
+//    physical footprint tracks the control plane's optimistic budget
+//    (memory.cpp:84-104) and every accounted target is backed.
+//  * Block tables: per request, the block ids in position order; new blocks
+//    come from the lowest free index (deterministic).
+//  * Steps run on one compute stream per device (temporal exclusivity of the
+//    reference's node loop, SPEC "one iteration per node at a time"); the
+//    host never waits for a step unless asked (tickets).
+//  * Swap: an evicted request's blocks are copied to pinned host memory on a
+//    side stream; its next prefill step restores them and feeds only the
+//    last token (equivalent to the reference's re-prefill of I+O tokens).
+//  * Migration: peer copy of a request's blocks into another instance.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../../include/mesh_gpu.h"
+#include "decode.cuh"
+#include "prefill.cuh"
+
+using namespace meshgpu;
+
+namespace {
+
+// ------------------------------------------------------------------ errors
+struct MeshError : std::runtime_error {
+    mesh_status code;
+    MeshError(mesh_status c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+#define CK(expr)                                                                                      \
+    do {                                                                                              \
+        cudaError_t _e = (expr);                                                                      \
+        if (_e != cudaSuccess)                                                                        \
+            throw MeshError(MESH_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+    } while (0)
+
+// ------------------------------------------------------- driver VMM entry
+struct Driver {
+    decltype(&cuMemAddressReserve) addr_reserve = nullptr;
+    decltype(&cuMemAddressFree) addr_free = nullptr;
+    decltype(&cuMemCreate) create = nullptr;
+    decltype(&cuMemRelease) release = nullptr;
+    decltype(&cuMemMap) map = nullptr;
+    decltype(&cuMemUnmap) unmap = nullptr;
+    decltype(&cuMemSetAccess) set_access = nullptr;
+    decltype(&cuMemGetAllocationGranularity) granularity = nullptr;
+    bool ok = false;
+};
+Driver& drv() {
+    static Driver d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        auto get = [](const char* name, void** fn) {
+            cudaDriverEntryPointQueryResult q;
+            return cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) == cudaSuccess &&
+                   q == cudaDriverEntryPointSuccess && *fn != nullptr;
+        };
+        d.ok = get("cuMemAddressReserve", (void**)&d.addr_reserve) &&
+               get("cuMemAddressFree", (void**)&d.addr_free) && get("cuMemCreate", (void**)&d.create) &&
+               get("cuMemRelease", (void**)&d.release) && get("cuMemMap", (void**)&d.map) &&
+               get("cuMemUnmap", (void**)&d.unmap) && get("cuMemSetAccess", (void**)&d.set_access) &&
+               get("cuMemGetAllocationGranularity", (void**)&d.granularity);
+    });
+    return d;
+}
+void CU(CUresult r, const char* what) {
+    if (r != CUDA_SUCCESS) throw MeshError(MESH_ERR_CUDA, std::string(what) + " failed: CUresult " + std::to_string(int(r)));
+}
+
+// -------------------------------------------------------------- kernels
+template <int SEL>
+__global__ void init_tiled(uint8_t* dst, Shape s, uint64_t seed, int layer, int N, int K) {
+    // SEL: 0 qkv, 1 o, 2 gu, 3 down, 4 lm
+    size_t total = size_t(N) * K;
+    uint16_t* out = reinterpret_cast<uint16_t*>(dst);
+    const int kbs = K / 64;
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x) {
+        size_t block = e >> 10;
+        int inb = int(e & 1023);
+        int tile = int(block / kbs), kb = int(block % kbs);
+        int r = inb >> 6, cs = inb & 63;
+        int c = ((((cs >> 3) ^ (r & 7))) << 3) + (cs & 7);
+        int prow = tile * 16 + r, col = kb * 64 + c;
+        uint32_t tensor;
+        size_t index;
+        if (SEL == 0) {
+            QkvRow q = qkv_row(s, prow);
+            tensor = q.section == 0 ? T_WQ : (q.section == 1 ? T_WK : T_WV);
+            index = size_t(q.head * s.dh + q.dim) * K + col;
+        } else if (SEL == 1) {
+            tensor = T_WO;
+            index = size_t(prow) * K + col;
+        } else if (SEL == 2) {
+            int up, row;
+            gu_row(prow, &up, &row);
+            tensor = up ? T_WUP : T_WGATE;
+            index = size_t(row) * K + col;
+        } else if (SEL == 3) {
+            tensor = T_WDOWN;
+            index = size_t(prow) * K + col;
+        } else {
+            tensor = s.tied ? T_EMB : T_LM;
+            index = size_t(prow) * K + col;
+        }
+        uint64_t key = tensor_key(seed, tensor, (SEL == 4) ? 0u : uint32_t(layer));
+        out[e] = f_to_bf16(weight_value(key, index));
+    }
+}
+__global__ void init_emb(uint16_t* dst, Shape s, uint64_t seed) {
+    size_t total = size_t(s.vocab) * s.d;
+    uint64_t key = tensor_key(seed, T_EMB, 0);
+    for (size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x; e < total; e += size_t(gridDim.x) * blockDim.x)
+        dst[e] = f_to_bf16(weight_value(key, e));
+}
+__global__ void init_gain(float* dst, int n, uint64_t seed, uint32_t tensor, int layer) {
+    uint64_t key = tensor_key(seed, tensor, uint32_t(layer));
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        dst[i] = gain_value(key, uint64_t(i));
+}
+// Batched block copy within one KV region: pairs[i] = (src block, dst block).
+__global__ void kv_block_copy(uint8_t* base, long long block_bytes, const int2* pairs) {
+    int2 p = pairs[blockIdx.y];
+    const uint4* src = reinterpret_cast<const uint4*>(base + size_t(p.x) * block_bytes);
+    uint4* dst = reinterpret_cast<uint4*>(base + size_t(p.y) * block_bytes);
+    size_t n = size_t(block_bytes) / 16;
+    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
+        dst[i] = src[i];
+}
+__global__ void set_int(int* p, int v) { *p = v; }
+__global__ void read_tiled_row(const uint8_t* W, int K, int prow, float* out) {
+    const uint16_t* w = reinterpret_cast<const uint16_t*>(W);
+    for (int col = threadIdx.x; col < K; col += blockDim.x) out[col] = bf16_to_f(w[tiled_index(prow, col, K)]);
+}
+
+// ----------------------------------------------------------- structures
+constexpr int MAX_SLOTS = 64;  // concurrent requests per instance (batch cap 8 + queued)
+
+struct Granule {
+    CUmemGenericAllocationHandle h;
+};
+
+struct PhysPool {
+    int device = 0;
+    size_t gran = 2u << 20;
+    long long limit = 0;
+    long long mapped = 0;  // granules in use x gran
+    std::vector<CUmemGenericAllocationHandle> free_list;
+    std::vector<CUmemGenericAllocationHandle> all;
+
+    CUmemGenericAllocationHandle take() {
+        if (mapped + (long long)gran > limit)
+            throw MeshError(MESH_ERR_NOMEM, "KV pool exhausted (limit " + std::to_string(limit) + " bytes)");
+        mapped += gran;
+        if (!free_list.empty()) {
+            auto h = free_list.back();
+            free_list.pop_back();
+            return h;
+        }
+        CUmemAllocationProp prop = {};
+        prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop.location.id = device;
+        CUmemGenericAllocationHandle h;
+        CUresult r = drv().create(&h, gran, &prop, 0);
+        if (r != CUDA_SUCCESS) {
+            mapped -= gran;
+            throw MeshError(MESH_ERR_NOMEM, "cuMemCreate failed: " + std::to_string(int(r)));
+        }
+        all.push_back(h);
+        return h;
+    }
+    void give(CUmemGenericAllocationHandle h) {
+        mapped -= gran;
+        free_list.push_back(h);
+    }
+};
+
+struct ReqState {
+    int slot = -1;
+    int ctx = 0;               // tokens whose KV is resident
+    std::vector<int> blocks;   // block ids by position / 16
+    std::vector<int> tokens;   // prompt + generated ids (host history)
+    int pending_tokens = 0;    // emitted on device, not yet copied back
+};
+
+struct SwapEntry {
+    uint64_t shape_key = 0;
+    int ctx = 0;
+    std::vector<int> tokens;
+    void* host = nullptr;  // pinned, ctx rounded up to whole blocks
+    size_t bytes = 0;
+    long long block_bytes = 0;
+    cudaEvent_t done = nullptr;
+};
+
+struct Instance {
+    int64_t id = -1;
+    Shape s{};
+    uint64_t seed = 0;
+    uint64_t shape_key = 0;
+    uint8_t* wmem = nullptr;
+    Weights w{};
+    // KV region
+    CUdeviceptr va = 0;
+    size_t va_size = 0;
+    std::vector<CUmemGenericAllocationHandle> granules;  // mapped, in VA order
+    long long block_bytes = 0;
+    long long target = 0;  // accounted KV bytes (control plane target)
+    int cap_blocks = 0;
+    std::set<int> free_blocks;
+    int live_blocks = 0;
+    // requests
+    std::map<int64_t, ReqState> reqs;
+    std::vector<int> free_slots;
+    int* d_block_table = nullptr;  // [MAX_SLOTS][bt_stride]
+    int bt_stride = 0;
+    int* d_last_tok = nullptr;     // [MAX_SLOTS]
+    std::vector<int> h_block_table;
+};
+
+struct Ticket {
+    int64_t instance = -1;
+    bool prefill = false;
+    std::vector<int64_t> reqs;
+    int ring = -1;
+    cudaEvent_t start = nullptr, kend = nullptr, end = nullptr;
+    bool logits = false;
+    int vocab = 0;
+    bool drained = false;
+    std::vector<int> toks;
+};
+
+constexpr int RING = 64;
+
+}  // namespace
+
+struct mesh_gpu {
+    mesh_gpu_cfg cfg{};
+    std::string err;
+    int sms = 0;
+    cudaStream_t stream = nullptr;   // compute
+    cudaStream_t side = nullptr;     // swap / migration copies
+    PhysPool pool;
+    std::map<int64_t, std::unique_ptr<Instance>> insts;
+    // decode / prefill scratch (sized for the largest registered shape)
+    size_t cap_d = 0, cap_ff = 0, cap_vocab = 0, cap_q = 0, cap_ap = 0, cap_seq = 0;
+    float* h = nullptr;
+    uint16_t* act = nullptr;
+    uint16_t* attn = nullptr;
+    uint16_t* abuf = nullptr;
+    float* q = nullptr;
+    float* ssA = nullptr;
+    float* ssB = nullptr;
+    float* apart = nullptr;
+    int* acnt = nullptr;
+    float* arg_val = nullptr;
+    int* arg_idx = nullptr;
+    int* arg_cnt = nullptr;
+    float* logits = nullptr;
+    unsigned* bar = nullptr;  // [count, gen]
+    // prefill scratch
+    float* p_h = nullptr;
+    uint16_t* p_act = nullptr;
+    float* p_rs = nullptr;
+    float* p_q = nullptr;
+    uint16_t* p_attn = nullptr;
+    uint16_t* p_abuf = nullptr;
+    float* p_logits = nullptr;
+    int* p_tokens = nullptr;
+    int* h_tokens_pinned = nullptr;  // staging for prefill prompt ids
+    // step rings
+    StepDesc* h_desc = nullptr;
+    StepDesc* d_desc = nullptr;
+    int* h_tok = nullptr;   // [RING][8]
+    int* d_tok = nullptr;   // [RING][8]
+    cudaEvent_t ring_ev[RING] = {};
+    bool ring_used[RING] = {};
+    int ring_next = 0;
+    std::map<int64_t, Ticket> tickets;
+    int64_t next_ticket = 1;
+    bool capture_logits = false;
+    mesh_gpu_stats st{};
+};
+
+namespace {
+
+std::map<int64_t, SwapEntry>& swap_store() {
+    static std::map<int64_t, SwapEntry> s;
+    return s;
+}
+
+uint64_t shape_key_of(const Shape& s, uint64_t seed) {
+    uint64_t k = seed;
+    int v[] = {s.n_layers, s.d, s.n_heads, s.n_kv, s.dh, s.ff, s.vocab, s.tied};
+    for (int x : v) k = splitmix64(k ^ uint64_t(x));
+    return k;
+}
+
+void device_guard(mesh_gpu* g) { CK(cudaSetDevice(g->cfg.device)); }
+
+template <typename T>
+void dalloc(T** p, size_t n) {
+    if (*p) CK(cudaFree(*p));
+    *p = nullptr;
+    CK(cudaMalloc((void**)p, std::max<size_t>(n, 1) * sizeof(T)));
+    CK(cudaMemset(*p, 0, std::max<size_t>(n, 1) * sizeof(T)));
+}
+
+void ensure_scratch(mesh_gpu* g, const Shape& s) {
+    size_t nd = std::max(g->cap_d, size_t(s.d)), nff = std::max(g->cap_ff, size_t(s.ff)),
+           nv = std::max(g->cap_vocab, size_t(s.vocab)), nq = std::max(g->cap_q, size_t(s.n_heads) * s.dh),
+           nap = std::max(g->cap_ap, decode_apart_floats(s)), nseq = std::max(g->cap_seq, size_t(s.max_seq));
+    if (g->h && nd == g->cap_d && nff == g->cap_ff && nv == g->cap_vocab && nq == g->cap_q && nap == g->cap_ap &&
+        nseq == g->cap_seq)
+        return;
+    CK(cudaStreamSynchronize(g->stream));
+    g->cap_d = nd;
+    g->cap_ff = nff;
+    g->cap_vocab = nv;
+    g->cap_q = nq;
+    g->cap_ap = nap;
+    g->cap_seq = nseq;
+    dalloc(&g->h, 8 * nd);
+    dalloc(&g->act, 8 * nd);
+    dalloc(&g->attn, 8 * nd);
+    dalloc(&g->abuf, 8 * nff);
+    dalloc(&g->q, 8 * nq);
+    dalloc(&g->ssA, 8 * (nd / 16));
+    dalloc(&g->ssB, 8 * (nd / 16));
+    dalloc(&g->apart, nap);
+    dalloc(&g->acnt, size_t(8) * 64);
+    dalloc(&g->logits, 8 * nv);
+    dalloc(&g->p_h, nseq * nd);
+    dalloc(&g->p_act, nseq * nd);
+    dalloc(&g->p_rs, nseq);
+    dalloc(&g->p_q, nseq * nq);
+    dalloc(&g->p_attn, nseq * nd);
+    dalloc(&g->p_abuf, nseq * nff);
+    dalloc(&g->p_logits, nv);
+    dalloc(&g->p_tokens, nseq);
+    if (g->h_tokens_pinned) CK(cudaFreeHost(g->h_tokens_pinned));
+    CK(cudaHostAlloc((void**)&g->h_tokens_pinned, nseq * sizeof(int), cudaHostAllocDefault));
+}
+
+Instance& inst_of(mesh_gpu* g, int64_t id) {
+    auto it = g->insts.find(id);
+    if (it == g->insts.end()) throw MeshError(MESH_ERR_ARG, "unknown instance " + std::to_string(id));
+    return *it->second;
+}
+
+// ---- KV region management
+int blocks_for_target(const Instance& in, long long target) {
+    if (target <= 0) return 0;
+    long long tokens = target / in.s.kv_bytes_per_token();
+    long long blocks = (tokens + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
+    return int(blocks) + DEC_MAXB;  // one partial tail block per resident request
+}
+
+void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
+    size_t gran = g->pool.gran;
+    size_t want = (bytes + gran - 1) / gran;
+    Driver& d = drv();
+    while (in.granules.size() < want) {
+        size_t off = in.granules.size() * gran;
+        if (off + gran > in.va_size) throw MeshError(MESH_ERR_NOMEM, "instance KV VA range exhausted");
+        CUmemGenericAllocationHandle h = g->pool.take();
+        CU(d.map(in.va + off, gran, 0, h, 0), "cuMemMap");
+        CUmemAccessDesc acc = {};
+        acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc.location.id = g->cfg.device;
+        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+        CU(d.set_access(in.va + off, gran, &acc, 1), "cuMemSetAccess");
+        in.granules.push_back(h);
+    }
+    while (in.granules.size() > want) {
+        size_t off = (in.granules.size() - 1) * gran;
+        CU(d.unmap(in.va + off, gran), "cuMemUnmap");
+        g->pool.give(in.granules.back());
+        in.granules.pop_back();
+    }
+}
+
+void write_bt_entry(Instance& in, int slot, int idx, int block) {
+    in.h_block_table[size_t(slot) * in.bt_stride + idx] = block;
+}
+
+void resize_kv(mesh_gpu* g, Instance& in, long long to) {
+    int new_cap = blocks_for_target(in, to);
+    if (new_cap >= in.cap_blocks) {
+        map_to(g, in, size_t(new_cap) * in.block_bytes);
+        for (int b = in.cap_blocks; b < new_cap; ++b) in.free_blocks.insert(b);
+        in.cap_blocks = new_cap;
+        in.target = to;
+        return;
+    }
+    // shrink: compact live blocks >= new_cap into the lowest free ids < new_cap
+    if (in.live_blocks > new_cap)
+        throw MeshError(MESH_ERR_RUNTIME, "kv shrink below live blocks (" + std::to_string(in.live_blocks) + " > " +
+                                              std::to_string(new_cap) + ")");
+    std::vector<int2> moves;
+    std::set<int> low_free;
+    for (int b : in.free_blocks)
+        if (b < new_cap) low_free.insert(b);
+    for (auto& [rid, r] : in.reqs) {
+        for (size_t i = 0; i < r.blocks.size(); ++i) {
+            int b = r.blocks[i];
+            if (b < new_cap) continue;
+            int dst = *low_free.begin();
+            low_free.erase(low_free.begin());
+            moves.push_back(make_int2(b, dst));
+            r.blocks[i] = dst;
+            write_bt_entry(in, r.slot, int(i), dst);
+        }
+    }
+    if (!moves.empty()) {
+        int2* dpairs = nullptr;
+        CK(cudaMallocAsync((void**)&dpairs, moves.size() * sizeof(int2), g->stream));
+        CK(cudaMemcpyAsync(dpairs, moves.data(), moves.size() * sizeof(int2), cudaMemcpyHostToDevice, g->stream));
+        dim3 grid(std::max(1, int(std::min<long long>(64, in.block_bytes / (16 * 256)))), unsigned(moves.size()));
+        kv_block_copy<<<grid, 256, 0, g->stream>>>(reinterpret_cast<uint8_t*>(in.va), in.block_bytes, dpairs);
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(in.d_block_table, in.h_block_table.data(), in.h_block_table.size() * sizeof(int),
+                           cudaMemcpyHostToDevice, g->stream));
+        CK(cudaFreeAsync(dpairs, g->stream));
+        g->st.blocks_moved += (long long)moves.size();
+        g->st.bytes_moved += 2LL * (long long)moves.size() * in.block_bytes;
+    }
+    // everything that may still touch the tail must finish before unmapping it
+    CK(cudaStreamSynchronize(g->stream));
+    CK(cudaStreamSynchronize(g->side));
+    in.free_blocks = low_free;
+    in.cap_blocks = new_cap;
+    in.target = to;
+    map_to(g, in, size_t(new_cap) * in.block_bytes);
+}
+
+int alloc_block(mesh_gpu* g, Instance& in) {
+    if (in.free_blocks.empty()) {
+        // physical overcommit beyond the accounted target (rounding slack exhausted)
+        int b = in.cap_blocks;
+        map_to(g, in, size_t(b + 1) * in.block_bytes);
+        in.cap_blocks = b + 1;
+        in.live_blocks++;
+        return b;
+    }
+    int b = *in.free_blocks.begin();
+    in.free_blocks.erase(in.free_blocks.begin());
+    in.live_blocks++;
+    return b;
+}
+
+void release_blocks(Instance& in, ReqState& r) {
+    for (int b : r.blocks) {
+        if (b < in.cap_blocks) in.free_blocks.insert(b);
+        in.live_blocks--;
+    }
+    r.blocks.clear();
+    r.ctx = 0;
+}
+
+ReqState& req_slot(Instance& in, int64_t rid) {
+    auto it = in.reqs.find(rid);
+    if (it != in.reqs.end()) return it->second;
+    if (in.free_slots.empty()) throw MeshError(MESH_ERR_NOMEM, "instance request table full");
+    ReqState r;
+    r.slot = in.free_slots.back();
+    in.free_slots.pop_back();
+    return in.reqs.emplace(rid, std::move(r)).first->second;
+}
+
+void free_request(Instance& in, int64_t rid) {
+    auto it = in.reqs.find(rid);
+    if (it == in.reqs.end()) return;
+    release_blocks(in, it->second);
+    in.free_slots.push_back(it->second.slot);
+    in.reqs.erase(it);
+}
+
+// Collect a finished ticket's tokens into the host histories (once).
+void drain_ticket(mesh_gpu* g, Ticket& t) {
+    if (t.drained) return;
+    CK(cudaEventSynchronize(t.end));
+    const int* toks = g->h_tok + t.ring * 8;
+    int n = int(t.reqs.size());
+    auto it = g->insts.find(t.instance);
+    t.toks.assign(toks, toks + n);
+    for (int i = 0; i < n; ++i) {
+        if (it == g->insts.end()) break;
+        auto rit = it->second->reqs.find(t.reqs[i]);
+        if (rit != it->second->reqs.end()) {
+            rit->second.tokens.push_back(toks[i]);
+            rit->second.pending_tokens--;
+        }
+    }
+    float ms = 0.f, kms = 0.f;
+    cudaEventElapsedTime(&ms, t.start, t.end);
+    cudaEventElapsedTime(&kms, t.start, t.kend);
+    g->st.last_step_ms = ms;
+    g->st.last_kernel_ms = kms;
+    g->ring_used[t.ring] = false;
+    t.drained = true;
+}
+
+// Drain every outstanding ticket of an instance up to `upto` (in issue order)
+// so request histories stay in token order.
+void drain_instance(mesh_gpu* g, int64_t inst, int64_t upto = INT64_MAX) {
+    for (auto& [tid, t] : g->tickets) {
+        if (tid > upto) break;
+        if (t.instance == inst) drain_ticket(g, t);
+    }
+}
+
+void flush_request(mesh_gpu* g, int64_t inst, int64_t rid) {
+    (void)rid;
+    drain_instance(g, inst);
+}
+
+void destroy_ticket(Ticket& t) {
+    cudaEventDestroy(t.start);
+    cudaEventDestroy(t.kend);
+    cudaEventDestroy(t.end);
+}
+
+int take_ring(mesh_gpu* g) {
+    for (int k = 0; k < RING; ++k) {
+        int i = (g->ring_next + k) % RING;
+        if (!g->ring_used[i]) {
+            g->ring_next = (i + 1) % RING;
+            // the previous user of this slot may still be copying
+            CK(cudaEventSynchronize(g->ring_ev[i]));
+            g->ring_used[i] = true;
+            return i;
+        }
+    }
+    throw MeshError(MESH_ERR_RUNTIME, "too many outstanding step tickets (wait on older tickets)");
+}
+
+DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
+    DecodeArgs a{};
+    a.s = in.s;
+    a.w = in.w;
+    a.kv_base = reinterpret_cast<uint8_t*>(in.va);
+    a.block_bytes = in.block_bytes;
+    a.block_table = in.d_block_table;
+    a.bt_stride = in.bt_stride;
+    a.last_tok = in.d_last_tok;
+    a.desc = d_desc;
+    a.h = g->h;
+    a.act = g->act;
+    a.attn = g->attn;
+    a.abuf = g->abuf;
+    a.q = g->q;
+    a.ssA = g->ssA;
+    a.ssB = g->ssB;
+    a.apart = g->apart;
+    a.acnt = g->acnt;
+    a.arg_val = g->arg_val;
+    a.arg_idx = g->arg_idx;
+    a.arg_cnt = g->arg_cnt;
+    a.logits = g->capture_logits ? g->logits : nullptr;
+    a.tok_out = g->d_tok + ring * 8;
+    a.bar_count = g->bar;
+    a.bar_gen = g->bar + 1;
+    return a;
+}
+
+int grid_of(mesh_gpu* g) { return g->cfg.sm_quota > 0 ? std::min(g->cfg.sm_quota, g->sms) : g->sms; }
+
+// Build the decode descriptor for `rids` (allocating blocks for new positions).
+void build_decode_desc(mesh_gpu* g, Instance& in, const int64_t* rids, int n, StepDesc& d) {
+    d.B = n;
+    d.n_upd = 0;
+    for (int i = 0; i < n; ++i) {
+        auto it = in.reqs.find(rids[i]);
+        if (it == in.reqs.end() || it->second.ctx == 0)
+            throw MeshError(MESH_ERR_ARG, "decode of request " + std::to_string(rids[i]) + " without prefill");
+        ReqState& r = it->second;
+        if (r.ctx >= in.s.max_seq) throw MeshError(MESH_ERR_ARG, "context exceeds max_seq_len");
+        d.slot[i] = r.slot;
+        d.pos[i] = r.ctx;
+        if (r.ctx % KV_BLOCK_TOKENS == 0) {
+            int b = alloc_block(g, in);
+            r.blocks.push_back(b);
+            write_bt_entry(in, r.slot, int(r.blocks.size()) - 1, b);
+            if (d.n_upd >= MAX_BT_UPDATES) throw MeshError(MESH_ERR_RUNTIME, "too many block-table updates");
+            d.upd[d.n_upd][0] = r.slot;
+            d.upd[d.n_upd][1] = int(r.blocks.size()) - 1;
+            d.upd[d.n_upd][2] = b;
+            d.n_upd++;
+        }
+    }
+}
+
+void launch_decode_step(mesh_gpu* g, Instance& in, const int64_t* rids, int n, Ticket& t) {
+    StepDesc& hd = g->h_desc[t.ring];
+    build_decode_desc(g, in, rids, n, hd);
+    CK(cudaMemcpyAsync(g->d_desc + t.ring, &hd, sizeof(StepDesc), cudaMemcpyHostToDevice, g->stream));
+    CK(cudaEventRecord(t.start, g->stream));
+    DecodeArgs a = decode_args(g, in, g->d_desc + t.ring, t.ring);
+    CK(launch_decode(a, grid_of(g), g->stream));
+    CK(cudaEventRecord(t.kend, g->stream));
+    for (int i = 0; i < n; ++i) {
+        ReqState& r = in.reqs[rids[i]];
+        r.ctx += 1;
+        r.pending_tokens++;
+    }
+    g->st.decode_tokens += n;
+}
+
+void restore_from_swap(mesh_gpu* g, Instance& in, int64_t rid, ReqState& r, SwapEntry& e) {
+    // allocate blocks and scatter the pinned copy back (side stream ordered before compute)
+    int nblk = (e.ctx + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
+    CK(cudaEventSynchronize(e.done));
+    for (int i = 0; i < nblk; ++i) {
+        int b = alloc_block(g, in);
+        r.blocks.push_back(b);
+        write_bt_entry(in, r.slot, i, b);
+        CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(in.va) + size_t(b) * in.block_bytes,
+                           static_cast<uint8_t*>(e.host) + size_t(i) * in.block_bytes, in.block_bytes,
+                           cudaMemcpyHostToDevice, g->stream));
+    }
+    r.ctx = e.ctx;
+    r.tokens = e.tokens;
+    g->st.swap_in_bytes += (long long)nblk * in.block_bytes;
+    CK(cudaFreeHost(e.host));
+    cudaEventDestroy(e.done);
+    swap_store().erase(rid);
+}
+
+void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Ticket& t) {
+    const int64_t rid = p.prefill_request;
+    ReqState& r = req_slot(in, rid);
+    int n = p.prefill_len;
+    if (n < 1 || n > in.s.max_seq) throw MeshError(MESH_ERR_ARG, "prefill_len out of range");
+    flush_request(g, in.id, rid);
+    // a request that was evicted resumes from its parked KV (or at least its history)
+    auto sit = swap_store().find(rid);
+    if (sit != swap_store().end() && r.ctx == 0) {
+        SwapEntry& e = sit->second;
+        if (e.host && e.shape_key == in.shape_key && e.ctx == n - 1) {
+            restore_from_swap(g, in, rid, r, e);
+        } else {
+            r.tokens = e.tokens;
+            if (e.host) CK(cudaFreeHost(e.host));
+            if (e.done) cudaEventDestroy(e.done);
+            swap_store().erase(sit);
+        }
+    }
+    if (r.tokens.empty()) {
+        int I = p.prefill_input_len > 0 ? p.prefill_input_len : n;
+        for (int i = 0; i < I; ++i) r.tokens.push_back(prompt_token(g->cfg.prompt_seed, rid, i, in.s.vocab));
+    }
+    if (int(r.tokens.size()) < n)
+        throw MeshError(MESH_ERR_RUNTIME, "prefill of " + std::to_string(n) + " tokens but history has " +
+                                              std::to_string(r.tokens.size()));
+    int p0, L;
+    if (r.ctx == n - 1 && r.ctx > 0) {  // resume: KV for [0, n-1) resident, feed token n-1
+        p0 = n - 1;
+        L = 1;
+    } else {
+        release_blocks(in, r);  // re-prefill from scratch
+        p0 = 0;
+        L = n;
+    }
+    // blocks for positions [p0, p0 + L)
+    int need = (p0 + L + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
+    while (int(r.blocks.size()) < need) {
+        int b = alloc_block(g, in);
+        r.blocks.push_back(b);
+        write_bt_entry(in, r.slot, int(r.blocks.size()) - 1, b);
+    }
+    // stage the block table row and the tokens
+    CK(cudaMemcpyAsync(in.d_block_table + size_t(r.slot) * in.bt_stride,
+                       in.h_block_table.data() + size_t(r.slot) * in.bt_stride, sizeof(int) * in.bt_stride,
+                       cudaMemcpyHostToDevice, g->stream));
+    // pinned staging is reused per step: wait for the previous prefill's copy
+    CK(cudaStreamSynchronize(g->stream));
+    std::memcpy(g->h_tokens_pinned, r.tokens.data() + p0, sizeof(int) * L);
+    CK(cudaMemcpyAsync(g->p_tokens, g->h_tokens_pinned, sizeof(int) * L, cudaMemcpyHostToDevice, g->stream));
+    PrefillArgs a{};
+    a.s = in.s;
+    a.w = in.w;
+    a.kv_base = reinterpret_cast<uint8_t*>(in.va);
+    a.block_bytes = in.block_bytes;
+    a.bt_row = in.d_block_table + size_t(r.slot) * in.bt_stride;
+    a.slot = r.slot;
+    a.L = L;
+    a.p0 = p0;
+    a.tokens = g->p_tokens;
+    a.h = g->p_h;
+    a.act = g->p_act;
+    a.rs = g->p_rs;
+    a.q = g->p_q;
+    a.attn = g->p_attn;
+    a.abuf = g->p_abuf;
+    a.logits = g->p_logits;
+    a.last_tok = in.d_last_tok;
+    a.tok_out = g->d_tok + t.ring * 8;
+    CK(cudaEventRecord(t.start, g->stream));
+    CK(launch_prefill(a, g->stream));
+    CK(cudaEventRecord(t.kend, g->stream));
+    r.ctx = p0 + L;
+    // history: the prefill consumed tokens[0, n); anything beyond is stale
+    r.tokens.resize(n);
+    r.pending_tokens++;
+    g->st.prefill_tokens += L;
+}
+
+mesh_status fail(mesh_gpu* g, const std::exception& e) {
+    if (auto* me = dynamic_cast<const MeshError*>(&e)) {
+        if (g) g->err = me->what();
+        return me->code;
+    }
+    if (g) g->err = e.what();
+    return MESH_ERR_RUNTIME;
+}
+
+template <typename F>
+mesh_status guarded(mesh_gpu* g, F&& body) {
+    try {
+        if (g) device_guard(g);
+        body();
+        return MESH_OK;
+    } catch (const std::exception& e) {
+        return fail(g, e);
+    }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* mesh_gpu_version(void) { return "0.1.0-sm100a"; }
+
+int32_t mesh_gpu_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) return 0;
+    return n;
+}
+
+const char* mesh_gpu_last_error(const mesh_gpu* g) { return g ? g->err.c_str() : "null mesh_gpu handle"; }
+
+mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
+    if (!cfg || !out) return MESH_ERR_ARG;
+    *out = nullptr;
+    auto g = std::make_unique<mesh_gpu>();
+    g->cfg = *cfg;
+    mesh_status st = guarded(g.get(), [&] {
+        int n = 0;
+        CK(cudaGetDeviceCount(&n));
+        if (cfg->device < 0 || cfg->device >= n) throw MeshError(MESH_ERR_CUDA, "no such CUDA device");
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, cfg->device));
+        if (prop.major != 10)
+            throw MeshError(MESH_ERR_CUDA, std::string("sm_100a kernels need a Blackwell B200, found ") + prop.name);
+        g->sms = prop.multiProcessorCount;
+        if (!drv().ok) throw MeshError(MESH_ERR_CUDA, "CUDA VMM driver entry points unavailable");
+        CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+        g->pool.device = cfg->device;
+        CUmemAllocationProp prop2 = {};
+        prop2.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+        prop2.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        prop2.location.id = cfg->device;
+        size_t gran = 0;
+        CU(drv().granularity(&gran, &prop2, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
+        g->pool.gran = std::max<size_t>(gran, 2u << 20);
+        g->pool.limit = cfg->kv_pool_bytes > 0 ? cfg->kv_pool_bytes : (long long)(prop.totalGlobalMem / 2);
+        dalloc(&g->bar, 2);
+        dalloc(&g->arg_val, size_t(8) * g->sms);
+        dalloc(&g->arg_idx, size_t(8) * g->sms);
+        dalloc(&g->arg_cnt, 1);
+        CK(cudaHostAlloc((void**)&g->h_desc, sizeof(StepDesc) * RING, cudaHostAllocDefault));
+        CK(cudaMalloc((void**)&g->d_desc, sizeof(StepDesc) * RING));
+        CK(cudaHostAlloc((void**)&g->h_tok, sizeof(int) * 8 * RING, cudaHostAllocDefault));
+        CK(cudaMalloc((void**)&g->d_tok, sizeof(int) * 8 * RING));
+        for (int i = 0; i < RING; ++i) CK(cudaEventCreateWithFlags(&g->ring_ev[i], cudaEventDisableTiming));
+        g->st.kv_pool_bytes = g->pool.limit;
+    });
+    if (st != MESH_OK) {
+        // keep the message reachable: hand the handle back only on success
+        static thread_local std::string last;
+        last = g->err;
+        std::fprintf(stderr, "mesh_gpu_open: %s\n", last.c_str());
+        return st;
+    }
+    *out = g.release();
+    return MESH_OK;
+}
+
+void mesh_gpu_close(mesh_gpu* g) {
+    if (!g) return;
+    cudaSetDevice(g->cfg.device);
+    cudaDeviceSynchronize();
+    for (auto& [id, t] : g->tickets) destroy_ticket(t);
+    for (auto& [id, in] : g->insts) {
+        try {
+            map_to(g, *in, 0);
+        } catch (...) {
+        }
+        if (in->va) drv().addr_free(in->va, in->va_size);
+        cudaFree(in->wmem);
+        cudaFree(in->d_block_table);
+        cudaFree(in->d_last_tok);
+    }
+    for (auto h : g->pool.all) drv().release(h);
+    void* dev_ptrs[] = {g->h, g->act, g->attn, g->abuf, g->q, g->ssA, g->ssB, g->apart, g->acnt, g->arg_val,
+                        g->arg_idx, g->arg_cnt, g->logits, g->bar, g->p_h, g->p_act, g->p_rs, g->p_q, g->p_attn,
+                        g->p_abuf, g->p_logits, g->p_tokens, g->d_desc, g->d_tok};
+    for (void* p : dev_ptrs)
+        if (p) cudaFree(p);
+    if (g->h_desc) cudaFreeHost(g->h_desc);
+    if (g->h_tok) cudaFreeHost(g->h_tok);
+    if (g->h_tokens_pinned) cudaFreeHost(g->h_tokens_pinned);
+    for (int i = 0; i < RING; ++i)
+        if (g->ring_ev[i]) cudaEventDestroy(g->ring_ev[i]);
+    if (g->stream) cudaStreamDestroy(g->stream);
+    if (g->side) cudaStreamDestroy(g->side);
+    delete g;
+}
+
+mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mesh_model_shape* sh,
+                                     uint64_t weight_seed) {
+    if (!g || !sh) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        if (g->insts.count(instance_id)) throw MeshError(MESH_ERR_ARG, "duplicate instance id");
+        Shape s{};
+        s.n_layers = sh->n_layers;
+        s.d = sh->d_model;
+        s.n_heads = sh->n_heads;
+        s.n_kv = sh->n_kv_heads;
+        s.dh = sh->d_head;
+        s.ff = sh->d_ff;
+        s.vocab = sh->vocab;
+        s.tied = sh->tied_embeddings;
+        s.max_seq = sh->max_seq_len;
+        s.rope_theta = sh->rope_theta > 0 ? sh->rope_theta : 10000.f;
+        s.eps = sh->rms_eps > 0 ? sh->rms_eps : 1e-5f;
+        if (s.dh != 64 && s.dh != 128) throw MeshError(MESH_ERR_CONFIG, "d_head must be 64 or 128");
+        if (s.n_heads % s.n_kv != 0 || s.gq() > 8) throw MeshError(MESH_ERR_CONFIG, "GQA group must divide and be <= 8");
+        if (s.n_heads * s.dh != s.d) throw MeshError(MESH_ERR_CONFIG, "n_heads * d_head must equal d_model");
+        if (s.d % 256 || s.ff % 256 || s.vocab % 128 || (s.qkv_rows() % 128))
+            throw MeshError(MESH_ERR_CONFIG, "d_model/d_ff must be multiples of 256, vocab of 128");
+        if (s.max_seq < 2 || s.max_seq > ATT_SPLIT * ATT_MAX_SPLITS)
+            throw MeshError(MESH_ERR_CONFIG, "max_seq_len out of range");
+        ensure_scratch(g, s);
+        auto in = std::make_unique<Instance>();
+        in->id = instance_id;
+        in->s = s;
+        in->seed = weight_seed;
+        in->shape_key = shape_key_of(s, weight_seed);
+        const size_t L = s.n_layers;
+        size_t qkv = size_t(s.qkv_rows()) * s.d * 2, o = size_t(s.d) * s.n_heads * s.dh * 2,
+               gu = size_t(2 * s.ff) * s.d * 2, dn = size_t(s.d) * s.ff * 2, lm = size_t(s.vocab) * s.d * 2,
+               emb = size_t(s.vocab) * s.d * 2;
+        size_t norms = (2 * L + 1) * s.d * 4, rope = size_t(s.max_seq) * (s.dh / 2) * 8;
+        size_t total = L * (qkv + o + gu + dn) + lm + emb + norms + rope + 4096;
+        CK(cudaMalloc((void**)&in->wmem, total));
+        uint8_t* p = in->wmem;
+        auto take = [&](size_t n) {
+            uint8_t* r = p;
+            p += (n + 255) & ~size_t(255);
+            return r;
+        };
+        uint8_t* wq = take(L * qkv);
+        uint8_t* wo = take(L * o);
+        uint8_t* wgu = take(L * gu);
+        uint8_t* wdn = take(L * dn);
+        uint8_t* wlm = take(lm);
+        uint16_t* wemb = reinterpret_cast<uint16_t*>(take(emb));
+        float* ga = reinterpret_cast<float*>(take(L * s.d * 4));
+        float* gm = reinterpret_cast<float*>(take(L * s.d * 4));
+        float* gf = reinterpret_cast<float*>(take(size_t(s.d) * 4));
+        float2* rp = reinterpret_cast<float2*>(take(rope));
+        in->w = Weights{wq, wo, wgu, wdn, wlm, wemb, ga, gm, gf, rp, qkv, o, gu, dn};
+        const int blocks = g->sms * 8;
+        for (int l = 0; l < s.n_layers; ++l) {
+            init_tiled<0><<<blocks, 256, 0, g->stream>>>(wq + l * qkv, s, weight_seed, l, s.qkv_rows(), s.d);
+            init_tiled<1><<<blocks, 256, 0, g->stream>>>(wo + l * o, s, weight_seed, l, s.d, s.n_heads * s.dh);
+            init_tiled<2><<<blocks, 256, 0, g->stream>>>(wgu + l * gu, s, weight_seed, l, 2 * s.ff, s.d);
+            init_tiled<3><<<blocks, 256, 0, g->stream>>>(wdn + l * dn, s, weight_seed, l, s.d, s.ff);
+            init_gain<<<32, 256, 0, g->stream>>>(ga + size_t(l) * s.d, s.d, weight_seed, T_GATTN, l);
+            init_gain<<<32, 256, 0, g->stream>>>(gm + size_t(l) * s.d, s.d, weight_seed, T_GMLP, l);
+        }
+        init_tiled<4><<<blocks, 256, 0, g->stream>>>(wlm, s, weight_seed, 0, s.vocab, s.d);
+        init_emb<<<blocks, 256, 0, g->stream>>>(wemb, s, weight_seed);
+        init_gain<<<32, 256, 0, g->stream>>>(gf, s.d, weight_seed, T_GFINAL, 0);
+        CK(cudaGetLastError());
+        // rotate-half RoPE table, computed in double on the host (the oracle uses the same formula)
+        std::vector<float2> tab(size_t(s.max_seq) * (s.dh / 2));
+        for (int pos = 0; pos < s.max_seq; ++pos)
+            for (int i = 0; i < s.dh / 2; ++i) {
+                double inv = std::pow(double(s.rope_theta), -2.0 * i / double(s.dh));
+                double ang = double(pos) * inv;
+                tab[size_t(pos) * (s.dh / 2) + i] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+            }
+        CK(cudaMemcpyAsync(rp, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, g->stream));
+        // KV region: reserve the whole pool's worth of VA
+        in->block_bytes = (long long)KV_BLOCK_TOKENS * s.kv_bytes_per_token();
+        size_t gran = g->pool.gran;
+        in->va_size = ((size_t(g->pool.limit) + size_t(in->block_bytes) * (DEC_MAXB + 2)) / gran + 1) * gran;
+        CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
+        in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
+        in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
+        CK(cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()));
+        CK(cudaMemsetAsync(in->d_block_table, 0, sizeof(int) * in->h_block_table.size(), g->stream));
+        CK(cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS));
+        CK(cudaMemsetAsync(in->d_last_tok, 0, sizeof(int) * MAX_SLOTS, g->stream));
+        for (int i = MAX_SLOTS - 1; i >= 0; --i) in->free_slots.push_back(i);
+        CK(cudaStreamSynchronize(g->stream));
+        g->insts.emplace(instance_id, std::move(in));
+    });
+}
+
+mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        CK(cudaStreamSynchronize(g->stream));
+        CK(cudaStreamSynchronize(g->side));
+        map_to(g, in, 0);
+        CU(drv().addr_free(in.va, in.va_size), "cuMemAddressFree");
+        CK(cudaFree(in.wmem));
+        CK(cudaFree(in.d_block_table));
+        CK(cudaFree(in.d_last_tok));
+        std::vector<int64_t> dead;
+        for (auto& [tid, t] : g->tickets)
+            if (t.instance == instance_id) dead.push_back(tid);
+        for (int64_t tid : dead) {
+            Ticket& t = g->tickets[tid];
+            g->ring_used[t.ring] = false;
+            destroy_ticket(t);
+            g->tickets.erase(tid);
+        }
+        g->insts.erase(instance_id);
+    });
+}
+
+mesh_status mesh_gpu_kv_resize(mesh_gpu* g, int64_t instance_id, int64_t from_bytes, int64_t to_bytes) {
+    if (!g || from_bytes < 0 || to_bytes < 0) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        if (from_bytes != in.target)
+            throw MeshError(MESH_ERR_ARG, "kv_resize: from (" + std::to_string(from_bytes) +
+                                              ") does not match current target (" + std::to_string(in.target) + ")");
+        resize_kv(g, in, to_bytes);
+        g->st.kv_mapped_bytes = g->pool.mapped;
+    });
+}
+
+mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan* plan, int64_t* ticket) {
+    if (!g || !plan || !ticket) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        Ticket t;
+        t.instance = instance_id;
+        t.prefill = plan->is_prefill != 0;
+        t.logits = g->capture_logits;
+        t.vocab = in.s.vocab;
+        t.ring = take_ring(g);
+        CK(cudaEventCreate(&t.start));
+        CK(cudaEventCreate(&t.kend));
+        CK(cudaEventCreate(&t.end));
+        try {
+            if (t.prefill) {
+                t.reqs.push_back(plan->prefill_request);
+                launch_prefill_step(g, in, *plan, t);
+            } else {
+                if (plan->n_decode < 1 || plan->n_decode > DEC_MAXB || !plan->decode_requests)
+                    throw MeshError(MESH_ERR_ARG, "decode batch must hold 1..8 requests");
+                t.reqs.assign(plan->decode_requests, plan->decode_requests + plan->n_decode);
+                launch_decode_step(g, in, plan->decode_requests, plan->n_decode, t);
+            }
+        } catch (...) {
+            g->ring_used[t.ring] = false;
+            destroy_ticket(t);
+            throw;
+        }
+        CK(cudaMemcpyAsync(g->h_tok + t.ring * 8, g->d_tok + t.ring * 8, sizeof(int) * 8, cudaMemcpyDeviceToHost,
+                           g->stream));
+        CK(cudaEventRecord(t.end, g->stream));
+        CK(cudaEventRecord(g->ring_ev[t.ring], g->stream));
+        g->st.steps++;
+        *ticket = g->next_ticket++;
+        g->tickets.emplace(*ticket, std::move(t));
+    });
+}
+
+mesh_status mesh_gpu_step_wait(mesh_gpu* g, int64_t ticket, int32_t* tokens_out, int32_t cap, int32_t* n_out,
+                               float* logits_out, int64_t logits_cap) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        auto it = g->tickets.find(ticket);
+        if (it == g->tickets.end()) throw MeshError(MESH_ERR_ARG, "unknown or already-waited ticket");
+        Ticket& t = it->second;
+        drain_instance(g, t.instance, ticket);
+        int n = int(t.toks.size());
+        for (int i = 0; i < n && tokens_out && i < cap; ++i) tokens_out[i] = t.toks[i];
+        if (n_out) *n_out = n;
+        if (logits_out) {
+            if (!t.logits) throw MeshError(MESH_ERR_ARG, "logits capture was off for this step");
+            // valid only for the most recent step (scratch is reused)
+            size_t cnt = t.prefill ? size_t(t.vocab) : t.reqs.size() * size_t(t.vocab);
+            if ((int64_t)cnt > logits_cap) throw MeshError(MESH_ERR_ARG, "logits buffer too small");
+            CK(cudaMemcpy(logits_out, t.prefill ? g->p_logits : g->logits, cnt * sizeof(float),
+                          cudaMemcpyDeviceToHost));
+        }
+        destroy_ticket(t);
+        g->tickets.erase(it);
+    });
+}
+
+mesh_status mesh_gpu_set_capture_logits(mesh_gpu* g, int32_t enable) {
+    if (!g) return MESH_ERR_ARG;
+    g->capture_logits = enable != 0;
+    return MESH_OK;
+}
+
+mesh_status mesh_gpu_request_free(mesh_gpu* g, int64_t instance_id, int64_t request_id) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        flush_request(g, instance_id, request_id);
+        free_request(in, request_id);
+    });
+}
+
+mesh_status mesh_gpu_swap_out(mesh_gpu* g, int64_t instance_id, int64_t request_id) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        auto it = in.reqs.find(request_id);
+        if (it == in.reqs.end()) throw MeshError(MESH_ERR_ARG, "swap_out: request not resident");
+        flush_request(g, instance_id, request_id);
+        ReqState& r = it->second;
+        SwapEntry e;
+        e.shape_key = in.shape_key;
+        e.tokens = r.tokens;
+        if (r.ctx > 0) {
+            e.ctx = r.ctx;
+            e.block_bytes = in.block_bytes;
+            e.bytes = r.blocks.size() * size_t(in.block_bytes);
+            CK(cudaHostAlloc(&e.host, e.bytes, cudaHostAllocPortable));
+            // order after every step that wrote this request's KV
+            cudaEvent_t ready;
+            CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+            CK(cudaEventRecord(ready, g->stream));
+            CK(cudaStreamWaitEvent(g->side, ready, 0));
+            cudaEventDestroy(ready);
+            for (size_t i = 0; i < r.blocks.size(); ++i)
+                CK(cudaMemcpyAsync(static_cast<uint8_t*>(e.host) + i * in.block_bytes,
+                                   reinterpret_cast<uint8_t*>(in.va) + size_t(r.blocks[i]) * in.block_bytes,
+                                   in.block_bytes, cudaMemcpyDeviceToHost, g->side));
+            CK(cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming));
+            CK(cudaEventRecord(e.done, g->side));
+            // the blocks return to the free list only after the copy drains
+            CK(cudaEventSynchronize(e.done));
+            g->st.swap_out_bytes += (long long)e.bytes;
+        }
+        auto& store = swap_store();
+        auto old = store.find(request_id);
+        if (old != store.end()) {
+            if (old->second.host) cudaFreeHost(old->second.host);
+            if (old->second.done) cudaEventDestroy(old->second.done);
+            store.erase(old);
+        }
+        store.emplace(request_id, std::move(e));
+        free_request(in, request_id);
+    });
+}
+
+mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst, int64_t dst_instance,
+                             int64_t request_id) {
+    if (!src || !dst) return MESH_ERR_ARG;
+    return guarded(dst, [&] {
+        CK(cudaSetDevice(src->cfg.device));
+        Instance& si = inst_of(src, src_instance);
+        auto it = si.reqs.find(request_id);
+        if (it == si.reqs.end()) throw MeshError(MESH_ERR_ARG, "migrate: request not resident at source");
+        flush_request(src, src_instance, request_id);
+        CK(cudaStreamSynchronize(src->stream));
+        CK(cudaSetDevice(dst->cfg.device));
+        Instance& di = inst_of(dst, dst_instance);
+        if (di.shape_key != si.shape_key) throw MeshError(MESH_ERR_ARG, "migrate: instances serve different models");
+        ReqState& sr = it->second;
+        if (di.reqs.count(request_id)) throw MeshError(MESH_ERR_ARG, "migrate: request already at destination");
+        ReqState& dr = req_slot(di, request_id);
+        dr.tokens = sr.tokens;
+        dr.ctx = sr.ctx;
+        for (size_t i = 0; i < sr.blocks.size(); ++i) {
+            int b = alloc_block(dst, di);
+            dr.blocks.push_back(b);
+            write_bt_entry(di, dr.slot, int(i), b);
+            void* dptr = reinterpret_cast<uint8_t*>(di.va) + size_t(b) * di.block_bytes;
+            const void* sptr = reinterpret_cast<uint8_t*>(si.va) + size_t(sr.blocks[i]) * si.block_bytes;
+            if (src->cfg.device == dst->cfg.device)
+                CK(cudaMemcpyAsync(dptr, sptr, di.block_bytes, cudaMemcpyDeviceToDevice, dst->stream));
+            else
+                CK(cudaMemcpyPeerAsync(dptr, dst->cfg.device, sptr, src->cfg.device, di.block_bytes, dst->stream));
+        }
+        // the device-side last token travels with the request
+        int last = sr.tokens.empty() ? 0 : sr.tokens.back();
+        set_int<<<1, 1, 0, dst->stream>>>(di.d_last_tok + dr.slot, last);
+        CK(cudaMemcpyAsync(di.d_block_table + size_t(dr.slot) * di.bt_stride,
+                           di.h_block_table.data() + size_t(dr.slot) * di.bt_stride, sizeof(int) * di.bt_stride,
+                           cudaMemcpyHostToDevice, dst->stream));
+        CK(cudaStreamSynchronize(dst->stream));
+        dst->st.migrate_bytes += (long long)sr.blocks.size() * di.block_bytes;
+        CK(cudaSetDevice(src->cfg.device));
+        free_request(si, request_id);
+        CK(cudaSetDevice(dst->cfg.device));
+    });
+}
+
+mesh_status mesh_gpu_request_info(mesh_gpu* g, int64_t instance_id, int64_t request_id, int32_t* ctx_len,
+                                  int32_t* blocks, int32_t* block_ids, int32_t cap) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        auto it = in.reqs.find(request_id);
+        if (it == in.reqs.end()) throw MeshError(MESH_ERR_ARG, "request not resident");
+        if (ctx_len) *ctx_len = it->second.ctx;
+        if (blocks) *blocks = int(it->second.blocks.size());
+        if (block_ids)
+            for (int i = 0; i < std::min<int>(cap, int(it->second.blocks.size())); ++i) block_ids[i] = it->second.blocks[i];
+    });
+}
+
+mesh_status mesh_gpu_request_tokens(mesh_gpu* g, int64_t instance_id, int64_t request_id, int32_t* tokens, int32_t cap,
+                                    int32_t* n_out) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        flush_request(g, instance_id, request_id);
+        auto it = in.reqs.find(request_id);
+        const std::vector<int>* src = nullptr;
+        if (it != in.reqs.end())
+            src = &it->second.tokens;
+        else {
+            auto sit = swap_store().find(request_id);
+            if (sit == swap_store().end()) throw MeshError(MESH_ERR_ARG, "unknown request");
+            src = &sit->second.tokens;
+        }
+        int n = int(src->size());
+        for (int i = 0; i < std::min(n, cap); ++i) tokens[i] = (*src)[i];
+        if (n_out) *n_out = n;
+    });
+}
+
+mesh_status mesh_gpu_instance_kv(mesh_gpu* g, int64_t instance_id, int64_t* target_bytes, int64_t* mapped_bytes,
+                                 int32_t* capacity_blocks, int32_t* live_blocks) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        if (target_bytes) *target_bytes = in.target;
+        if (mapped_bytes) *mapped_bytes = (int64_t)in.granules.size() * (int64_t)g->pool.gran;
+        if (capacity_blocks) *capacity_blocks = in.cap_blocks;
+        if (live_blocks) *live_blocks = in.live_blocks;
+    });
+}
+
+mesh_status mesh_gpu_read_weight(mesh_gpu* g, int64_t instance_id, int32_t tensor, int32_t layer, int32_t row,
+                                 float* out, int32_t n) {
+    if (!g || !out) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        const Shape& s = in.s;
+        // locate the physical row that holds logical (tensor, row)
+        const uint8_t* W = nullptr;
+        int K = 0, prow = -1;
+        if (tensor == T_WQ || tensor == T_WK || tensor == T_WV) {
+            W = in.w.qkv + size_t(layer) * in.w.qkv_layer;
+            K = s.d;
+            for (int p = 0; p < s.qkv_rows() && prow < 0; ++p) {
+                QkvRow q = qkv_row(s, p);
+                int sec = tensor == T_WQ ? 0 : (tensor == T_WK ? 1 : 2);
+                if (q.section == sec && q.head * s.dh + q.dim == row) prow = p;
+            }
+        } else if (tensor == T_WO) {
+            W = in.w.o + size_t(layer) * in.w.o_layer;
+            K = s.n_heads * s.dh;
+            prow = row;
+        } else if (tensor == T_WGATE || tensor == T_WUP) {
+            W = in.w.gu + size_t(layer) * in.w.gu_layer;
+            K = s.d;
+            prow = (row / 8) * 16 + (row % 8) + (tensor == T_WUP ? 8 : 0);
+        } else if (tensor == T_WDOWN) {
+            W = in.w.down + size_t(layer) * in.w.down_layer;
+            K = s.ff;
+            prow = row;
+        } else if (tensor == T_LM) {
+            W = in.w.lm;
+            K = s.d;
+            prow = row;
+        } else {
+            throw MeshError(MESH_ERR_ARG, "read_weight: unsupported tensor");
+        }
+        if (prow < 0 || n < K) throw MeshError(MESH_ERR_ARG, "read_weight: bad row or buffer");
+        float* d = nullptr;
+        CK(cudaMalloc((void**)&d, sizeof(float) * K));
+        read_tiled_row<<<1, 256, 0, g->stream>>>(W, K, prow, d);
+        CK(cudaMemcpyAsync(out, d, sizeof(float) * K, cudaMemcpyDeviceToHost, g->stream));
+        CK(cudaStreamSynchronize(g->stream));
+        CK(cudaFree(d));
+    });
+}
+
+mesh_status mesh_gpu_stats_get(mesh_gpu* g, mesh_gpu_stats* out) {
+    if (!g || !out) return MESH_ERR_ARG;
+    g->st.kv_mapped_bytes = g->pool.mapped;
+    *out = g->st;
+    return MESH_OK;
+}
+
+mesh_status mesh_gpu_sync(mesh_gpu* g) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        CK(cudaStreamSynchronize(g->stream));
+        CK(cudaStreamSynchronize(g->side));
+    });
+}
+
+mesh_status mesh_gpu_bench_decode(mesh_gpu* g, int64_t instance_id, const mesh_step_plan* plan, int32_t iters,
+                                  double* ms_per_step) {
+    if (!g || !plan || !ms_per_step || iters < 1) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        if (plan->n_decode < 1 || plan->n_decode > DEC_MAXB) throw MeshError(MESH_ERR_ARG, "bad batch");
+        // fixed positions: every iteration re-decodes the same positions (no state advance)
+        StepDesc hd{};
+        hd.B = plan->n_decode;
+        for (int i = 0; i < hd.B; ++i) {
+            ReqState& r = in.reqs.at(plan->decode_requests[i]);
+            if (r.ctx < 1) throw MeshError(MESH_ERR_ARG, "bench_decode needs prefilled requests");
+            hd.slot[i] = r.slot;
+            hd.pos[i] = r.ctx - 1;  // rewrite the last resident position: no new blocks needed
+        }
+        StepDesc* dd = nullptr;
+        int* scratch_tok = nullptr;
+        CK(cudaMalloc((void**)&dd, sizeof(StepDesc)));
+        CK(cudaMalloc((void**)&scratch_tok, sizeof(int) * MAX_SLOTS));
+        CK(cudaMemcpy(dd, &hd, sizeof(StepDesc), cudaMemcpyHostToDevice));
+        CK(cudaMemcpy(scratch_tok, in.d_last_tok, sizeof(int) * MAX_SLOTS, cudaMemcpyDeviceToDevice));
+        int ring = take_ring(g);
+        DecodeArgs a = decode_args(g, in, dd, ring);
+        a.last_tok = scratch_tok;
+        a.logits = nullptr;
+        cudaEvent_t e0, e1;
+        CK(cudaEventCreate(&e0));
+        CK(cudaEventCreate(&e1));
+        CK(launch_decode(a, grid_of(g), g->stream));  // warm
+        CK(cudaEventRecord(e0, g->stream));
+        for (int i = 0; i < iters; ++i) CK(launch_decode(a, grid_of(g), g->stream));
+        CK(cudaEventRecord(e1, g->stream));
+        CK(cudaEventSynchronize(e1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, e0, e1));
+        *ms_per_step = double(ms) / iters;
+        g->ring_used[ring] = false;
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+        CK(cudaFree(dd));
+        CK(cudaFree(scratch_tok));
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Model description shared by the decode/prefill kernels and the host-side
+// data plane: Llama-family shapes, the deterministic weight generator, the
+// physical row permutations applied when weights are tiled, and the paged KV
+// block layout. The CPU oracle (oracle/llama_ref.c) restates the generator.
+#pragma once
+
+#include <stddef.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace meshgpu {
+
+struct Shape {
+    int n_layers, d, n_heads, n_kv, dh, ff, vocab;
+    int tied;          // lm_head == embedding (Llama-3.2-3B)
+    float rope_theta;  // rotate-half RoPE base
+    float eps;         // RMSNorm epsilon
+    int max_seq;       // longest context the instance serves (rope table rows)
+    __host__ __device__ int gq() const { return n_heads / n_kv; }
+    __host__ __device__ int qkv_rows() const { return (n_heads + 2 * n_kv) * dh; }
+    __host__ __device__ long long kv_bytes_per_token() const { return 2LL * n_layers * n_kv * dh * 2; }
+};
+
+// Tensor ids of the generator (part of the weight contract with the oracle).
+enum TensorId : uint32_t {
+    T_EMB = 0, T_WQ = 1, T_WK = 2, T_WV = 3, T_WO = 4, T_WGATE = 5, T_WUP = 6, T_WDOWN = 7,
+    T_LM = 8, T_GATTN = 9, T_GMLP = 10, T_GFINAL = 11,
+};
+
+__host__ __device__ inline uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ inline uint64_t tensor_key(uint64_t seed, uint32_t tensor, uint32_t layer) {
+    return splitmix64(seed ^ (uint64_t(tensor) << 56) ^ (uint64_t(layer) << 40) ^ 0x5eedull);
+}
+// Signed 24-bit integer drawn from the element's hash.
+__host__ __device__ inline int32_t elem_i24(uint64_t tkey, uint64_t index) {
+    return int32_t(splitmix64(tkey + index) >> 40) - (1 << 23);
+}
+// Weights: uniform on [-2^-5, 2^-5) (std 0.018), exact in fp32 before the bf16 rounding.
+__host__ __device__ inline float weight_value(uint64_t tkey, uint64_t index) {
+    return float(elem_i24(tkey, index)) * (1.0f / 268435456.0f);  // 2^-28
+}
+// RMSNorm gains: 1 + uniform on [-2^-4, 2^-4).
+__host__ __device__ inline float gain_value(uint64_t tkey, uint64_t index) {
+    return 1.0f + float(elem_i24(tkey, index)) * (1.0f / 134217728.0f);  // 2^-27
+}
+// Synthetic prompt ids, keyed (seed, request id, position).
+__host__ __device__ inline int prompt_token(uint64_t seed, int64_t request, int pos, int vocab) {
+    uint64_t h = splitmix64(splitmix64(seed ^ 0x70726f6d7074ull) + uint64_t(request) * 0x100000001b3ull +
+                            uint64_t(pos));
+    return int(h % uint64_t(vocab));
+}
+
+// ---- physical row maps of the fused/permuted matrices (tile = 16 rows) ----
+// QKV: sections q (n_heads), k (n_kv), v (n_kv); within a head, tile j holds
+// dims [8j, 8j+8) in rows 0-7 and [8j+dh/2, 8j+dh/2+8) in rows 8-15 so every
+// rotate-half RoPE pair lands in one thread's mma accumulator (rows g, g+8).
+struct QkvRow {
+    int section;  // 0 q, 1 k, 2 v
+    int head;
+    int dim;
+};
+__host__ __device__ inline QkvRow qkv_row(const Shape& s, int prow) {
+    int tiles_per_head = s.dh / 16;
+    int tile = prow >> 4, r = prow & 15;
+    int head_global = tile / tiles_per_head, j = tile % tiles_per_head;
+    QkvRow out;
+    if (head_global < s.n_heads) {
+        out.section = 0;
+        out.head = head_global;
+    } else if (head_global < s.n_heads + s.n_kv) {
+        out.section = 1;
+        out.head = head_global - s.n_heads;
+    } else {
+        out.section = 2;
+        out.head = head_global - s.n_heads - s.n_kv;
+    }
+    out.dim = (r < 8) ? (8 * j + r) : (8 * j + (r - 8) + s.dh / 2);
+    return out;
+}
+// Gate/up: tile j holds gate rows [8j, 8j+8) in rows 0-7 and the matching up
+// rows in rows 8-15, so silu(gate) * up is formed in registers.
+__host__ __device__ inline void gu_row(int prow, int* is_up, int* row) {
+    int tile = prow >> 4, r = prow & 15;
+    *is_up = r >= 8;
+    *row = 8 * tile + (r & 7);
+}
+
+// ---- paged KV block layout ----
+// A block holds KV_BLOCK_TOKENS tokens of every layer: [layer][k|v][kv_head][slot][dh] bf16.
+constexpr int KV_BLOCK_TOKENS = 16;
+__host__ __device__ inline size_t kv_offset(const Shape& s, int layer, int kv, int head, int slot) {
+    return ((((size_t(layer) * 2 + kv) * s.n_kv + head) * KV_BLOCK_TOKENS + slot) * s.dh) * 2;
+}
+
+// ---- device view of one instance's weights ----
+struct Weights {
+    const uint8_t* qkv;    // [L] tiled [qkv_rows][d]
+    const uint8_t* o;      // [L] tiled [d][H*dh]
+    const uint8_t* gu;     // [L] tiled [2ff][d]
+    const uint8_t* down;   // [L] tiled [d][ff]
+    const uint8_t* lm;     // tiled [V][d]
+    const uint16_t* emb;   // row-major [V][d] bf16
+    const float* g_attn;   // [L][d]
+    const float* g_mlp;    // [L][d]
+    const float* g_final;  // [d]
+    const float2* rope;    // [max_seq][dh/2] (cos, sin)
+    size_t qkv_layer, o_layer, gu_layer, down_layer;  // bytes per layer
+};
+
+}  // namespace meshgpu

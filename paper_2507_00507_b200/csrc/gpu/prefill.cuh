@@ -1,0 +1,33 @@
+// Prefill step: one request, L tokens (SURVEY 8a row a-new-2, plan_for
+// prefill branch compute.cpp:104-115).
+#pragma once
+
+#include "model.cuh"
+
+namespace meshgpu {
+
+struct PrefillArgs {
+    Shape s;
+    Weights w;
+    uint8_t* kv_base;
+    long long block_bytes;
+    const int* bt_row;  // block table row of the request (device)
+    int slot;
+    int L;              // tokens in this pass
+    int p0;             // absolute position of the first token
+    const int* tokens;  // [L] device
+    // scratch sized for max_seq tokens
+    float* h;           // [L][d]
+    uint16_t* act;      // [L][d]
+    float* rs;          // [L]
+    float* q;           // [L][H][dh]
+    uint16_t* attn;     // [L][d]
+    uint16_t* abuf;     // [L][ff]
+    float* logits;      // [vocab] (last token)
+    int* last_tok;      // instance request table
+    int* tok_out;       // [1]
+};
+
+cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t stream);
+
+}  // namespace meshgpu

@@ -1,0 +1,197 @@
+#include "gpu_executor.hpp"
+
+#include <dlfcn.h>
+
+#include <cstring>
+
+#include "../../../include/mesh_gpu.h"
+
+namespace mesh {
+
+const LlamaShape& llama_shape_for(const std::string& sc) {
+    static const std::map<std::string, LlamaShape> shapes = {
+        {"1b", {22, 2048, 32, 4, 64, 5632, 32000, 0, 2048, 10000.f, 1e-5f}},     // TinyLlama-1.1B
+        {"3b", {28, 3072, 24, 8, 128, 8192, 128256, 1, 4096, 500000.f, 1e-5f}},  // Llama-3.2-3B
+        {"7b", {32, 4096, 32, 32, 128, 11008, 32000, 0, 4096, 10000.f, 1e-5f}},  // Llama-2-7B
+        {"13b", {40, 5120, 40, 40, 128, 13824, 32000, 0, 4096, 10000.f, 1e-5f}}, // Llama-2-13B
+        {"tiny", {2, 256, 4, 2, 64, 512, 512, 0, 512, 10000.f, 1e-5f}},          // tests
+    };
+    auto it = shapes.find(sc);
+    if (it == shapes.end()) throw ConfigError("no Llama shape for size class `" + sc + "` on the GPU data plane");
+    return it->second;
+}
+
+struct GpuExecutor::Api {
+    decltype(&mesh_gpu_open) open;
+    decltype(&mesh_gpu_close) close;
+    decltype(&mesh_gpu_last_error) last_error;
+    decltype(&mesh_gpu_instance_create) instance_create;
+    decltype(&mesh_gpu_instance_destroy) instance_destroy;
+    decltype(&mesh_gpu_kv_resize) kv_resize;
+    decltype(&mesh_gpu_step) step;
+    decltype(&mesh_gpu_step_wait) step_wait;
+    decltype(&mesh_gpu_request_free) request_free;
+    decltype(&mesh_gpu_swap_out) swap_out;
+    decltype(&mesh_gpu_stats_get) stats_get;
+};
+
+namespace {
+uint64_t weight_seed(const std::string& model_id) {  // every instance of a model is the same replica
+    uint64_t h = 1469598103934665603ULL;
+    for (unsigned char ch : model_id) {
+        h ^= ch;
+        h *= 1099511628211ULL;
+    }
+    return h;
+}
+}  // namespace
+
+GpuExecutor::GpuExecutor(const std::string& lib_path, std::vector<int> devices, long long kv_pool_bytes)
+    : devices_(std::move(devices)), pool_bytes_(kv_pool_bytes) {
+    if (devices_.empty()) throw ConfigError("attach_gpu: no devices given");
+    dl_ = dlopen(lib_path.c_str(), RTLD_NOW | RTLD_LOCAL);
+    if (!dl_) throw SimError(std::string("attach_gpu: cannot load ") + lib_path + ": " + dlerror());
+    api_ = new Api();
+    auto sym = [&](const char* n) {
+        void* p = dlsym(dl_, n);
+        if (!p) throw SimError(std::string("attach_gpu: missing symbol ") + n);
+        return p;
+    };
+#define BIND(field, name) api_->field = reinterpret_cast<decltype(api_->field)>(sym(name))
+    BIND(open, "mesh_gpu_open");
+    BIND(close, "mesh_gpu_close");
+    BIND(last_error, "mesh_gpu_last_error");
+    BIND(instance_create, "mesh_gpu_instance_create");
+    BIND(instance_destroy, "mesh_gpu_instance_destroy");
+    BIND(kv_resize, "mesh_gpu_kv_resize");
+    BIND(step, "mesh_gpu_step");
+    BIND(step_wait, "mesh_gpu_step_wait");
+    BIND(request_free, "mesh_gpu_request_free");
+    BIND(swap_out, "mesh_gpu_swap_out");
+    BIND(stats_get, "mesh_gpu_stats_get");
+#undef BIND
+    for (int dev : devices_) {
+        mesh_gpu_cfg cfg{};
+        cfg.device = dev;
+        cfg.sm_quota = 0;
+        cfg.kv_pool_bytes = pool_bytes_;
+        cfg.prompt_seed = 1234;
+        mesh_gpu* h = nullptr;
+        if (api_->open(&cfg, &h) != MESH_OK) throw SimError("attach_gpu: mesh_gpu_open failed on device " + std::to_string(dev));
+        handles_.push_back(h);
+    }
+}
+
+GpuExecutor::~GpuExecutor() {
+    if (api_)
+        for (mesh_gpu* h : handles_) api_->close(h);
+    delete api_;
+    if (dl_) dlclose(dl_);
+}
+
+void GpuExecutor::check(mesh_gpu* h, int status, const char* what) {
+    if (status != MESH_OK) throw SimError(std::string("gpu data plane: ") + what + ": " + api_->last_error(h));
+}
+
+mesh_gpu* GpuExecutor::handle_for_node(NodeId node) {
+    return handles_[static_cast<std::size_t>(node) % handles_.size()];
+}
+
+void GpuExecutor::instance_start(const Cluster&, const Instance& inst) {
+    const LlamaShape& L = llama_shape_for(inst.model->size_class);
+    mesh_model_shape s{L.n_layers, L.d_model, L.n_heads, L.n_kv_heads, L.d_head, L.d_ff, L.vocab, L.tied,
+                       std::min(L.max_seq_len, inst.model->max_seq_len), L.rope_theta, L.rms_eps};
+    mesh_gpu* h = handle_for_node(inst.node_id);
+    inst_dev_[inst.id] = static_cast<int>(static_cast<std::size_t>(inst.node_id) % handles_.size());
+    check(h, api_->instance_create(h, inst.id, &s, weight_seed(inst.model->model_id)), "instance_create");
+}
+
+void GpuExecutor::kv_issue(const Cluster&, const Instance& inst, const ScaleOp& op) {
+    mesh_gpu* h = handle_for_node(inst.node_id);
+    check(h, api_->kv_resize(h, inst.id, op.from_bytes, op.to_bytes), "kv_resize");
+}
+
+void GpuExecutor::iteration_start(const Cluster& c, const Node& nd, const Instance& inst, const IterationPlan& p) {
+    mesh_gpu* h = handle_for_node(nd.id);
+    std::vector<long long>& tk = tickets_[nd.id];
+    if (p.is_prefill) {
+        const Request& r = c.requests().get(p.prefill_request);
+        mesh_step_plan sp{1, p.prefill_request, p.kind.input_len, r.input_len, 0, nullptr};
+        int64_t t = 0;
+        check(h, api_->step(h, inst.id, &sp, &t), "prefill step");
+        tk.push_back(t);
+        prefill_tokens_ += p.kind.input_len;
+        return;
+    }
+    std::vector<int64_t> rids;
+    for (RequestId rid : inst.batch)
+        if (c.requests().get(rid).prefill_done) rids.push_back(rid);
+    for (std::size_t o = 0; o < rids.size(); o += 8) {  // the decode kernel takes <= 8 columns
+        const int n = static_cast<int>(std::min<std::size_t>(8, rids.size() - o));
+        mesh_step_plan sp{0, -1, 0, 0, n, rids.data() + o};
+        int64_t t = 0;
+        check(h, api_->step(h, inst.id, &sp, &t), "decode step");
+        tk.push_back(t);
+    }
+    decode_tokens_ += static_cast<long long>(rids.size());
+}
+
+void GpuExecutor::iteration_done(const Cluster&, const Node& nd, const IterationPlan&, const IterationOutcome&) {
+    mesh_gpu* h = handle_for_node(nd.id);
+    auto it = tickets_.find(nd.id);
+    if (it == tickets_.end()) return;
+    for (long long t : it->second) {
+        int32_t toks[8];
+        int32_t n = 0;
+        check(h, api_->step_wait(h, t, toks, 8, &n, nullptr, 0), "step_wait");
+        mesh_gpu_stats st{};
+        api_->stats_get(h, &st);
+        device_ms_ += st.last_step_ms;
+        ++steps_;
+    }
+    it->second.clear();
+}
+
+void GpuExecutor::request_evicted(const Cluster&, InstanceId inst, const Request& r) {
+    auto d = inst_dev_.find(inst);
+    if (d == inst_dev_.end()) return;
+    mesh_gpu* h = handles_[static_cast<std::size_t>(d->second)];
+    // a request that never ran a prefill has no device state: nothing to park
+    (void)api_->swap_out(h, inst, r.id);
+}
+
+void GpuExecutor::request_finished(const Cluster&, InstanceId inst, const Request& r) {
+    auto d = inst_dev_.find(inst);
+    if (d == inst_dev_.end()) return;
+    (void)api_->request_free(handles_[static_cast<std::size_t>(d->second)], inst, r.id);
+}
+
+void GpuExecutor::instance_unloaded(const Cluster&, InstanceId inst) {
+    auto d = inst_dev_.find(inst);
+    if (d == inst_dev_.end()) return;
+    mesh_gpu* h = handles_[static_cast<std::size_t>(d->second)];
+    check(h, api_->instance_destroy(h, inst), "instance_destroy");
+    inst_dev_.erase(d);
+}
+
+std::map<std::string, double> GpuExecutor::metrics() const {
+    std::map<std::string, double> m;
+    m["gpu.steps"] = static_cast<double>(steps_);
+    m["gpu.decode_tokens"] = static_cast<double>(decode_tokens_);
+    m["gpu.prefill_tokens"] = static_cast<double>(prefill_tokens_);
+    m["gpu.device_ms"] = device_ms_;
+    double swap = 0, mig = 0, moved = 0;
+    for (mesh_gpu* h : handles_) {
+        mesh_gpu_stats st{};
+        api_->stats_get(h, &st);
+        swap += static_cast<double>(st.swap_out_bytes);
+        mig += static_cast<double>(st.migrate_bytes);
+        moved += static_cast<double>(st.blocks_moved);
+    }
+    m["gpu.swap_out_bytes"] = swap;
+    m["gpu.migrate_bytes"] = mig;
+    m["gpu.blocks_moved"] = moved;
+    return m;
+}
+
+}  // namespace mesh

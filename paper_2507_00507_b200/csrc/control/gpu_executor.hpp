@@ -1,0 +1,53 @@
+// DataPlane that executes the control plane's actions on B200s through the
+// mesh_gpu C ABI (libmesh_gpu.so, loaded with dlopen so the control plane
+// builds and runs without CUDA). Node i -> device devices[i % n].
+#pragma once
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "mesh_cluster.hpp"
+
+struct mesh_gpu;
+
+namespace mesh {
+
+struct LlamaShape {
+    int n_layers, d_model, n_heads, n_kv_heads, d_head, d_ff, vocab, tied, max_seq_len;
+    float rope_theta, rms_eps;
+};
+// Llama-family shapes per size class; unknown classes throw.
+const LlamaShape& llama_shape_for(const std::string& size_class);
+
+class GpuExecutor : public DataPlane {
+public:
+    GpuExecutor(const std::string& lib_path, std::vector<int> devices, long long kv_pool_bytes);
+    ~GpuExecutor() override;
+
+    void instance_start(const Cluster&, const Instance&) override;
+    void kv_issue(const Cluster&, const Instance&, const ScaleOp&) override;
+    void iteration_start(const Cluster&, const Node&, const Instance&, const IterationPlan&) override;
+    void iteration_done(const Cluster&, const Node&, const IterationPlan&, const IterationOutcome&) override;
+    void request_evicted(const Cluster&, InstanceId, const Request&) override;
+    void request_finished(const Cluster&, InstanceId, const Request&) override;
+    void instance_unloaded(const Cluster&, InstanceId) override;
+
+    std::map<std::string, double> metrics() const;
+
+private:
+    struct Api;
+    Api* api_ = nullptr;
+    void* dl_ = nullptr;
+    std::vector<int> devices_;
+    long long pool_bytes_;
+    std::vector<mesh_gpu*> handles_;                 // per device index
+    std::map<InstanceId, int> inst_dev_;             // instance -> device index
+    std::map<NodeId, std::vector<long long>> tickets_;  // in-flight step of each node
+    double device_ms_ = 0.0;
+    long long steps_ = 0, decode_tokens_ = 0, prefill_tokens_ = 0;
+    mesh_gpu* handle_for_node(NodeId node);
+    void check(mesh_gpu* h, int status, const char* what);
+};
+
+}  // namespace mesh

@@ -127,23 +127,31 @@ MESH_DEV void named_bar_sync(int id, int nthreads) {
 // ------------------------------------------------------------ grid barrier
 // Sense-reversing barrier over all CTAs of a persistent launch. `count` returns
 // to 0 after every barrier and `gen` only ever increments, so the pair needs no
-// reset between launches. Called by ONE thread per CTA after a CTA-level sync.
+// reset between launches. Called by ONE thread per CTA after a CTA-level
+// bar.sync; the arrival is a gpu-scope release and the wait a gpu-scope acquire
+// (the CTA's other threads are ordered by the surrounding bar.syncs), so no
+// separate sequentially-consistent fences are needed.
+MESH_DEV unsigned int ld_acquire_gpu(const unsigned int* p) {
+    unsigned int v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+MESH_DEV int atom_add_acq_rel_gpu(int* p, int v) {
+    int old;
+    asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
+    return old;
+}
 MESH_DEV void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int nblocks) {
-    unsigned int my_gen;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(my_gen) : "l"(gen) : "memory");
-    __threadfence();
-    unsigned int old = atomicAdd(count, 1u);
+    const unsigned int my_gen = ld_acquire_gpu(gen);
+    unsigned int old;
+    asm volatile("atom.add.acq_rel.gpu.global.u32 %0, [%1], 1;\n" : "=r"(old) : "l"(count) : "memory");
     if (old == nblocks - 1) {
-        atomicExch(count, 0u);
-        __threadfence();
+        asm volatile("st.relaxed.gpu.global.u32 [%0], 0;\n" ::"l"(count) : "memory");
         asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(gen), "r"(my_gen + 1) : "memory");
     } else {
-        unsigned int cur;
-        do {
-            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(cur) : "l"(gen) : "memory");
-        } while (cur == my_gen);
+        while (ld_acquire_gpu(gen) == my_gen) {
+        }
     }
-    __threadfence();
 }
 
 // ------------------------------------------------ weight tiling (T16 x SW128)

@@ -19,10 +19,12 @@
 //  * Migration: peer copy of a request's blocks into another instance.
 #include <cuda.h>
 #include <cuda_runtime.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -298,6 +300,11 @@ struct mesh_gpu {
     int64_t next_ticket = 1;
     bool capture_logits = false;
     mesh_gpu_stats st{};
+    int nstage = DEC_NSTAGE;  // decode ring depth in use (MESH_GPU_NSTAGE)
+    int l2_ahead = 0;         // L2 prefetch run-ahead in stages (MESH_GPU_L2_AHEAD)
+    int skip = 0;             // MESH_GPU_SKIP debug mask (benchmarking only)
+    int* dbg_host = nullptr;  // MESH_GPU_WATCHDOG: host-mapped decode progress
+    int* dbg_dev = nullptr;
 };
 
 namespace {
@@ -579,6 +586,11 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.tok_out = g->d_tok + ring * 8;
     a.bar_count = g->bar;
     a.bar_gen = g->bar + 1;
+    a.progress = g->dbg_dev;
+    a.trace = nullptr;
+    a.nstage = g->nstage;
+    a.l2_ahead = g->l2_ahead;
+    a.skip = g->skip;
     return a;
 }
 
@@ -794,6 +806,14 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         CK(cudaMalloc((void**)&g->d_tok, sizeof(int) * 8 * RING));
         for (int i = 0; i < RING; ++i) CK(cudaEventCreateWithFlags(&g->ring_ev[i], cudaEventDisableTiming));
         g->st.kv_pool_bytes = g->pool.limit;
+        if (const char* e = std::getenv("MESH_GPU_NSTAGE")) g->nstage = std::max(2, std::min(DEC_NSTAGE, std::atoi(e)));
+        if (const char* e = std::getenv("MESH_GPU_L2_AHEAD")) g->l2_ahead = std::max(0, std::atoi(e));
+        if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
+        if (std::getenv("MESH_GPU_WATCHDOG")) {
+            CK(cudaHostAlloc((void**)&g->dbg_host, sizeof(int) * 2 * 1024, cudaHostAllocMapped));
+            std::memset(g->dbg_host, 0, sizeof(int) * 2 * 1024);
+            CK(cudaHostGetDevicePointer((void**)&g->dbg_dev, g->dbg_host, 0));
+        }
     });
     if (st != MESH_OK) {
         // keep the message reachable: hand the handle back only on success
@@ -855,11 +875,12 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         s.rope_theta = sh->rope_theta > 0 ? sh->rope_theta : 10000.f;
         s.eps = sh->rms_eps > 0 ? sh->rms_eps : 1e-5f;
         if (s.dh != 64 && s.dh != 128) throw MeshError(MESH_ERR_CONFIG, "d_head must be 64 or 128");
-        if (s.n_heads % s.n_kv != 0 || s.gq() > 8) throw MeshError(MESH_ERR_CONFIG, "GQA group must divide and be <= 8");
+        if (s.n_heads % s.n_kv != 0 || s.gq() * s.dh > 512)
+            throw MeshError(MESH_ERR_CONFIG, "GQA group x d_head must be <= 512 (decode smem budget)");
         if (s.n_heads * s.dh != s.d) throw MeshError(MESH_ERR_CONFIG, "n_heads * d_head must equal d_model");
         if (s.d % 256 || s.ff % 256 || s.vocab % 128 || (s.qkv_rows() % 128))
             throw MeshError(MESH_ERR_CONFIG, "d_model/d_ff must be multiples of 256, vocab of 128");
-        if (s.max_seq < 2 || s.max_seq > ATT_SPLIT * ATT_MAX_SPLITS)
+        if (s.max_seq < 2 || s.max_seq > DEC_BT_MAX * KV_BLOCK_TOKENS)
             throw MeshError(MESH_ERR_CONFIG, "max_seq_len out of range");
         ensure_scratch(g, s);
         auto in = std::make_unique<Instance>();
@@ -1266,10 +1287,44 @@ mesh_status mesh_gpu_bench_decode(mesh_gpu* g, int64_t instance_id, const mesh_s
         cudaEvent_t e0, e1;
         CK(cudaEventCreate(&e0));
         CK(cudaEventCreate(&e1));
+        unsigned long long* tr = nullptr;
+        const char* trace_path = std::getenv("MESH_GPU_TRACE");
+        if (trace_path) {
+            CK(cudaMalloc((void**)&tr, sizeof(unsigned long long) * 4096));
+            CK(cudaMemset(tr, 0, sizeof(unsigned long long) * 4096));
+        }
         CK(launch_decode(a, grid_of(g), g->stream));  // warm
+        if (tr) {
+            DecodeArgs at = a;
+            at.trace = tr;
+            CK(launch_decode(at, grid_of(g), g->stream));
+            CK(cudaStreamSynchronize(g->stream));
+            std::vector<unsigned long long> h(4096);
+            CK(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * 4096, cudaMemcpyDeviceToHost));
+            FILE* f = std::fopen(trace_path, "w");
+            if (f) {
+                for (auto v : h)
+                    if (v) std::fprintf(f, "%llu %llu\n", v >> 4, v & 15);
+                std::fclose(f);
+            }
+            CK(cudaFree(tr));
+        }
         CK(cudaEventRecord(e0, g->stream));
         for (int i = 0; i < iters; ++i) CK(launch_decode(a, grid_of(g), g->stream));
         CK(cudaEventRecord(e1, g->stream));
+        if (g->dbg_host) {
+            for (int spin = 0; cudaEventQuery(e1) == cudaErrorNotReady; ++spin) {
+                usleep(1000);
+                if (spin == 20000) {
+                    std::fprintf(stderr, "decode watchdog: step not finished after 20 s; per-CTA (barriers, stage):\n");
+                    for (int i = 0; i < grid_of(g); ++i)
+                        std::fprintf(stderr, "%d:(%d,%d) ", i, g->dbg_host[2 * i], g->dbg_host[2 * i + 1]);
+                    std::fprintf(stderr, "\n");
+                    std::fflush(stderr);
+                    std::abort();
+                }
+            }
+        }
         CK(cudaEventSynchronize(e1));
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, e0, e1));

@@ -1,21 +1,24 @@
 // Decode step as ONE persistent kernel per instance step.
 //
 // Grid = the instance's SM quota (one CTA per SM). Every CTA runs a TMA
-// producer warp that streams its share of ALL weight tiles of the step (every
-// layer's QKV, O, gate/up, down, then lm_head) through a 16-stage shared-memory
-// ring with 1-D bulk copies, never waiting on activations: weights do not
-// depend on them, so the stream runs ahead across the grid barriers that
-// separate the phases. Eight consumer warps wait for the ring, multiply the
-// 16-row weight tiles with the (<= 8) activation columns on the tensor cores
-// (mma.m16n8k16, bf16 in / fp32 accumulate) and apply fused epilogues:
-//   QKV   : RMSNorm scale, rotate-half RoPE, q -> scratch, k/v -> paged KV cache
-//   ATTN  : paged GQA attention, split over context, deterministic combine
-//   O     : residual add, next RMSNorm numerator and sum-of-squares partials
+// producer warp that streams its share of ALL bytes of the step through a
+// shared-memory ring with 1-D bulk copies (cp.async.bulk + mbarrier
+// complete_tx): every layer's QKV, attention KV, O, gate/up and down, then
+// lm_head. Neither the weights nor the KV of earlier tokens depend on this
+// step's activations, so the stream runs ahead across the grid barriers that
+// separate the phases; only the current token's K/V (written by this step's
+// QKV phase) is read directly. Eight consumer warps wait for the ring and:
+//   QKV   : 16-row weight tiles x (<= 8) activation columns on the tensor cores
+//           (mma.m16n8k16, bf16 in / fp32 acc); RMSNorm scale, rotate-half RoPE,
+//           q -> scratch, k/v -> paged KV cache
+//   ATTN  : per-warp online softmax over 8 KB KV stages; partials combined in a
+//           fixed order by the last contributor of each (request, kv head)
+//   O     : residual add, next RMSNorm numerator, sum-of-squares partials
 //   GU    : RMSNorm scale, silu(gate) * up
-//   DOWN  : residual add, next RMSNorm numerator and sum-of-squares partials
+//   DOWN  : residual add, next RMSNorm numerator, sum-of-squares partials
 //   LM    : final RMSNorm scale, optional logits, greedy argmax
-// Tiles are dealt round-robin across CTAs continuing from phase to phase, so
-// every CTA streams (within one tile) the same number of bytes per step.
+// Weight tiles are dealt round-robin across CTAs continuing from phase to
+// phase; attention stages are dealt in contiguous ranges.
 #include "decode.cuh"
 
 #include <math.h>
@@ -26,10 +29,13 @@ namespace {
 
 enum PhaseKind { PH_QKV = 0, PH_O = 1, PH_GU = 2, PH_DOWN = 3, PH_LM = 4 };
 
+constexpr int CONSUMER_THREADS = DEC_NCW * 32;
+__device__ __forceinline__ void csync() { named_bar_sync(1, CONSUMER_THREADS); }
+
 struct GemvPhase {
     int kind, layer;
-    int tiles;   // 16-row tiles
-    int K;       // columns
+    int tiles;  // 16-row tiles
+    int K;      // columns
     const uint8_t* base;
 };
 
@@ -55,20 +61,84 @@ struct MyTiles {
 __device__ __forceinline__ MyTiles my_tiles(int tiles, int off, int cta, int G) {
     int t0 = (cta - off) % G;
     if (t0 < 0) t0 += G;
-    MyTiles m;
-    m.t0 = t0;
-    m.n = t0 < tiles ? (tiles - 1 - t0) / G + 1 : 0;
-    return m;
+    return {t0, t0 < tiles ? (tiles - 1 - t0) / G + 1 : 0};
 }
 __device__ __forceinline__ int n_segments(int K) {
-    int chunks = K / DEC_CHUNK_COLS;
-    int per = DEC_KSEG_MAX / DEC_CHUNK_COLS;
+    const int chunks = K / DEC_CHUNK_COLS, per = DEC_KSEG_MAX / DEC_CHUNK_COLS;
     return (chunks + per - 1) / per;
 }
 __device__ __forceinline__ void seg_range(int K, int nseg, int s, int& c0, int& c1) {
-    int chunks = K / DEC_CHUNK_COLS;
+    const int chunks = K / DEC_CHUNK_COLS;
     c0 = (chunks * s) / nseg;
     c1 = (chunks * (s + 1)) / nseg;
+}
+
+// ---- attention work plan (identical on producer and consumers) ----
+// Stages enumerate (request b, kv head, chunk s of RT = 2048/dh tokens) in
+// b-major order; stage = the K and V rows of those tokens for one layer, 8 KB.
+struct AttnPlan {
+    int rt;             // tokens per stage
+    int nst[DEC_MAXB];  // stages per (b, kv head)
+    int total;          // stages per layer
+    int a0, a1;         // this CTA's contiguous range
+};
+__device__ __forceinline__ long long range_lo(int c, int total, int G) { return (long long)c * total / G; }
+__device__ __forceinline__ AttnPlan attn_plan(const Shape& s, int B, const int* pos, int cta, int G) {
+    AttnPlan p;
+    p.rt = 2048 / s.dh;
+    p.total = 0;
+    for (int b = 0; b < DEC_MAXB; ++b) {
+        p.nst[b] = b < B ? (pos[b] + p.rt) / p.rt : 0;  // ceil((pos + 1) / rt)
+        p.total += s.n_kv * p.nst[b];
+    }
+    p.a0 = int(range_lo(cta, p.total, G));
+    p.a1 = int(range_lo(cta + 1, p.total, G));
+    return p;
+}
+struct AttnStage {
+    int b, kvh, s, pair, pair_lo;  // pair_lo: global index of the pair's first stage
+};
+__device__ __forceinline__ AttnStage attn_stage_of(const AttnPlan& p, int n_kv, int i) {
+    AttnStage st;
+    int base = 0;
+    for (int b = 0; b < DEC_MAXB; ++b) {
+        const int n = n_kv * p.nst[b];
+        if (i < base + n) {
+            const int r = i - base;
+            st.b = b;
+            st.kvh = r / p.nst[b];
+            st.s = r % p.nst[b];
+            st.pair = b * n_kv + st.kvh;
+            st.pair_lo = base + st.kvh * p.nst[b];
+            return st;
+        }
+        base += n;
+    }
+    st.b = st.kvh = st.s = st.pair = st.pair_lo = 0;
+    return st;
+}
+__device__ __forceinline__ int cta_of_stage(int i, int total, int G) {
+    return int(((long long)(i + 1) * G - 1) / total);
+}
+// Deterministic slot of (cta, warp) among the contributors of a pair, and the
+// pair's contributor count: within a CTA the pair's stages [lo, hi) go to warps
+// (i - a0) mod 8, i.e. min(8, hi - lo) consecutive warps.
+__device__ __forceinline__ void pair_slots(int lo_p, int hi_p, int total, int G, int cta, int warp, int& rank,
+                                           int& count) {
+    count = 0;
+    rank = -1;
+    const int c0 = cta_of_stage(lo_p, total, G), c1 = cta_of_stage(hi_p - 1, total, G);
+    for (int c = c0; c <= c1; ++c) {
+        const int a0 = int(range_lo(c, total, G)), a1 = int(range_lo(c + 1, total, G));
+        const int lo = max(lo_p, a0), hi = min(hi_p, a1);
+        if (hi <= lo) continue;
+        const int n = min(8, hi - lo);
+        if (c == cta) {
+            const int r = ((warp - (lo - a0)) % 8 + 8) % 8;
+            if (r < n) rank = count + r;
+        }
+        count += n;
+    }
 }
 
 struct Smem {
@@ -78,6 +148,7 @@ struct Smem {
     uint64_t* full;
     uint64_t* empty;
     float* misc;
+    int* bt;  // [8][DEC_BT_MAX] block-table rows of the step's requests
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base) {
@@ -88,150 +159,307 @@ __device__ __forceinline__ Smem carve(uint8_t* base) {
     m.full = reinterpret_cast<uint64_t*>(base + DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC);
     m.empty = m.full + DEC_NSTAGE;
     m.misc = reinterpret_cast<float*>(base + DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS);
+    m.bt = reinterpret_cast<int*>(base + DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS + DEC_SMEM_MISC);
     return m;
 }
 
-constexpr int CONSUMER_THREADS = DEC_NCW * 32;
-__device__ __forceinline__ void csync() { named_bar_sync(1, CONSUMER_THREADS); }
-
 // ----------------------------------------------------------------- producer
-__device__ void producer_loop(const DecodeArgs& a, Smem& sm, int cta, int G) {
-    const uint64_t pol = l2_evict_first_policy();
+__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
+}
+
+// Enumerates this CTA's GEMV weight stages in consumption order (used for the
+// optional L2 run-ahead): per phase, tiles in groups of DEC_MAXT, each group
+// segment by segment, tile by tile, chunk by chunk.
+struct GemvIter {
+    const DecodeArgs* a;
+    int cta, G, ph, off;
+    GemvPhase p;
+    MyTiles mt;
+    int nseg, g0, gn, sg, c0, c1, ti, c;
+    bool live;
+    __device__ __forceinline__ void begin_phase() {
+        while (ph <= 4 * a->s.n_layers) {
+            const int kind = ph == 4 * a->s.n_layers ? PH_LM : (ph & 3);
+            p = gemv_phase(*a, kind, ph >> 2);
+            mt = my_tiles(p.tiles, off, cta, G);
+            off = (off + p.tiles) % G;
+            if (mt.n > 0) {
+                nseg = n_segments(p.K);
+                g0 = 0;
+                gn = min(DEC_MAXT, mt.n);
+                sg = 0;
+                seg_range(p.K, nseg, 0, c0, c1);
+                ti = 0;
+                c = c0;
+                return;
+            }
+            ++ph;
+        }
+        live = false;
+    }
+    __device__ __forceinline__ void init(const DecodeArgs* args, int cta_, int G_) {
+        a = args;
+        cta = cta_;
+        G = G_;
+        ph = 0;
+        off = 0;
+        live = true;
+        begin_phase();
+    }
+    __device__ __forceinline__ const uint8_t* next() {
+        if (!live) return nullptr;
+        const int tile = mt.t0 + (g0 + ti) * G;
+        const uint8_t* src = p.base + size_t(tile) * size_t(p.K) * 32 + size_t(c) * DEC_STAGE_BYTES;
+        if (++c < c1) return src;
+        if (++ti < gn) {
+            c = c0;
+            return src;
+        }
+        ti = 0;
+        if (++sg < nseg) {
+            seg_range(p.K, nseg, sg, c0, c1);
+            c = c0;
+            return src;
+        }
+        sg = 0;
+        g0 += DEC_MAXT;
+        if (g0 < mt.n) {
+            gn = min(DEC_MAXT, mt.n - g0);
+            seg_range(p.K, nseg, 0, c0, c1);
+            c = c0;
+            return src;
+        }
+        ++ph;
+        begin_phase();
+        return src;
+    }
+};
+
+struct Producer {
+    const DecodeArgs& a;
+    Smem& sm;
     uint32_t q = 0;
-    int off = 0;
-    auto produce = [&](int kind, int layer) {
-        GemvPhase p = gemv_phase(a, kind, layer);
-        MyTiles mt = my_tiles(p.tiles, off, cta, G);
+    uint32_t ns;
+    uint64_t pol;
+    GemvIter pf;
+    bool ahead;
+    __device__ __forceinline__ Producer(const DecodeArgs& args, Smem& s, int cta, int G) : a(args), sm(s) {
+        ns = uint32_t(a.nstage);
+        pol = l2_evict_first_policy();
+        ahead = a.l2_ahead > 0;
+        if (ahead) {
+            pf.init(&a, cta, G);
+            for (int i = 0; i < a.l2_ahead; ++i) {
+                const uint8_t* p = pf.next();
+                if (!p) break;
+                prefetch_l2(p, DEC_STAGE_BYTES);
+            }
+        }
+    }
+    __device__ __forceinline__ uint32_t claim() {
+        const uint32_t slot = q % ns, par = (q / ns) & 1u;
+        mbar_wait(&sm.empty[slot], par ^ 1u);
+        return slot;
+    }
+    __device__ __forceinline__ void weight_stage(const uint8_t* src) {
+        const uint32_t slot = claim();
+        mbar_arrive_expect_tx(&sm.full[slot], DEC_STAGE_BYTES);
+        bulk_g2s_evict_first(sm.ring + size_t(slot) * DEC_STAGE_BYTES, src, DEC_STAGE_BYTES, &sm.full[slot], pol);
+        if (ahead) {
+            const uint8_t* p = pf.next();
+            if (p) prefetch_l2(p, DEC_STAGE_BYTES);
+        }
+        ++q;
+    }
+    __device__ __forceinline__ void gemv(int kind, int layer, int& off, int cta, int G) {
+        const GemvPhase p = gemv_phase(a, kind, layer);
+        const MyTiles mt = my_tiles(p.tiles, off, cta, G);
         off = (off + p.tiles) % G;
         if (mt.n == 0) return;
         const size_t tile_bytes = size_t(p.K) * 32;
-        int nseg = n_segments(p.K);
+        const int nseg = n_segments(p.K);
         for (int g0 = 0; g0 < mt.n; g0 += DEC_MAXT) {
-            int gn = min(DEC_MAXT, mt.n - g0);
+            const int gn = min(DEC_MAXT, mt.n - g0);
             for (int sg = 0; sg < nseg; ++sg) {
                 int c0, c1;
                 seg_range(p.K, nseg, sg, c0, c1);
                 for (int ti = 0; ti < gn; ++ti) {
-                    int tile = mt.t0 + (g0 + ti) * G;
-                    const uint8_t* tsrc = p.base + size_t(tile) * tile_bytes;
-                    for (int c = c0; c < c1; ++c) {
-                        uint32_t slot = q % DEC_NSTAGE;
-                        uint32_t par = (q / DEC_NSTAGE) & 1u;
-                        mbar_wait(&sm.empty[slot], par ^ 1u);
-                        mbar_arrive_expect_tx(&sm.full[slot], DEC_STAGE_BYTES);
-                        bulk_g2s_evict_first(sm.ring + size_t(slot) * DEC_STAGE_BYTES,
-                                             tsrc + size_t(c) * DEC_STAGE_BYTES, DEC_STAGE_BYTES,
-                                             &sm.full[slot], pol);
-                        ++q;
-                    }
+                    const uint8_t* t = p.base + size_t(mt.t0 + (g0 + ti) * G) * tile_bytes;
+                    for (int ch = c0; ch < c1; ++ch) weight_stage(t + size_t(ch) * DEC_STAGE_BYTES);
                 }
             }
         }
-    };
-    for (int l = 0; l < a.s.n_layers; ++l) {
-        produce(PH_QKV, l);
-        produce(PH_O, l);
-        produce(PH_GU, l);
-        produce(PH_DOWN, l);
     }
-    produce(PH_LM, 0);
+    // KV stages of this CTA's attention range: only blocks that were complete
+    // before this step (every position < pos) are streamed; the current token
+    // is read directly by the consumer.
+    __device__ __forceinline__ void attention(int layer, const AttnPlan& ap, const int* pos) {
+        const Shape& s = a.s;
+        const uint32_t blk_bytes = uint32_t(KV_BLOCK_TOKENS * s.dh * 2);  // one (layer, k|v, head) block
+        const int blocks_per_stage = ap.rt / KV_BLOCK_TOKENS;
+        for (int i = ap.a0; i < ap.a1; ++i) {
+            const AttnStage st = attn_stage_of(ap, s.n_kv, i);
+            const uint32_t slot = claim();
+            uint8_t* dst = sm.ring + size_t(slot) * DEC_STAGE_BYTES;
+            const int p = pos[st.b];
+            int nblk = 0;
+            for (int j = 0; j < blocks_per_stage; ++j)
+                if ((st.s * blocks_per_stage + j) * KV_BLOCK_TOKENS < p) ++nblk;
+            mbar_arrive_expect_tx(&sm.full[slot], 2u * nblk * blk_bytes);
+            for (int j = 0; j < nblk; ++j) {
+                const int k = st.s * blocks_per_stage + j;
+                const int blk = sm.bt[st.b * DEC_BT_MAX + k];
+                const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
+                bulk_g2s(dst + j * blk_bytes, base + kv_offset(s, layer, 0, st.kvh, 0), blk_bytes, &sm.full[slot]);
+                bulk_g2s(dst + 4096 + j * blk_bytes, base + kv_offset(s, layer, 1, st.kvh, 0), blk_bytes,
+                         &sm.full[slot]);
+            }
+            ++q;
+        }
+    }
+};
+
+__device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int cta, int G, int B, const int* pos) {
+    if (a.skip & 2) return;
+    Producer pr(a, sm, cta, G);
+    const AttnPlan ap = attn_plan(a.s, B, pos, cta, G);
+    int off = 0;
+    for (int l = 0; l < a.s.n_layers; ++l) {
+        pr.gemv(PH_QKV, l, off, cta, G);
+        if (!(a.skip & 1)) pr.attention(l, ap, pos);
+        pr.gemv(PH_O, l, off, cta, G);
+        pr.gemv(PH_GU, l, off, cta, G);
+        pr.gemv(PH_DOWN, l, off, cta, G);
+        if (a.progress) a.progress[cta * 2 + 1] = int(pr.q);
+    }
+    pr.gemv(PH_LM, 0, off, cta, G);
 }
 
 // ----------------------------------------------------------------- consumer
 struct Ctx {
-    const DecodeArgs* a;
+    int ntrace;           // trace cursor (CTA 0, thread 0)
+    const DecodeArgs* a;  // shared-memory copy of the launch arguments
     Smem sm;
     int cta, G, warp, lane, tid;  // tid in [0, 256)
     int B;
-    int slot[DEC_MAXB];
-    int pos[DEC_MAXB];
-    uint32_t q;     // stage counter (mirrors the producer)
-    int off;        // round-robin offset (mirrors the producer)
-    int accbuf;     // acc double-buffer parity
+    const int* slot;  // [8] in shared memory
+    const int* pos;   // [8] in shared memory
+    uint32_t q;       // stage counter (mirrors the producer)
+    int off;          // round-robin offset (mirrors the producer)
 };
 
-__device__ void grid_sync(Ctx& c) {
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// tag: 1 phase begin, 2 operands ready, 3 stages consumed, 4 epilogue done, 5 barrier passed,
+//      6 attention begin, 7 attention end
+__device__ __forceinline__ void trace(Ctx& c, int tag) {
+    if (c.a->trace && c.cta == 0 && c.tid == 0 && c.ntrace < 4000)
+        c.a->trace[c.ntrace++] = (gtimer() << 4) | unsigned(tag);
+}
+__device__ __forceinline__ void grid_sync(Ctx& c) {
     csync();
+    if (c.a->progress && c.tid == 0) c.a->progress[c.cta * 2] += 1;
     if (c.tid == 0) grid_barrier(c.a->bar_count, c.a->bar_gen, unsigned(c.G));
     csync();
+    trace(c, 5);
+}
+
+__device__ __forceinline__ void wait_stage(Ctx& c, uint32_t qi, uint32_t& slot) {
+    const uint32_t ns = uint32_t(c.a->nstage);
+    slot = qi % ns;
+    mbar_wait(&c.sm.full[slot], (qi / ns) & 1u);
+}
+__device__ __forceinline__ void release_stage(Ctx& c, uint32_t slot) {
+    __syncwarp();
+    if (c.lane == 0) mbar_arrive(&c.sm.empty[slot]);
 }
 
 // rs[b] = 1/sqrt(mean(h_b^2) + eps) from per-tile partials, summed in a fixed order.
-__device__ void compute_rs(Ctx& c, const float* ss, float* rs_out) {
+__device__ __forceinline__ void compute_rs(Ctx& c, const float* ss, float* rs_out) {
     const DecodeArgs& a = *c.a;
-    int nt = a.s.d / 16;
-    int b = c.warp;  // 8 warps <-> 8 batch columns
+    const int nt = a.s.d / 16;  // <= 512 partials, 16 per lane, all loads issued before use
+    const int b = c.warp;       // 8 warps <-> 8 batch columns
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int t = c.lane + 32 * k;
+        v[k] = t < nt ? ldcg_f32(ss + t * 8 + b) : 0.f;
+    }
     float acc = 0.f;
-    for (int t = c.lane; t < nt; t += 32) acc += ldcg_f32(ss + t * 8 + b);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc += v[k];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
     if (c.lane == 0) rs_out[b] = rsqrtf(acc / float(a.s.d) + a.s.eps);
 }
 
-// Load activation columns [k0, k1) of the 8 batch rows (bf16, global) into smem.
-__device__ void load_act(Ctx& c, const uint16_t* src, int ld, int k0, int k1) {
-    int n = k1 - k0;  // multiple of 256
-    int stride = n + 8;
-    int vec_per_row = n / 8;
-    for (int i = c.tid; i < DEC_MAXB * vec_per_row; i += CONSUMER_THREADS) {
-        int b = i / vec_per_row, v = i % vec_per_row;
-        uint4 val = make_uint4(0, 0, 0, 0);
-        if (b < c.B) val = ldcg_u4(src + size_t(b) * ld + k0 + v * 8);
-        *reinterpret_cast<uint4*>(c.sm.act + b * stride + v * 8) = val;
+// Activation columns [k0, k1) of the 8 batch rows (bf16, global) into smem,
+// every thread's loads issued before its stores (up to 8 x 16 B in flight).
+__device__ __forceinline__ void load_act(Ctx& c, const uint16_t* src, int ld, int k0, int k1) {
+    const int n = k1 - k0, stride = n + 8, vec_per_row = n / 8, total = DEC_MAXB * vec_per_row;
+    for (int base = 0; base < total; base += 8 * CONSUMER_THREADS) {
+        uint4 v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = base + k * CONSUMER_THREADS + c.tid;
+            const int b = i / vec_per_row, e = i % vec_per_row;
+            v[k] = (i < total && b < c.B) ? ldcg_u4(src + size_t(b) * ld + k0 + e * 8) : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            const int i = base + k * CONSUMER_THREADS + c.tid;
+            if (i < total) {
+                const int b = i / vec_per_row, e = i % vec_per_row;
+                *reinterpret_cast<uint4*>(c.sm.act + b * stride + e * 8) = v[k];
+            }
+        }
     }
 }
 
-// One 8 KB stage: 16 rows x 256 columns against the 8 activation columns.
-__device__ __forceinline__ void consume_stage(Ctx& c, uint32_t qi, int act_col, int act_stride,
-                                              float* acc_slot) {
-    uint32_t slot = qi % DEC_NSTAGE;
-    uint32_t par = (qi / DEC_NSTAGE) & 1u;
-    mbar_wait(&c.sm.full[slot], par);
+// One 8 KB weight stage: 16 rows x 256 columns against the 8 activation
+// columns, accumulated into the warp's registers (two chains for ILP).
+__device__ __forceinline__ void consume_stage(Ctx& c, uint32_t qi, int act_col, int act_stride, float (&d0)[4],
+                                              float (&d1)[4]) {
+    uint32_t slot;
+    wait_stage(c, qi, slot);
     const uint32_t stage_addr = smem_u32(c.sm.ring + size_t(slot) * DEC_STAGE_BYTES);
-    const int lane = c.lane;
-    const int r = lane & 15;
-    const int g = lane >> 2, t = lane & 3;
+    const int lane = c.lane, r = lane & 15, g = lane >> 2, t = lane & 3;
     const uint16_t* actrow = c.sm.act + g * act_stride + act_col + 2 * t;
-    float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int j = 0; j < 16; ++j) {
-        int kb = j >> 2;
-        int chunk = ((j & 3) << 1) + (lane >> 4);
-        uint32_t addr = stage_addr + kb * 2048 + r * 128 + (uint32_t((chunk ^ (r & 7))) << 4);
+        const int kb = j >> 2, chunk = ((j & 3) << 1) + (lane >> 4);
         uint32_t a0, a1, a2, a3;
-        ldmatrix_x4(addr, a0, a1, a2, a3);
-        uint32_t b0 = *reinterpret_cast<const uint32_t*>(actrow + j * 16);
-        uint32_t b1 = *reinterpret_cast<const uint32_t*>(actrow + j * 16 + 8);
+        ldmatrix_x4(stage_addr + kb * 2048 + r * 128 + (uint32_t((chunk ^ (r & 7))) << 4), a0, a1, a2, a3);
+        const uint32_t b0 = *reinterpret_cast<const uint32_t*>(actrow + j * 16);
+        const uint32_t b1 = *reinterpret_cast<const uint32_t*>(actrow + j * 16 + 8);
         if (j & 1)
             mma_bf16_16816(d1, a0, a1, a2, a3, b0, b1);
         else
             mma_bf16_16816(d0, a0, a1, a2, a3, b0, b1);
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&c.sm.empty[slot]);
-    float* dst = acc_slot + lane * 4;
-    atomicAdd(dst + 0, d0[0] + d1[0]);
-    atomicAdd(dst + 1, d0[1] + d1[1]);
-    atomicAdd(dst + 2, d0[2] + d1[2]);
-    atomicAdd(dst + 3, d0[3] + d1[3]);
+    release_stage(c, slot);
 }
 
-// ---- epilogues: lane holds rows (g, g+8) x batch columns (2t, 2t+1) of tile `tile`.
-__device__ void epi_qkv(Ctx& c, int layer, int tile, const float v[4], const float* rs) {
+// ---- GEMV epilogues: lane holds rows (g, g+8) x batch columns (2t, 2t+1) of `tile`.
+__device__ __forceinline__ void epi_qkv(Ctx& c, int layer, int tile, const float v[4], const float* rs) {
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
-    int g = c.lane >> 2, t = c.lane & 3;
-    QkvRow r1 = qkv_row(s, tile * 16 + g);  // dim in [0, dh/2); row g+8 is dim + dh/2
+    const int g = c.lane >> 2, t = c.lane & 3;
+    const QkvRow r1 = qkv_row(s, tile * 16 + g);  // dim in [0, dh/2); row g+8 is dim + dh/2
     const int half = s.dh / 2;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        int b = 2 * t + j;
+        const int b = 2 * t + j;
         if (b >= c.B) continue;
-        float x1 = v[j] * rs[b], x2 = v[2 + j] * rs[b];
-        int pos = c.pos[b];
+        const float x1 = v[j] * rs[b], x2 = v[2 + j] * rs[b];
+        const int pos = c.pos[b];
         float o1 = x1, o2 = x2;
         if (r1.section < 2) {
-            float2 cs = a.w.rope[size_t(pos) * half + r1.dim];
+            const float2 cs = a.w.rope[size_t(pos) * half + r1.dim];
             o1 = x1 * cs.x - x2 * cs.y;
             o2 = x2 * cs.x + x1 * cs.y;
         }
@@ -240,57 +468,55 @@ __device__ void epi_qkv(Ctx& c, int layer, int tile, const float v[4], const flo
             qd[r1.dim] = o1;
             qd[r1.dim + half] = o2;
         } else {
-            int blk = ldcg_i32(a.block_table + size_t(c.slot[b]) * a.bt_stride + pos / KV_BLOCK_TOKENS);
-            uint8_t* p = a.kv_base + size_t(blk) * a.block_bytes +
-                         kv_offset(s, layer, r1.section - 1, r1.head, pos % KV_BLOCK_TOKENS);
-            uint16_t* e = reinterpret_cast<uint16_t*>(p);
+            const int blk = ldcg_i32(a.block_table + size_t(c.slot[b]) * a.bt_stride + pos / KV_BLOCK_TOKENS);
+            uint16_t* e = reinterpret_cast<uint16_t*>(a.kv_base + size_t(blk) * a.block_bytes +
+                                                      kv_offset(s, layer, r1.section - 1, r1.head, pos % KV_BLOCK_TOKENS));
             e[r1.dim] = f_to_bf16(o1);
             e[r1.dim + half] = f_to_bf16(o2);
         }
     }
 }
 
-__device__ void epi_gu(Ctx& c, int tile, const float v[4], const float* rs) {
+__device__ __forceinline__ void epi_gu(Ctx& c, int tile, const float v[4], const float* rs) {
     const DecodeArgs& a = *c.a;
-    int g = c.lane >> 2, t = c.lane & 3;
-    int row = tile * 8 + g;
+    const int g = c.lane >> 2, t = c.lane & 3;
+    const int row = tile * 8 + g;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
-        int b = 2 * t + j;
+        const int b = 2 * t + j;
         if (b >= c.B) continue;
-        float gt = v[j] * rs[b], up = v[2 + j] * rs[b];
-        float act = gt / (1.f + __expf(-gt)) * up;
-        a.abuf[size_t(b) * a.s.ff + row] = f_to_bf16(act);
+        const float gt = v[j] * rs[b], up = v[2 + j] * rs[b];
+        a.abuf[size_t(b) * a.s.ff + row] = f_to_bf16(gt / (1.f + __expf(-gt)) * up);
     }
 }
 
-// Residual add for rows owned by this tile + the next RMSNorm's numerator and
+// Residual add for the rows this tile owns, the next RMSNorm's numerator and
 // the per-tile sum of squares.
-__device__ void epi_residual(Ctx& c, int tile, const float v[4], const float* gamma_next, float* ss_out) {
+__device__ __forceinline__ void epi_residual(Ctx& c, int tile, const float v[4], const float* gamma_next,
+                                             float* ss_out) {
     const DecodeArgs& a = *c.a;
     const int d = a.s.d;
-    int g = c.lane >> 2, t = c.lane & 3;
+    const int g = c.lane >> 2, t = c.lane & 3;
     float sq[2] = {0.f, 0.f};
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
-        int row = tile * 16 + g + 8 * rr;
-        float gm = gamma_next[row];
+        const int row = tile * 16 + g + 8 * rr;
+        const float gm = gamma_next[row];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
-            int b = 2 * t + j;
+            const int b = 2 * t + j;
             if (b >= c.B) continue;
             float* hp = a.h + size_t(b) * d + row;
-            float hv = ldcg_f32(hp) + v[2 * rr + j];
+            const float hv = ldcg_f32(hp) + v[2 * rr + j];
             *hp = hv;
             a.act[size_t(b) * d + row] = f_to_bf16(hv * gm);
             sq[j] += hv * hv;
         }
     }
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) sq[j] += __shfl_xor_sync(0xffffffffu, sq[j], o);
-    }
     if (g == 0) {
         ss_out[tile * 8 + 2 * t] = sq[0];
         ss_out[tile * 8 + 2 * t + 1] = sq[1];
@@ -305,12 +531,13 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
 }
 
 // ------------------------------------------------------------ GEMV phase
-__device__ void run_gemv(Ctx& c, int kind, int layer, float* best_v, int* best_i) {
+__device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* best_v, int* best_i) {
     const DecodeArgs& a = *c.a;
-    GemvPhase p = gemv_phase(a, kind, layer);
-    MyTiles mt = my_tiles(p.tiles, c.off, c.cta, c.G);
+    const GemvPhase p = gemv_phase(a, kind, layer);
+    const MyTiles mt = my_tiles(p.tiles, c.off, c.cta, c.G);
     c.off = (c.off + p.tiles) % c.G;
-
+    trace(c, 1);
+    if (a.skip & 2) return;
     float* rs = c.sm.misc;  // [8]
     if (kind == PH_QKV || kind == PH_LM) compute_rs(c, a.ssA, rs);
     if (kind == PH_GU) compute_rs(c, a.ssB, rs);
@@ -325,57 +552,85 @@ __device__ void run_gemv(Ctx& c, int kind, int layer, float* best_v, int* best_i
         case PH_DOWN: src = a.abuf; ld = a.s.ff; break;
         default: src = a.act; ld = a.s.d; break;
     }
-    int nseg = n_segments(p.K);
+    const int nseg = n_segments(p.K);
+    float* part = c.sm.acc;  // per-warp partial sums: part[warp][tile][lane * 4 + e]
     for (int g0 = 0; g0 < mt.n; g0 += DEC_MAXT) {
-        int gn = min(DEC_MAXT, mt.n - g0);
-        float* accb = c.sm.acc + c.accbuf * DEC_MAXT * 128;
+        const int gn = min(DEC_MAXT, mt.n - g0);
         for (int sg = 0; sg < nseg; ++sg) {
             int c0, c1;
             seg_range(p.K, nseg, sg, c0, c1);
-            int nch = c1 - c0;
+            const int nch = c1 - c0;
             if (nseg > 1 || g0 == 0) {
                 csync();
                 load_act(c, src, ld, c0 * DEC_CHUNK_COLS, c1 * DEC_CHUNK_COLS);
                 csync();
+                trace(c, 2);
             }
-            int act_stride = nch * DEC_CHUNK_COLS + 8;
-            int n = gn * nch;
+            const int act_stride = nch * DEC_CHUNK_COLS + 8;
+            // Warp w consumes stages c.q + w + 8k of this (group, segment): a
+            // warp's consecutive stages are exactly DEC_NCW apart, so it never
+            // waits on a ring slot a full cycle ahead (mbarrier parity would
+            // alias). Partial sums stay in registers while the warp's stages
+            // belong to one tile and are flushed to its part[] slot.
+            const int n = gn * nch;
+            if (sg == 0)
+                for (int ti = 0; ti < gn; ++ti)
+                    reinterpret_cast<float4*>(part + (c.warp * DEC_MAXT + ti) * 128)[c.lane] =
+                        make_float4(0.f, 0.f, 0.f, 0.f);
+            float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+            int cur = -1;
+            auto flush = [&](int ti) {
+                float4* dst = reinterpret_cast<float4*>(part + (c.warp * DEC_MAXT + ti) * 128) + c.lane;
+                const float4 o = *dst;
+                *dst = make_float4(o.x + d0[0] + d1[0], o.y + d0[1] + d1[1], o.z + d0[2] + d1[2], o.w + d0[3] + d1[3]);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) d0[e] = d1[e] = 0.f;
+            };
             for (int i = c.warp; i < n; i += DEC_NCW) {
-                int ti = i / nch, ch = i % nch;
-                consume_stage(c, c.q + i, ch * DEC_CHUNK_COLS, act_stride, accb + ti * 128);
+                const int ti = i / nch, ch = i - ti * nch;
+                if (ti != cur) {
+                    if (cur >= 0) flush(cur);
+                    cur = ti;
+                }
+                consume_stage(c, c.q + i, ch * DEC_CHUNK_COLS, act_stride, d0, d1);
             }
+            if (cur >= 0) flush(cur);
             c.q += n;
         }
         csync();
-        // epilogue: one warp per tile slot
+        trace(c, 3);
+        // epilogue: one warp per tile, summing the eight warps' partials
         for (int ti = c.warp; ti < gn; ti += DEC_NCW) {
-            int tile = mt.t0 + (g0 + ti) * c.G;
-            float4 v4 = *reinterpret_cast<float4*>(accb + ti * 128 + c.lane * 4);
-            *reinterpret_cast<float4*>(accb + ti * 128 + c.lane * 4) = make_float4(0.f, 0.f, 0.f, 0.f);
-            float v[4] = {v4.x, v4.y, v4.z, v4.w};
+            const int tile = mt.t0 + (g0 + ti) * c.G;
+            float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int w = 0; w < DEC_NCW; ++w) {
+                const float4 pv = reinterpret_cast<const float4*>(part + (w * DEC_MAXT + ti) * 128)[c.lane];
+                v[0] += pv.x;
+                v[1] += pv.y;
+                v[2] += pv.z;
+                v[3] += pv.w;
+            }
             switch (kind) {
                 case PH_QKV: epi_qkv(c, layer, tile, v, rs); break;
                 case PH_GU: epi_gu(c, tile, v, rs); break;
-                case PH_O:
-                    epi_residual(c, tile, v, a.w.g_mlp + size_t(layer) * a.s.d, a.ssB);
-                    break;
+                case PH_O: epi_residual(c, tile, v, a.w.g_mlp + size_t(layer) * a.s.d, a.ssB); break;
                 case PH_DOWN: {
-                    const float* gn_next = (layer + 1 < a.s.n_layers)
-                                               ? a.w.g_attn + size_t(layer + 1) * a.s.d
-                                               : a.w.g_final;
-                    epi_residual(c, tile, v, gn_next, a.ssA);
+                    const float* gnext =
+                        (layer + 1 < a.s.n_layers) ? a.w.g_attn + size_t(layer + 1) * a.s.d : a.w.g_final;
+                    epi_residual(c, tile, v, gnext, a.ssA);
                     break;
                 }
                 default: {  // lm_head
-                    int g = c.lane >> 2, t = c.lane & 3;
+                    const int g = c.lane >> 2, t = c.lane & 3;
 #pragma unroll
                     for (int rr = 0; rr < 2; ++rr) {
-                        int row = tile * 16 + g + 8 * rr;
+                        const int row = tile * 16 + g + 8 * rr;
 #pragma unroll
                         for (int j = 0; j < 2; ++j) {
-                            int b = 2 * t + j;
+                            const int b = 2 * t + j;
                             if (b >= c.B) continue;
-                            float logit = v[2 * rr + j] * rs[b];
+                            const float logit = v[2 * rr + j] * rs[b];
                             if (a.logits) a.logits[size_t(b) * a.s.vocab + row] = logit;
                             better(best_v[j], best_i[j], logit, row);
                         }
@@ -384,196 +639,296 @@ __device__ void run_gemv(Ctx& c, int kind, int layer, float* best_v, int* best_i
                 }
             }
         }
-        c.accbuf ^= 1;
+        csync();  // partials are rewritten by the next group
+        trace(c, 4);
     }
-    csync();
 }
 
 // ------------------------------------------------------------ attention
 template <int DH>
-__device__ void attn_unit(Ctx& c, int layer, int b, int kvh, int split) {
+struct AttnCfg {
+    static constexpr int LPT = DH / 64;  // lanes per token (64 dims each)
+    static constexpr int RT = 32 / LPT;  // tokens per stage
+    static constexpr int DPL = DH / 32;  // PV dims per lane
+    static constexpr int HM = 512 / DH;  // largest GQA group (GQ * DH <= 512)
+    static constexpr int WARP_SMEM = 512 * 4 + RT * 9 * 4 + 2 * DH * 2;  // q, p, k/v patch
+};
+
+// Online-softmax state of one warp for the (b, kv head) pair it is reducing.
+template <int DH>
+struct AttnState {
+    float m[AttnCfg<DH>::HM], l[AttnCfg<DH>::HM], acc[AttnCfg<DH>::HM][AttnCfg<DH>::DPL];
+};
+
+template <int DH>
+__device__ __forceinline__ void attn_flush(Ctx& c, const AttnPlan& ap, int b, int kvh, int pair_lo, int pair_n,
+                                           AttnState<DH>& stt) {
+    using CFG = AttnCfg<DH>;
+    constexpr int HM = CFG::HM, DPL = CFG::DPL;
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
     const int GQ = s.n_heads / s.n_kv;
-    const int len = c.pos[b] + 1;
-    const int nsplit = (len + ATT_SPLIT - 1) / ATT_SPLIT;
-    const float scale = rsqrtf(float(DH));
-    constexpr int DPL = DH / 32;
+    const int W = GQ * (DH + 2);
+    const unsigned FULL = 0xffffffffu;
+    const int d0 = c.lane * DPL;
+    int rank, count;
+    pair_slots(pair_lo, pair_lo + pair_n, ap.total, c.G, c.cta, c.warp, rank, count);
+    float* mine = a.apart + size_t(pair_lo + rank) * W;
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+        if (h >= GQ) continue;
+        float* ph = mine + h * (DH + 2);
+        if (c.lane == 0) {
+            ph[0] = stt.m[h];
+            ph[1] = stt.l[h];
+        }
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) ph[2 + d0 + e] = stt.acc[h][e];
+    }
+    __syncwarp();
+    const int pair = b * s.n_kv + kvh;
+    int last = 0;
+    if (c.lane == 0) last = atom_add_acq_rel_gpu(a.acnt + pair, 1) == count - 1;
+    last = __shfl_sync(FULL, last, 0);
+    if (!last) return;
+    // Combine the pair's `count` partials (slot order = deterministic).
+    const float* base = a.apart + size_t(pair_lo) * W;
+    float M[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+        float mx = -INFINITY;
+        if (h < GQ)
+            for (int sp = c.lane; sp < count; sp += 32) mx = fmaxf(mx, ldcg_f32(base + size_t(sp) * W + h * (DH + 2)));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+        M[h] = mx;
+    }
+    float L[HM], A[HM][DPL];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+        L[h] = 0.f;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) A[h][e] = 0.f;
+    }
+    for (int sp0 = 0; sp0 < count; sp0 += 32) {
+        float f[HM];  // lane sp0 + lane owns that partial's scale factors
+#pragma unroll
+        for (int h = 0; h < HM; ++h) {
+            const int sp = sp0 + c.lane;
+            f[h] = 0.f;
+            if (h < GQ && sp < count) {
+                const float* ph = base + size_t(sp) * W + h * (DH + 2);
+                f[h] = __expf(ldcg_f32(ph) - M[h]);
+                L[h] += ldcg_f32(ph + 1) * f[h];
+            }
+        }
+        const int nj = min(32, count - sp0);
+        for (int j0 = 0; j0 < nj; j0 += 4) {
+            float v[4][HM][DPL];
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < HM; ++h) {
+                    const bool ok = h < GQ && j0 + j < nj;
+                    const float* ph = base + size_t(sp0 + j0 + j) * W + h * (DH + 2) + 2 + d0;
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) v[j][h][e] = ok ? ldcg_f32(ph + e) : 0.f;
+                }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+#pragma unroll
+                for (int h = 0; h < HM; ++h) {
+                    const float fj = __shfl_sync(FULL, f[h], (j0 + j) & 31);
+#pragma unroll
+                    for (int e = 0; e < DPL; ++e) A[h][e] += v[j][h][e] * fj;
+                }
+        }
+    }
+#pragma unroll
+    for (int h = 0; h < HM; ++h) {
+        if (h >= GQ) continue;
+        float lsum = L[h];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(FULL, lsum, o);
+        uint16_t* out = a.attn + size_t(b) * s.d + (size_t(kvh) * GQ + h) * DH + d0;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) out[e] = f_to_bf16(A[h][e] / lsum);
+    }
+    if (c.lane == 0) atomicExch(a.acnt + pair, 0);
+}
 
-    float* q_s = reinterpret_cast<float*>(c.sm.act);          // [GQ][DH]
-    float* p_s = q_s + 8 * DH;                                  // [8 warps][32][9]
-    float* mw = p_s + DEC_NCW * 32 * 9;                         // [8][8]
-    float* lw = mw + 64;                                        // [8][8]
-    float* accw = lw + 64;                                      // [8][GQ*DH]
-    int* flag = reinterpret_cast<int*>(c.sm.misc + 16);
-
-    const float* qsrc = a.q + (size_t(b) * s.n_heads + size_t(kvh) * GQ) * DH;
-    for (int i = c.tid; i < GQ * DH; i += CONSUMER_THREADS) q_s[i] = ldcg_f32(qsrc + i);
-    csync();
-
-    const int* bt = a.block_table + size_t(c.slot[b]) * a.bt_stride;
-    const int t0 = split * ATT_SPLIT + c.warp * 32;
-    const int tok = t0 + c.lane;
+// One attention stage: RT tokens of (b, kvh); K rows at [0, 4 KB) and V rows
+// at [4 KB, 8 KB) of the ring slot (token r at row r), except the current
+// token, read from the paged cache (written by this step's QKV phase).
+template <int DH>
+__device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage& st, uint32_t qi, AttnState<DH>& stt,
+                                             const float* q_s, float* p_s, uint16_t* kpatch, uint16_t* vpatch) {
+    using CFG = AttnCfg<DH>;
+    constexpr int LPT = CFG::LPT, RT = CFG::RT, DPL = CFG::DPL, HM = CFG::HM;
+    const DecodeArgs& a = *c.a;
+    const Shape& s = a.s;
+    const int GQ = s.n_heads / s.n_kv;
+    const unsigned FULL = 0xffffffffu;
+    const int cur = c.pos[st.b], len = cur + 1;
+    const int t0 = st.s * RT;
+    const int tl = c.lane / LPT, part = c.lane % LPT;
+    const int tok = t0 + tl;
     const bool valid = tok < len;
-    float sc[8];
+    const int d0 = c.lane * DPL;
+    const float scale = rsqrtf(float(DH));
+    if (valid && tok == cur) {  // the current token's K/V half-rows from the paged cache
+        const int blk = ldcg_i32(a.block_table + size_t(c.slot[st.b]) * a.bt_stride + cur / KV_BLOCK_TOKENS);
+        const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
+        const uint8_t* kp = base + kv_offset(s, layer, 0, st.kvh, cur % KV_BLOCK_TOKENS) + part * 128;
+        const uint8_t* vp = base + kv_offset(s, layer, 1, st.kvh, cur % KV_BLOCK_TOKENS) + part * 128;
+        uint4 kv[8], vv[8];
 #pragma unroll
-    for (int h = 0; h < 8; ++h) sc[h] = 0.f;
+        for (int i = 0; i < 8; ++i) {
+            kv[i] = ldcg_u4(kp + i * 16);
+            vv[i] = ldcg_u4(vp + i * 16);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            reinterpret_cast<uint4*>(kpatch + part * 64)[i] = kv[i];
+            reinterpret_cast<uint4*>(vpatch + part * 64)[i] = vv[i];
+        }
+    }
+    uint32_t slot;
+    wait_stage(c, qi, slot);
+    __syncwarp();
+    const uint8_t* stage = c.sm.ring + size_t(slot) * DEC_STAGE_BYTES;
+    const uint8_t* krow = (tok == cur) ? reinterpret_cast<const uint8_t*>(kpatch) : stage + size_t(tl) * DH * 2;
+    float sc[HM];
+#pragma unroll
+    for (int h = 0; h < HM; ++h) sc[h] = 0.f;
     if (valid) {
-        int blk = ldcg_i32(bt + tok / KV_BLOCK_TOKENS);
-        const uint8_t* kp = a.kv_base + size_t(blk) * a.block_bytes +
-                            kv_offset(s, layer, 0, kvh, tok % KV_BLOCK_TOKENS);
+        // rotated 16-byte chunk order: the 8 lanes of a quarter-warp read 8
+        // different bank groups of their (128-byte strided) rows
 #pragma unroll
-        for (int cix = 0; cix < DH / 8; ++cix) {
-            uint4 kv = ldcg_u4(kp + cix * 16);
-            float kf[8] = {bf16_lo(kv.x), bf16_hi(kv.x), bf16_lo(kv.y), bf16_hi(kv.y),
-                           bf16_lo(kv.z), bf16_hi(kv.z), bf16_lo(kv.w), bf16_hi(kv.w)};
+        for (int i = 0; i < 8; ++i) {
+            const int cc = (i + tl) & 7;
+            const uint4 kv = *reinterpret_cast<const uint4*>(krow + part * 128 + cc * 16);
+            const float k[8] = {bf16_lo(kv.x), bf16_hi(kv.x), bf16_lo(kv.y), bf16_hi(kv.y),
+                                bf16_lo(kv.z), bf16_hi(kv.z), bf16_lo(kv.w), bf16_hi(kv.w)};
 #pragma unroll
-            for (int h = 0; h < 8; ++h) {
+            for (int h = 0; h < HM; ++h) {
                 if (h < GQ) {
-                    const float4* qv = reinterpret_cast<const float4*>(q_s + h * DH + cix * 8);
-                    float4 qa = qv[0], qb = qv[1];
-                    sc[h] += qa.x * kf[0] + qa.y * kf[1] + qa.z * kf[2] + qa.w * kf[3] + qb.x * kf[4] +
-                             qb.y * kf[5] + qb.z * kf[6] + qb.w * kf[7];
+                    const float* qh = q_s + h * DH + part * 64 + cc * 8;
+                    const float4 qa = *reinterpret_cast<const float4*>(qh);
+                    const float4 qb = *reinterpret_cast<const float4*>(qh + 4);
+                    sc[h] += qa.x * k[0] + qa.y * k[1] + qa.z * k[2] + qa.w * k[3] + qb.x * k[4] + qb.y * k[5] +
+                             qb.z * k[6] + qb.w * k[7];
                 }
             }
         }
     }
-    float m[8], l[8];
 #pragma unroll
-    for (int h = 0; h < 8; ++h) {
-        float x = valid ? sc[h] * scale : -INFINITY;
+    for (int h = 0; h < HM; ++h) {
+        if (h >= GQ) continue;
+        float x = sc[h];
+        if (LPT == 2) x += __shfl_xor_sync(FULL, x, 1);
+        x = valid ? x * scale : -INFINITY;
         float mx = x;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        float p = (valid && mx != -INFINITY) ? __expf(x - mx) : 0.f;
-        float ls = p;
+        for (int o = 16; o >= LPT; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
+        const float mnew = fmaxf(stt.m[h], mx);  // finite: token t0 is valid
+        const float corr = __expf(stt.m[h] - mnew);
+        const float pv = valid ? __expf(x - mnew) : 0.f;
+        float ps = part == 0 ? pv : 0.f;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ls += __shfl_xor_sync(0xffffffffu, ls, o);
-        m[h] = mx;
-        l[h] = ls;
-        if (h < GQ) p_s[(c.warp * 32 + c.lane) * 9 + h] = p;
+        for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(FULL, ps, o);
+        stt.l[h] = stt.l[h] * corr + ps;
+        stt.m[h] = mnew;
+#pragma unroll
+        for (int e = 0; e < DPL; ++e) stt.acc[h][e] *= corr;
+        if (part == 0) p_s[tl * 9 + h] = pv;
     }
     __syncwarp();
-    float acc[8][DPL];
-#pragma unroll
-    for (int h = 0; h < 8; ++h)
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) acc[h][e] = 0.f;
-    int nvalid = min(32, len - t0);
-    const int d0 = c.lane * DPL;
+    const int nvalid = min(RT, len - t0);
     for (int j = 0; j < nvalid; ++j) {
-        int tk = t0 + j;
-        int blk = ldcg_i32(bt + tk / KV_BLOCK_TOKENS);
-        const uint8_t* vp = a.kv_base + size_t(blk) * a.block_bytes +
-                            kv_offset(s, layer, 1, kvh, tk % KV_BLOCK_TOKENS) + d0 * 2;
+        const uint16_t* vrow = (t0 + j == cur)
+                                   ? vpatch + d0
+                                   : reinterpret_cast<const uint16_t*>(stage + 4096 + size_t(j) * DH * 2) + d0;
         float vf[DPL];
         if constexpr (DPL == 2) {
-            uint32_t vv = ldcg_u32(vp);
+            const uint32_t vv = *reinterpret_cast<const uint32_t*>(vrow);
             vf[0] = bf16_lo(vv);
             vf[1] = bf16_hi(vv);
         } else {
-            uint2 vv = ldcg_u2(vp);
+            const uint2 vv = *reinterpret_cast<const uint2*>(vrow);
             vf[0] = bf16_lo(vv.x);
             vf[1] = bf16_hi(vv.x);
             vf[2] = bf16_lo(vv.y);
             vf[3] = bf16_hi(vv.y);
         }
-        const float* pj = p_s + (c.warp * 32 + j) * 9;
+        const float* pj = p_s + j * 9;
 #pragma unroll
-        for (int h = 0; h < 8; ++h) {
+        for (int h = 0; h < HM; ++h) {
             if (h < GQ) {
-                float pv = pj[h];
+                const float pv = pj[h];
 #pragma unroll
-                for (int e = 0; e < DPL; ++e) acc[h][e] += pv * vf[e];
+                for (int e = 0; e < DPL; ++e) stt.acc[h][e] += pv * vf[e];
             }
         }
     }
-#pragma unroll
-    for (int h = 0; h < 8; ++h) {
-        if (h < GQ) {
-            if (c.lane == 0) {
-                mw[c.warp * 8 + h] = m[h];
-                lw[c.warp * 8 + h] = l[h];
-            }
-#pragma unroll
-            for (int e = 0; e < DPL; ++e) accw[(c.warp * GQ + h) * DH + d0 + e] = acc[h][e];
-        }
-    }
-    csync();
-    // combine the 8 warps -> this split's partial
-    float* part = a.apart + ((size_t(b) * s.n_kv + kvh) * ATT_MAX_SPLITS + split) * GQ * (DH + 2);
-    for (int i = c.tid; i < GQ * DH; i += CONSUMER_THREADS) {
-        int h = i / DH, dd = i % DH;
-        float M = -INFINITY;
-        for (int w = 0; w < DEC_NCW; ++w) M = fmaxf(M, mw[w * 8 + h]);
-        float L = 0.f, A = 0.f;
-        for (int w = 0; w < DEC_NCW; ++w) {
-            float mwv = mw[w * 8 + h];
-            if (mwv == -INFINITY) continue;
-            float f = __expf(mwv - M);
-            L += lw[w * 8 + h] * f;
-            A += accw[(w * GQ + h) * DH + dd] * f;
-        }
-        float* ph = part + h * (DH + 2);
-        ph[2 + dd] = A;
-        if (dd == 0) {
-            ph[0] = M;
-            ph[1] = L;
-        }
-    }
-    __threadfence();
-    csync();
-    if (c.tid == 0) {
-        int old = atomicAdd(a.acnt + b * s.n_kv + kvh, 1);
-        *flag = (old == nsplit - 1);
-    }
-    csync();
-    if (*flag) {
-        __threadfence();
-        const float* base = a.apart + (size_t(b) * s.n_kv + kvh) * ATT_MAX_SPLITS * GQ * (DH + 2);
-        for (int i = c.tid; i < GQ * DH; i += CONSUMER_THREADS) {
-            int h = i / DH, dd = i % DH;
-            float M = -INFINITY;
-            for (int sp = 0; sp < nsplit; ++sp) M = fmaxf(M, ldcg_f32(base + (sp * GQ + h) * (DH + 2)));
-            float L = 0.f, A = 0.f;
-            for (int sp = 0; sp < nsplit; ++sp) {
-                const float* ph = base + (sp * GQ + h) * (DH + 2);
-                float f = __expf(ldcg_f32(ph) - M);
-                L += ldcg_f32(ph + 1) * f;
-                A += ldcg_f32(ph + 2 + dd) * f;
-            }
-            a.attn[size_t(b) * s.d + (size_t(kvh) * GQ + h) * DH + dd] = f_to_bf16(A / L);
-        }
-        if (c.tid == 0) atomicExch(a.acnt + b * s.n_kv + kvh, 0);
-    }
-    csync();
+    release_stage(c, slot);  // its __syncwarp also retires the p_s / patch reads
 }
 
-__device__ void run_attention(Ctx& c, int layer) {
-    const Shape& s = c.a->s;
-    int total = 0;
-    int per_b[DEC_MAXB];
-    for (int b = 0; b < c.B; ++b) {
-        per_b[b] = s.n_kv * ((c.pos[b] + ATT_SPLIT) / ATT_SPLIT);  // ceil((pos+1)/SPLIT)
-        total += per_b[b];
-    }
-    for (int u = c.cta; u < total; u += c.G) {
-        int b = 0, r = u;
-        while (r >= per_b[b]) {
-            r -= per_b[b];
-            ++b;
+template <int DH>
+__device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPlan& ap) {
+    using CFG = AttnCfg<DH>;
+    constexpr int HM = CFG::HM, DPL = CFG::DPL;
+    const DecodeArgs& a = *c.a;
+    const Shape& s = a.s;
+    const int GQ = s.n_heads / s.n_kv;
+    uint8_t* wbase = reinterpret_cast<uint8_t*>(c.sm.act) + c.warp * CFG::WARP_SMEM;
+    float* q_s = reinterpret_cast<float*>(wbase);                        // [GQ][DH]
+    float* p_s = q_s + 512;                                              // [RT][9]
+    uint16_t* kpatch = reinterpret_cast<uint16_t*>(p_s + CFG::RT * 9);  // [DH]
+    uint16_t* vpatch = kpatch + DH;                                      // [DH]
+    const int n = ap.a1 - ap.a0;
+    AttnState<DH> stt;
+    int cur_pair = -1, cur_b = 0, cur_kvh = 0, cur_lo = 0, cur_n = 0;
+    for (int i = c.warp; i < n; i += DEC_NCW) {
+        const AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0 + i);
+        if (st.pair != cur_pair) {
+            if (cur_pair >= 0) attn_flush<DH>(c, ap, cur_b, cur_kvh, cur_lo, cur_n, stt);
+            cur_pair = st.pair;
+            cur_b = st.b;
+            cur_kvh = st.kvh;
+            cur_lo = st.pair_lo;
+            cur_n = ap.nst[st.b];
+            const float4* qsrc =
+                reinterpret_cast<const float4*>(a.q + (size_t(st.b) * s.n_heads + size_t(st.kvh) * GQ) * DH);
+            float4 qv[4];  // GQ * DH <= 512 floats -> 4 float4 per lane
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int e = c.lane + 32 * k;
+                qv[k] = e * 4 < GQ * DH ? __ldcg(qsrc + e) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int e = c.lane + 32 * k;
+                if (e * 4 < GQ * DH) reinterpret_cast<float4*>(q_s)[e] = qv[k];
+            }
+#pragma unroll
+            for (int h = 0; h < HM; ++h) {
+                stt.m[h] = -INFINITY;
+                stt.l[h] = 0.f;
+#pragma unroll
+                for (int e = 0; e < DPL; ++e) stt.acc[h][e] = 0.f;
+            }
+            __syncwarp();
         }
-        int nsplit = per_b[b] / s.n_kv;
-        int kvh = r / nsplit, split = r % nsplit;
-        if (s.dh == 64)
-            attn_unit<64>(c, layer, b, kvh, split);
-        else
-            attn_unit<128>(c, layer, b, kvh, split);
+        attn_consume<DH>(c, layer, st, c.q + i, stt, q_s, p_s, kpatch, vpatch);
     }
+    if (cur_pair >= 0) attn_flush<DH>(c, ap, cur_b, cur_kvh, cur_lo, cur_n, stt);
+    c.q += n;
 }
 
 // ------------------------------------------------------------ embedding
-__device__ void run_embed(Ctx& c) {
+__device__ __forceinline__ void run_embed(Ctx& c) {
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
     if (c.cta == 0) {
@@ -581,15 +936,14 @@ __device__ void run_embed(Ctx& c) {
         for (int i = c.tid; i < dsc->n_upd; i += CONSUMER_THREADS)
             a.block_table[size_t(dsc->upd[i][0]) * a.bt_stride + dsc->upd[i][1]] = dsc->upd[i][2];
     }
-    int nt = s.d / 16;
-    int items = DEC_MAXB * nt;
+    const int nt = s.d / 16, items = DEC_MAXB * nt;
     for (int it = c.cta * DEC_NCW + c.warp; it < items; it += c.G * DEC_NCW) {
-        int b = it / nt, tile = it % nt;
+        const int b = it / nt, tile = it % nt;
         float sq = 0.f;
         if (b < c.B && c.lane < 16) {
-            int tok = ldcg_i32(a.last_tok + c.slot[b]);
-            int row = tile * 16 + c.lane;
-            float hv = bf16_to_f(a.w.emb[size_t(tok) * s.d + row]);
+            const int tok = ldcg_i32(a.last_tok + c.slot[b]);
+            const int row = tile * 16 + c.lane;
+            const float hv = bf16_to_f(a.w.emb[size_t(tok) * s.d + row]);
             a.h[size_t(b) * s.d + row] = hv;
             a.act[size_t(b) * s.d + row] = f_to_bf16(hv * a.w.g_attn[row]);
             sq = hv * hv;
@@ -600,20 +954,18 @@ __device__ void run_embed(Ctx& c) {
     }
 }
 
-__device__ void run_argmax_combine(Ctx& c, float best_v[2], int best_i[2]) {
+__device__ __forceinline__ void run_argmax_combine(Ctx& c, float best_v[2], int best_i[2]) {
     const DecodeArgs& a = *c.a;
-    // reduce over the 8 lanes sharing t, then across warps through smem
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
+    for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int o = 4; o < 32; o <<= 1) {
-            float ov = __shfl_xor_sync(0xffffffffu, best_v[j], o);
-            int oi = __shfl_xor_sync(0xffffffffu, best_i[j], o);
+            const float ov = __shfl_xor_sync(0xffffffffu, best_v[j], o);
+            const int oi = __shfl_xor_sync(0xffffffffu, best_i[j], o);
             better(best_v[j], best_i[j], ov, oi);
         }
-    }
-    float* wv = c.sm.misc + 32;                              // [8 warps][8]
-    int* wi = reinterpret_cast<int*>(c.sm.misc + 96);        // [8 warps][8]
+    float* wv = c.sm.misc + 32;                        // [8 warps][8]
+    int* wi = reinterpret_cast<int*>(c.sm.misc + 96);  // [8 warps][8]
     int* flag = reinterpret_cast<int*>(c.sm.misc + 16);
     if (c.lane < 4) {
         wv[c.warp * 8 + 2 * c.lane] = best_v[0];
@@ -629,62 +981,83 @@ __device__ void run_argmax_combine(Ctx& c, float best_v[2], int best_i[2]) {
         a.arg_val[c.cta * 8 + c.tid] = bv;
         a.arg_idx[c.cta * 8 + c.tid] = bi;
     }
-    __threadfence();
     csync();
-    if (c.tid == 0) {
-        int old = atomicAdd(a.arg_cnt, 1);
-        *flag = (old == c.G - 1);
-    }
+    if (c.tid == 0) *flag = atom_add_acq_rel_gpu(a.arg_cnt, 1) == c.G - 1;
     csync();
     if (*flag) {
-        __threadfence();
-        if (c.tid < c.B) {
-            float bv = -INFINITY;
-            int bi = 0x7fffffff;
-            for (int k = 0; k < c.G; ++k)
-                better(bv, bi, ldcg_f32(a.arg_val + k * 8 + c.tid), ldcg_i32(a.arg_idx + k * 8 + c.tid));
-            a.tok_out[c.tid] = bi;
-            a.last_tok[c.slot[c.tid]] = bi;
+        const int b = c.warp;  // warp b reduces CTA partials lane, lane + 32, ...
+        if (b < c.B) {
+            float bv = -INFINITY, vv[8];
+            int bi = 0x7fffffff, ii[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+                const int cta = c.lane + 32 * k;
+                vv[k] = cta < c.G ? ldcg_f32(a.arg_val + cta * 8 + b) : -INFINITY;
+                ii[k] = cta < c.G ? ldcg_i32(a.arg_idx + cta * 8 + b) : 0x7fffffff;
+            }
+#pragma unroll
+            for (int k = 0; k < 8; ++k) better(bv, bi, vv[k], ii[k]);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+                const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+                better(bv, bi, ov, oi);
+            }
+            if (c.lane == 0) {
+                a.tok_out[b] = bi;
+                a.last_tok[c.slot[b]] = bi;
+            }
         }
         if (c.tid == 0) atomicExch(a.arg_cnt, 0);
     }
 }
 
-__global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_constant__ DecodeArgs a) {
+__global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_constant__ DecodeArgs args) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
+    __shared__ DecodeArgs a_s;  // launch arguments, read with LDS instead of generic param loads
+    __shared__ int slot_s[DEC_MAXB], pos_s[DEC_MAXB];
     Smem sm = carve(smem_raw);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int B = args.desc->B;
     if (threadIdx.x == 0) {
+        a_s = args;
         for (int i = 0; i < DEC_NSTAGE; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 1);
         }
         fence_mbar_init();
     }
-    // zero the accumulation buffers
-    for (int i = threadIdx.x; i < 2 * DEC_MAXT * 128; i += DEC_THREADS) sm.acc[i] = 0.f;
+    if (threadIdx.x < DEC_MAXB) {
+        slot_s[threadIdx.x] = int(threadIdx.x) < B ? args.desc->slot[threadIdx.x] : 0;
+        pos_s[threadIdx.x] = int(threadIdx.x) < B ? args.desc->pos[threadIdx.x] : 0;
+    }
+    // block-table rows of the step's requests (entries that predate this step)
+    for (int i = threadIdx.x; i < DEC_MAXB * DEC_BT_MAX; i += DEC_THREADS) {
+        const int b = i / DEC_BT_MAX, k = i % DEC_BT_MAX;
+        sm.bt[i] = (b < B && k < args.bt_stride) ? args.block_table[size_t(args.desc->slot[b]) * args.bt_stride + k] : 0;
+    }
     __syncthreads();
+    const DecodeArgs& a = a_s;
 
     if (warp == DEC_NCW) {
-        if (lane == 0) producer_loop(a, sm, blockIdx.x, gridDim.x);
+        if (lane == 0) producer_loop(a, sm, blockIdx.x, gridDim.x, B, pos_s);
         return;
     }
     Ctx c;
-    c.a = &a;
+    c.ntrace = 0;
+    c.a = &a_s;
     c.sm = sm;
     c.cta = blockIdx.x;
     c.G = gridDim.x;
     c.warp = warp;
     c.lane = lane;
     c.tid = threadIdx.x;
-    c.B = a.desc->B;
-    for (int b = 0; b < DEC_MAXB; ++b) {
-        c.slot[b] = b < c.B ? a.desc->slot[b] : 0;
-        c.pos[b] = b < c.B ? a.desc->pos[b] : 0;
-    }
+    c.B = B;
+    c.slot = slot_s;
+    c.pos = pos_s;
     c.q = 0;
     c.off = 0;
-    c.accbuf = 0;
+    const AttnPlan ap = attn_plan(a.s, B, pos_s, c.cta, c.G);
 
     float best_v[2] = {-INFINITY, -INFINITY};
     int best_i[2] = {0x7fffffff, 0x7fffffff};
@@ -694,7 +1067,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     for (int l = 0; l < a.s.n_layers; ++l) {
         run_gemv(c, PH_QKV, l, best_v, best_i);
         grid_sync(c);
-        run_attention(c, l);
+        trace(c, 6);
+        if (!(a.skip & 1)) {
+            if (a.s.dh == 64)
+                run_attention_t<64>(c, l, ap);
+            else
+                run_attention_t<128>(c, l, ap);
+        }
+        trace(c, 7);
         grid_sync(c);
         run_gemv(c, PH_O, l, best_v, best_i);
         grid_sync(c);
@@ -710,14 +1090,14 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
 }  // namespace
 
 size_t decode_apart_floats(const Shape& s) {
-    return size_t(DEC_MAXB) * s.n_kv * ATT_MAX_SPLITS * s.gq() * (s.dh + 2);
+    const int rt = 2048 / s.dh;
+    return size_t(DEC_MAXB) * s.n_kv * ((s.max_seq + rt - 1) / rt) * s.gq() * (s.dh + 2);
 }
 
 cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {
-        cudaError_t e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             DEC_SMEM_TOTAL);
+        cudaError_t e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM_TOTAL);
         if (e != cudaSuccess) return e;
         configured = true;
     }

@@ -12,18 +12,19 @@ constexpr int DEC_NSTAGE = 16;                   // weight ring depth
 constexpr int DEC_STAGE_BYTES = 8192;            // 16 rows x 256 cols bf16
 constexpr int DEC_CHUNK_COLS = 256;
 constexpr int DEC_KSEG_MAX = 4096;  // activation columns resident in smem at once
-constexpr int DEC_MAXT = 16;        // tiles accumulated per group
+constexpr int DEC_MAXT = 4;         // tiles accumulated per group
 constexpr int DEC_MAXB = 8;         // batch columns of the mma (n = 8)
-constexpr int ATT_SPLIT = 256;      // context tokens per attention work unit
-constexpr int ATT_MAX_SPLITS = 32;  // supports contexts up to 8192
+constexpr int DEC_BT_MAX = 256;     // block-table entries per request -> contexts up to 4096 tokens
 constexpr int MAX_BT_UPDATES = 64;
 
 constexpr int DEC_SMEM_RING = DEC_NSTAGE * DEC_STAGE_BYTES;
 constexpr int DEC_SMEM_ACT = DEC_MAXB * (DEC_KSEG_MAX + 8) * 2;
-constexpr int DEC_SMEM_ACC = 2 * DEC_MAXT * 128 * 4;
+constexpr int DEC_SMEM_ACC = DEC_NCW * DEC_MAXT * 128 * 4;  // per-warp tile partials
 constexpr int DEC_SMEM_BARS = 2 * DEC_NSTAGE * 8;
 constexpr int DEC_SMEM_MISC = 1024;
-constexpr int DEC_SMEM_TOTAL = DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS + DEC_SMEM_MISC;
+constexpr int DEC_SMEM_BT = DEC_MAXB * DEC_BT_MAX * 4;
+constexpr int DEC_SMEM_TOTAL =
+    DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS + DEC_SMEM_MISC + DEC_SMEM_BT;
 
 // Per-step input written by the host (one H2D copy) before the launch.
 struct StepDesc {
@@ -51,8 +52,8 @@ struct DecodeArgs {
     float* q;          // [8][n_heads][dh] roped queries
     float* ssA;        // [d/16][8] sum-of-squares partials feeding QKV / lm_head
     float* ssB;        // [d/16][8] ... feeding gate/up
-    float* apart;      // attention split partials
-    int* acnt;         // [8][n_kv] split arrival counters (self-resetting)
+    float* apart;      // attention partials: [stage slot][gq][m, l, acc[dh]]
+    int* acnt;         // [8][n_kv] partial arrival counters (self-resetting)
     float* arg_val;    // [grid][8]
     int* arg_idx;      // [grid][8]
     int* arg_cnt;      // [1] (self-resetting)
@@ -60,6 +61,11 @@ struct DecodeArgs {
     int* tok_out;      // [8]
     unsigned int* bar_count;
     unsigned int* bar_gen;
+    volatile int* progress;  // optional host-mapped [grid][2]: consumer phase, producer stage
+    unsigned long long* trace;  // optional [4096]: %globaltimer at CTA 0's phase boundaries
+    int nstage;    // weight-ring stages in use (<= DEC_NSTAGE): bounds bytes in flight per SM
+    int l2_ahead;  // extra stages prefetched into L2 beyond the ring
+    int skip;      // debug: 1 skips attention work, 2 skips the GEMV phases (results are garbage)
 };
 
 cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t stream);

@@ -59,7 +59,7 @@ def test_generator_weights_bit_exact(gpu, name):
     gpu.create_instance(iid, shape, seed=77)
     try:
         d, ff = shape.d_model, shape.d_ff
-        checks = [(T_WQ, 1, 5, d), (T_WK, 0, shape.d_head + 3, d), (T_WV, 1, 2, d), (T_WO, 0, 7, d),
+        checks = [(T_WQ, 1, 5, d), (T_WK, 0, shape.n_kv_heads * shape.d_head - 3, d), (T_WV, 1, 2, d), (T_WO, 0, 7, d),
                   (T_WGATE, 1, 9, d), (T_WUP, 0, ff - 1, d), (T_WDOWN, 1, d - 2, ff)]
         if not shape.tied:
             checks.append((T_LM, 0, shape.vocab - 5, d))

@@ -1,0 +1,418 @@
+#!/usr/bin/env python
+"""Benchmark of the co-located token step on B200 (driver contract).
+
+Workload (BASELINE.json configs[1], "C2"): four co-located Llama-shaped models
+[1.1B, 3B, 1.1B, 3B] (random-init weights, synthetic prompts) on one B200,
+sharing the GPU's VMM KV pool; every instance serves a full batch of 8
+requests whose lengths come from the C2 scenario's length dataset; finished
+requests are replaced by new ones (prefill first, as select_next does).
+
+  step    one instance step of the co-located schedule (the planned decode of
+          that instance's batch, or the prefill of a newly admitted request),
+          launched through the mesh_gpu C ABI; instances take turns.
+  value   co-located tokens/s over the K timed steps (device-resident inputs),
+          counting only tokens of requests whose emissions met the TTFT/TPOT
+          SLO; wall clock between device synchronisations.
+  e2e     the same metric through the reference-facing plugin API
+          (llmmesh.h: llm_experiment_run with the GPU attached) on the C2
+          Poisson trace: control plane + per-step H2D descriptors/prompts +
+          D2H tokens inside the timed region.
+  roofline  dominant kernel = the persistent decode kernel; algorithmic bytes
+          per launch = W_m + sum_i L_i C_m + B C_m + B d_m 2 over its
+          CUDA-event duration, vs the measured HBM copy peak.
+
+`--impl reference` times the reference's own CPU path (its simulator, built
+from /root/reference by oracle/Makefile into oracle/_ref) on the same trace.
+Multi-GPU (torchrun): every rank runs an independent co-located node (instances
+shard by placement, no collective): weak scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SCEN = os.path.join(ROOT, "tests", "golden", "ctrl", "c2_colocated")
+METRIC = "co-located tokens/s at TTFT/TPOT SLO per B200"
+UNIT = "tokens/s"
+MODELS = ["1b", "3b", "1b", "3b"]
+BATCH = 8
+E2E_WINDOW_S = 20.0
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+class Dist:
+    def __init__(self):
+        self.ws, self.rank, self.local = dist_env()
+        self.pg = None
+        if self.ws > 1:
+            import torch
+            import torch.distributed as dist
+            backend = "nccl" if torch.cuda.is_available() else "gloo"
+            if backend == "nccl":
+                torch.cuda.set_device(self.local)
+            dist.init_process_group(backend=backend)
+            self.dist, self.torch, self.backend = dist, torch, backend
+
+    def barrier(self):
+        if self.ws > 1:
+            self.dist.barrier()
+
+    def reduce(self, x: float, op: str) -> float:
+        if self.ws == 1:
+            return x
+        t = self.torch.tensor([x], dtype=self.torch.float64,
+                              device=f"cuda:{self.local}" if self.backend == "nccl" else "cpu")
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX if op == "max" else self.dist.ReduceOp.SUM)
+        return float(t.item())
+
+    def close(self):
+        if self.ws > 1:
+            self.dist.destroy_process_group()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 7:
+                self.samples.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons}
+
+
+def load_lengths():
+    rows = []
+    with open(os.path.join(SCEN, "lengths.csv")) as fh:
+        next(fh)
+        for line in fh:
+            a, b = line.strip().split(",")
+            rows.append((int(a), int(b)))
+    return rows
+
+
+class Colocated:
+    """The C2 node: four instances, each with a full batch, served in turns."""
+
+    def __init__(self, device: int, seed: int = 7):
+        import random
+
+        from paper_2507_00507_b200.gpu import SHAPES, MeshGpu
+        self.g = MeshGpu(device, kv_pool_bytes=48 << 30, prompt_seed=seed)
+        self.shapes = [SHAPES[m] for m in MODELS]
+        self.rng = random.Random(seed)
+        self.lengths = load_lengths()
+        self.next_rid = 0
+        self.insts = []
+        for iid, shape in enumerate(self.shapes):
+            self.g.create_instance(iid, shape, seed=1000 + iid)
+            kv = BATCH * shape.max_seq_len * shape.kv_bytes_per_token
+            self.g.kv_resize(iid, 0, kv)
+            self.insts.append({"id": iid, "shape": shape, "reqs": [], "pending": []})
+        self.clock = 0.0  # device-time clock (s) for SLO accounting
+        self.tokens_ok = 0
+        self.tokens_all = 0
+        self.violations = 0
+        self.completed = 0
+        self.decode_bytes = 0.0
+        self.decode_kernel_ms = 0.0
+        self.decode_steps = 0
+
+    def new_request(self, inst):
+        i, o = self.lengths[self.rng.randrange(len(self.lengths))]
+        cap = inst["shape"].max_seq_len
+        if i + o > cap:
+            o = max(1, cap - i)
+        r = {"rid": self.next_rid, "I": i, "O": o, "gen": 0, "sched": 0, "arrival": self.clock, "ok": True}
+        self.next_rid += 1
+        inst["pending"].append(r)
+
+    def fill(self):
+        for inst in self.insts:
+            while len(inst["reqs"]) + len(inst["pending"]) < BATCH:
+                self.new_request(inst)
+
+    def plan(self, k):
+        """Step k of the schedule: instance k mod 4; a pending request is prefilled first."""
+        inst = self.insts[k % len(self.insts)]
+        if inst["pending"]:
+            return inst, "prefill", [inst["pending"][0]]
+        return inst, "decode", list(inst["reqs"])
+
+    def launch(self, inst, kind, reqs):
+        if kind == "prefill":
+            r = reqs[0]
+            return self.g.step_async(inst["id"], prefill=r["rid"], prefill_len=r["I"], input_len=r["I"])
+        return self.g.step_async(inst["id"], decode=[r["rid"] for r in reqs])
+
+    def schedule_effects(self, inst, kind, reqs):
+        """Host-side state the next plans depend on (known without waiting for the GPU)."""
+        if kind == "prefill":
+            r = inst["pending"].pop(0)
+            r["sched"] = 1
+            if r["sched"] >= r["O"]:
+                self.new_request(inst)
+            else:
+                inst["reqs"].append(r)
+            return
+        for r in reqs:
+            r["sched"] += 1
+        for r in [r for r in reqs if r["sched"] >= r["O"]]:
+            inst["reqs"].remove(r)
+            self.new_request(inst)
+
+    def run(self, steps):
+        """Launch `steps` steps asynchronously (<= 24 outstanding), retire them in order."""
+        from collections import deque
+        inflight = deque()
+        launches0 = self.g.stats()["kernel_launches"]
+        for _ in range(steps):
+            inst, kind, reqs = self.plan(self.k)
+            self.k += 1
+            inflight.append((self.launch(inst, kind, reqs), inst, kind, reqs))
+            self.schedule_effects(inst, kind, reqs)
+            while len(inflight) > 24:
+                self.retire(inflight.popleft())
+        while inflight:
+            self.retire(inflight.popleft())
+        return self.g.stats()["kernel_launches"] - launches0
+
+    def retire(self, item):
+        """Step finished: advance the device-time clock, account tokens against the SLO."""
+        t, inst, kind, reqs = item
+        self.g.wait(t)
+        st = self.g.stats()
+        self.clock += st["last_step_ms"] / 1e3
+        if kind == "decode":
+            s = inst["shape"]
+            ctx = sum(r["I"] + r["gen"] for r in reqs)
+            self.decode_bytes += (s.weight_bytes_streamed + ctx * s.kv_bytes_per_token +
+                                  len(reqs) * s.kv_bytes_per_token + len(reqs) * s.d_model * 2)
+            self.decode_kernel_ms += st["last_kernel_ms"]
+            self.decode_steps += 1
+        for r in reqs:
+            deadline = r["arrival"] + max(2.0, r["I"] / 512.0) + 0.25 * r["gen"]
+            if self.clock > deadline + 1e-9:
+                r["ok"] = False
+            r["gen"] += 1
+            self.tokens_all += 1
+            self.tokens_ok += 1 if r["ok"] else 0
+            if r["gen"] >= r["O"]:
+                self.g.request_free(inst["id"], r["rid"])
+                self.completed += 1
+                self.violations += 0 if r["ok"] else 1
+
+    def reset_counters(self):
+        self.tokens_ok = self.tokens_all = self.completed = self.violations = 0
+        self.decode_bytes = self.decode_kernel_ms = 0.0
+        self.decode_steps = 0
+
+
+def cpu_reference_sample(window_s: float):
+    """The reference's CPU path (its simulator) on the C2 trace: tokens / wall s, 1 core."""
+    ref = os.path.join(ROOT, "oracle", "_ref", "ref_capture")
+    if not os.path.exists(ref):
+        return None
+    out = subprocess.run([ref, "time", os.path.join(SCEN, "config.json"), "5", f"workload.window_s={window_s}"],
+                         cwd=ROOT, capture_output=True, text=True)
+    if out.returncode != 0:
+        return None
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    return {"value": r["tokens"] / r["best_s"], "unit": UNIT, "cores": 1, "kind": "reference",
+            "sample": f"reference simulator (oracle/_ref) on the C2 trace, window {window_s:g} s: "
+                      f"{r['tokens']} tokens, {r['events']} events, best of 5 = {r['best_s']:.4f} s"}
+
+
+def run_reference(args, d: Dist):
+    if d.rank != 0:
+        return
+    ref = os.path.join(ROOT, "oracle", "_ref", "ref_capture")
+    if not os.path.exists(ref):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
+        return
+    times, tokens = [], 0
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        out = subprocess.run([ref, "time", os.path.join(SCEN, "config.json"), "1",
+                              f"workload.window_s={E2E_WINDOW_S}"], cwd=ROOT, capture_output=True, text=True)
+        dt = time.perf_counter() - t0
+        r = json.loads(out.stdout.strip().splitlines()[-1])
+        if i >= args.warmup:
+            times.append(r["best_s"])
+            tokens += r["tokens"]
+    total = sum(times)
+    value = tokens / total
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": "C2: 4 co-located [1b,3b,1b,3b], Poisson trace 1.5 req/s/fn",
+                       "trace_window_s": E2E_WINDOW_S, "step": "one full simulation of the C2 trace window"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
+                             "sample": f"reference simulator, {args.steps} runs of the {E2E_WINDOW_S:g} s C2 trace"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def run_e2e(device: int):
+    """C2 trace through llmmesh.h with the B200 data plane attached (parity-mode schedule)."""
+    import tempfile
+
+    from paper_2507_00507_b200 import control, gpu
+    with control.Experiment(os.path.join(SCEN, "config.json")) as exp:
+        exp.set("workload.window_s", E2E_WINDOW_S)
+        exp.set("output.event_log", "false")
+        exp.out_dir(tempfile.mkdtemp(prefix="mesh_e2e_"))
+        exp.attach_gpu([device], 48 << 30, gpu.LIB_PATH)
+        t0 = time.perf_counter()
+        exp.run()
+        wall = time.perf_counter() - t0
+        m = {k: exp.metric(k) for k in ["gpu.steps", "gpu.decode_tokens", "gpu.h2d_bytes", "gpu.d2h_bytes",
+                                        "gpu.device_ms", "slo_compliant_rate", "total_requests",
+                                        "gpu.kernel_launches"]}
+    prefill_emits = m["total_requests"]  # one token per admitted request's prefill
+    tokens = m["gpu.decode_tokens"] + prefill_emits
+    steps = max(1.0, m["gpu.steps"])
+    return {"value": tokens * m["slo_compliant_rate"] / wall, "unit": UNIT,
+            "h2d_bytes_per_step": m["gpu.h2d_bytes"] / steps, "d2h_bytes_per_step": m["gpu.d2h_bytes"] / steps,
+            "wall_s": wall, "device_s": m["gpu.device_ms"] / 1e3, "steps": int(steps),
+            "slo_compliant_rate": m["slo_compliant_rate"], "tokens": int(tokens),
+            "api": "llmmesh.h llm_experiment_run + llm_experiment_attach_gpu"}
+
+
+def run_ours(args, d: Dist):
+    device = d.local
+    hbm, peak_kind = peaks()
+    node = Colocated(device)
+    node.k = 0
+    node.fill()
+    # initial admissions: every instance prefills its batch (untimed)
+    node.run(len(MODELS) * BATCH)
+    node.run(args.warmup * len(MODELS))
+    node.g.sync()
+    node.reset_counters()
+    d.barrier()
+    with Clocks(device) as clk:
+        node.g.sync()
+        t0 = time.perf_counter()
+        launches = node.run(args.steps)
+        node.g.sync()
+        wall = time.perf_counter() - t0
+    wall_max = d.reduce(wall, "max")
+    tok_ok = d.reduce(float(node.tokens_ok), "sum")
+    value = tok_ok / wall_max
+    achieved = node.decode_bytes / (node.decode_kernel_ms / 1e3) / 1e9 if node.decode_kernel_ms else 0.0
+    e2e = run_e2e(device) if not args.no_e2e else None
+    if d.rank != 0:
+        return
+    cpu = cpu_reference_sample(E2E_WINDOW_S) if d.ws == 1 else None
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "decode_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.ws, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * wall_max / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, synthetic prompts)",
+        "config": {"workload": "C2: 4 co-located Llama-shaped instances [1.1B, 3B, 1.1B, 3B] on one B200, "
+                               "batch 8 each, shared VMM KV pool",
+                   "models": MODELS, "batch_per_instance": BATCH, "step": "one instance step (decode of its batch "
+                   "or prefill of a newly admitted request), instances in turn",
+                   "l2": "weights 17 GB + KV streamed per 4-step round >> 126 MB L2",
+                   "slo_compliant_tokens": int(node.tokens_ok), "tokens": int(node.tokens_all),
+                   "completed_requests": node.completed, "slo_violations": node.violations,
+                   "decode_steps": node.decode_steps, "parallelism": f"{d.ws} independent co-located nodes"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                     "frac": achieved / hbm if hbm else None, "traffic": traffic,
+                     "kernel": "decode_kernel (persistent, TMA-ring)", "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": node.decode_bytes / max(1, node.decode_steps)},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    print(json.dumps(line))
+
+
+def main():
+    os.chdir(ROOT)  # scenario configs use repo-relative paths
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    d = Dist()
+    try:
+        if args.impl == "reference":
+            run_reference(args, d)
+        else:
+            run_ours(args, d)
+    finally:
+        d.close()
+
+
+if __name__ == "__main__":
+    main()

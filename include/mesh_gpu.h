@@ -75,7 +75,9 @@ typedef struct mesh_gpu_stats {
     int64_t swap_out_bytes, swap_in_bytes, migrate_bytes;
     int64_t steps, decode_tokens, prefill_tokens;
     double last_step_ms;          /* device time of the last waited step (CUDA events) */
-    double last_kernel_ms;        /* device time of its dominant kernel */
+    double last_kernel_ms;        /* device time of its kernels (descriptor copy excluded) */
+    int64_t kernel_launches;      /* kernels launched by steps */
+    int64_t h2d_bytes, d2h_bytes; /* per-step host<->device traffic (descriptors, prompts, tokens) */
 } mesh_gpu_stats;
 
 const char* mesh_gpu_version(void);

@@ -137,19 +137,29 @@ void GpuExecutor::iteration_start(const Cluster& c, const Node& nd, const Instan
 }
 
 void GpuExecutor::iteration_done(const Cluster&, const Node& nd, const IterationPlan&, const IterationOutcome&) {
-    mesh_gpu* h = handle_for_node(nd.id);
+    // Steps stay asynchronous: their tickets are retired lazily (bounded by the
+    // data plane's ticket ring), so the host keeps scheduling while the GPU runs.
     auto it = tickets_.find(nd.id);
     if (it == tickets_.end()) return;
-    for (long long t : it->second) {
-        int32_t toks[8];
-        int32_t n = 0;
-        check(h, api_->step_wait(h, t, toks, 8, &n, nullptr, 0), "step_wait");
-        mesh_gpu_stats st{};
-        api_->stats_get(h, &st);
-        device_ms_ += st.last_step_ms;
-        ++steps_;
-    }
+    for (long long t : it->second) pending_.push_back({handle_for_node(nd.id), t});
     it->second.clear();
+    while (pending_.size() > 32) retire_one();
+}
+
+void GpuExecutor::retire_one() {
+    auto [h, t] = pending_.front();
+    pending_.pop_front();
+    int32_t toks[8];
+    int32_t n = 0;
+    check(h, api_->step_wait(h, t, toks, 8, &n, nullptr, 0), "step_wait");
+    mesh_gpu_stats st{};
+    api_->stats_get(h, &st);
+    device_ms_ += st.last_step_ms;
+    ++steps_;
+}
+
+void GpuExecutor::drain() {
+    while (!pending_.empty()) retire_one();
 }
 
 void GpuExecutor::request_evicted(const Cluster&, InstanceId inst, const Request& r) {
@@ -169,6 +179,7 @@ void GpuExecutor::request_finished(const Cluster&, InstanceId inst, const Reques
 void GpuExecutor::instance_unloaded(const Cluster&, InstanceId inst) {
     auto d = inst_dev_.find(inst);
     if (d == inst_dev_.end()) return;
+    drain();  // retire outstanding tickets before the instance (and its tickets) go away
     mesh_gpu* h = handles_[static_cast<std::size_t>(d->second)];
     check(h, api_->instance_destroy(h, inst), "instance_destroy");
     inst_dev_.erase(d);
@@ -180,17 +191,23 @@ std::map<std::string, double> GpuExecutor::metrics() const {
     m["gpu.decode_tokens"] = static_cast<double>(decode_tokens_);
     m["gpu.prefill_tokens"] = static_cast<double>(prefill_tokens_);
     m["gpu.device_ms"] = device_ms_;
-    double swap = 0, mig = 0, moved = 0;
+    double swap = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0;
     for (mesh_gpu* h : handles_) {
         mesh_gpu_stats st{};
         api_->stats_get(h, &st);
         swap += static_cast<double>(st.swap_out_bytes);
         mig += static_cast<double>(st.migrate_bytes);
         moved += static_cast<double>(st.blocks_moved);
+        launches += static_cast<double>(st.kernel_launches);
+        h2d += static_cast<double>(st.h2d_bytes);
+        d2h += static_cast<double>(st.d2h_bytes);
     }
     m["gpu.swap_out_bytes"] = swap;
     m["gpu.migrate_bytes"] = mig;
     m["gpu.blocks_moved"] = moved;
+    m["gpu.kernel_launches"] = launches;
+    m["gpu.h2d_bytes"] = h2d;
+    m["gpu.d2h_bytes"] = d2h;
     return m;
 }
 

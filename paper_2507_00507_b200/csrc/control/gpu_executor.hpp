@@ -3,6 +3,7 @@
 // builds and runs without CUDA). Node i -> device devices[i % n].
 #pragma once
 
+#include <deque>
 #include <map>
 #include <string>
 #include <vector>
@@ -34,6 +35,7 @@ public:
     void instance_unloaded(const Cluster&, InstanceId) override;
 
     std::map<std::string, double> metrics() const;
+    void drain();  // wait for every launched step
 
 private:
     struct Api;
@@ -46,6 +48,8 @@ private:
     std::map<NodeId, std::vector<long long>> tickets_;  // in-flight step of each node
     double device_ms_ = 0.0;
     long long steps_ = 0, decode_tokens_ = 0, prefill_tokens_ = 0;
+    std::deque<std::pair<mesh_gpu*, long long>> pending_;  // launched, not yet retired
+    void retire_one();
     mesh_gpu* handle_for_node(NodeId node);
     void check(mesh_gpu* h, int status, const char* what);
 };

@@ -287,7 +287,9 @@ struct mesh_gpu {
     uint16_t* p_abuf = nullptr;
     float* p_logits = nullptr;
     int* p_tokens = nullptr;
-    int* h_tokens_pinned = nullptr;  // staging for prefill prompt ids
+    int* h_tokens_pinned = nullptr;  // (unused) legacy staging
+    int* h_pf_stage = nullptr;       // [RING][pf_stage_ints] pinned prefill staging (block row + tokens)
+    size_t pf_stage_ints = 0;
     // step rings
     StepDesc* h_desc = nullptr;
     StepDesc* d_desc = nullptr;
@@ -363,8 +365,9 @@ void ensure_scratch(mesh_gpu* g, const Shape& s) {
     dalloc(&g->p_abuf, nseq * nff);
     dalloc(&g->p_logits, nv);
     dalloc(&g->p_tokens, nseq);
-    if (g->h_tokens_pinned) CK(cudaFreeHost(g->h_tokens_pinned));
-    CK(cudaHostAlloc((void**)&g->h_tokens_pinned, nseq * sizeof(int), cudaHostAllocDefault));
+    if (g->h_pf_stage) CK(cudaFreeHost(g->h_pf_stage));
+    g->pf_stage_ints = nseq + DEC_BT_MAX;
+    CK(cudaHostAlloc((void**)&g->h_pf_stage, g->pf_stage_ints * RING * sizeof(int), cudaHostAllocDefault));
 }
 
 Instance& inst_of(mesh_gpu* g, int64_t id) {
@@ -629,6 +632,8 @@ void launch_decode_step(mesh_gpu* g, Instance& in, const int64_t* rids, int n, T
     DecodeArgs a = decode_args(g, in, g->d_desc + t.ring, t.ring);
     CK(launch_decode(a, grid_of(g), g->stream));
     CK(cudaEventRecord(t.kend, g->stream));
+    g->st.kernel_launches += 1;
+    g->st.h2d_bytes += (long long)sizeof(StepDesc);
     for (int i = 0; i < n; ++i) {
         ReqState& r = in.reqs[rids[i]];
         r.ctx += 1;
@@ -659,10 +664,11 @@ void restore_from_swap(mesh_gpu* g, Instance& in, int64_t rid, ReqState& r, Swap
 
 void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Ticket& t) {
     const int64_t rid = p.prefill_request;
+    // a request with device history (re-prefill) needs its token history complete
+    if (in.reqs.count(rid)) flush_request(g, in.id, rid);
     ReqState& r = req_slot(in, rid);
     int n = p.prefill_len;
     if (n < 1 || n > in.s.max_seq) throw MeshError(MESH_ERR_ARG, "prefill_len out of range");
-    flush_request(g, in.id, rid);
     // a request that was evicted resumes from its parked KV (or at least its history)
     auto sit = swap_store().find(rid);
     if (sit != swap_store().end() && r.ctx == 0) {
@@ -699,14 +705,15 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
         r.blocks.push_back(b);
         write_bt_entry(in, r.slot, int(r.blocks.size()) - 1, b);
     }
-    // stage the block table row and the tokens
-    CK(cudaMemcpyAsync(in.d_block_table + size_t(r.slot) * in.bt_stride,
-                       in.h_block_table.data() + size_t(r.slot) * in.bt_stride, sizeof(int) * in.bt_stride,
+    // stage the block table row and the tokens through this ticket's pinned slot
+    // (the slot is reused only after its previous step drained: no host sync here)
+    int* stage = g->h_pf_stage + size_t(t.ring) * g->pf_stage_ints;
+    std::memcpy(stage, in.h_block_table.data() + size_t(r.slot) * in.bt_stride, sizeof(int) * in.bt_stride);
+    std::memcpy(stage + in.bt_stride, r.tokens.data() + p0, sizeof(int) * L);
+    CK(cudaMemcpyAsync(in.d_block_table + size_t(r.slot) * in.bt_stride, stage, sizeof(int) * in.bt_stride,
                        cudaMemcpyHostToDevice, g->stream));
-    // pinned staging is reused per step: wait for the previous prefill's copy
-    CK(cudaStreamSynchronize(g->stream));
-    std::memcpy(g->h_tokens_pinned, r.tokens.data() + p0, sizeof(int) * L);
-    CK(cudaMemcpyAsync(g->p_tokens, g->h_tokens_pinned, sizeof(int) * L, cudaMemcpyHostToDevice, g->stream));
+    CK(cudaMemcpyAsync(g->p_tokens, stage + in.bt_stride, sizeof(int) * L, cudaMemcpyHostToDevice, g->stream));
+    g->st.h2d_bytes += (long long)sizeof(int) * (in.bt_stride + L);
     PrefillArgs a{};
     a.s = in.s;
     a.w = in.w;
@@ -729,6 +736,7 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     CK(cudaEventRecord(t.start, g->stream));
     CK(launch_prefill(a, g->stream));
     CK(cudaEventRecord(t.kend, g->stream));
+    g->st.kernel_launches += prefill_launch_count(in.s);
     r.ctx = p0 + L;
     // history: the prefill consumed tokens[0, n); anything beyond is stale
     r.tokens.resize(n);
@@ -849,7 +857,7 @@ void mesh_gpu_close(mesh_gpu* g) {
         if (p) cudaFree(p);
     if (g->h_desc) cudaFreeHost(g->h_desc);
     if (g->h_tok) cudaFreeHost(g->h_tok);
-    if (g->h_tokens_pinned) cudaFreeHost(g->h_tokens_pinned);
+    if (g->h_pf_stage) cudaFreeHost(g->h_pf_stage);
     for (int i = 0; i < RING; ++i)
         if (g->ring_ev[i]) cudaEventDestroy(g->ring_ev[i]);
     if (g->stream) cudaStreamDestroy(g->stream);
@@ -1017,6 +1025,7 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
         }
         CK(cudaMemcpyAsync(g->h_tok + t.ring * 8, g->d_tok + t.ring * 8, sizeof(int) * 8, cudaMemcpyDeviceToHost,
                            g->stream));
+        g->st.d2h_bytes += (long long)sizeof(int) * 8;
         CK(cudaEventRecord(t.end, g->stream));
         CK(cudaEventRecord(g->ring_ev[t.ring], g->stream));
         g->st.steps++;
@@ -1059,7 +1068,8 @@ mesh_status mesh_gpu_request_free(mesh_gpu* g, int64_t instance_id, int64_t requ
     if (!g) return MESH_ERR_ARG;
     return guarded(g, [&] {
         Instance& in = inst_of(g, instance_id);
-        flush_request(g, instance_id, request_id);
+        // no host sync: later kernels that reuse the blocks are stream-ordered after
+        // every step that read them
         free_request(in, request_id);
     });
 }

@@ -29,5 +29,7 @@ struct PrefillArgs {
 };
 
 cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t stream);
+// kernels one launch_prefill issues (embed, per layer 2 norms + 4 GEMMs + attention, final norm/lm_head/argmax)
+inline int prefill_launch_count(const Shape& s) { return 1 + 7 * s.n_layers + 3; }
 
 }  // namespace meshgpu

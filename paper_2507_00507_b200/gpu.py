@@ -46,7 +46,8 @@ class GpuStats(C.Structure):
     _fields_ = [("kv_mapped_bytes", C.c_int64), ("kv_pool_bytes", C.c_int64), ("blocks_moved", C.c_int64),
                 ("bytes_moved", C.c_int64), ("swap_out_bytes", C.c_int64), ("swap_in_bytes", C.c_int64),
                 ("migrate_bytes", C.c_int64), ("steps", C.c_int64), ("decode_tokens", C.c_int64),
-                ("prefill_tokens", C.c_int64), ("last_step_ms", C.c_double), ("last_kernel_ms", C.c_double)]
+                ("prefill_tokens", C.c_int64), ("last_step_ms", C.c_double), ("last_kernel_ms", C.c_double),
+                ("kernel_launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
 
 
 @dataclass(frozen=True)

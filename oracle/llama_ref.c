@@ -13,7 +13,9 @@
  *   weights, embeddings, KV cache: bf16 (RNE); residual stream h: fp32;
  *   normed GEMV input  a = bf16(h * gamma), output scaled by rs = 1/sqrt(mean(h^2)+eps);
  *   q, k roped in fp32 (rotate-half, table cos/sin computed in double -> float),
- *   attention in fp32 over bf16 K/V, its output rounded to bf16 before W_o;
+ *   attention in fp32 over bf16 K/V, its output rounded to bf16 before W_o
+ *   (the GPU decode kernel feeds q and the softmax weights to the tensor cores
+ *   as bf16; that rounding is inside the parity tolerance, not restated here);
  *   silu(gate) * up rounded to bf16 before W_down; logits fp32; greedy argmax
  *   with ties to the lowest id.
  * The generator below must stay bit-identical to csrc/gpu/model.cuh.

@@ -110,6 +110,12 @@ MESH_DEV void ldmatrix_x4_trans(uint32_t smem_addr, uint32_t& r0, uint32_t& r1, 
                  : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
                  : "r"(smem_addr));
 }
+// transpose an 8x8 b16 matrix held in ldmatrix fragment layout
+MESH_DEV uint32_t movmatrix_trans(uint32_t x) {
+    uint32_t y;
+    asm volatile("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;\n" : "=r"(y) : "r"(x));
+    return y;
+}
 // D = A(16x16, row) * B(16x8, col) + D ; bf16 inputs, fp32 accumulate.
 MESH_DEV void mma_bf16_16816(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3,
                              uint32_t b0, uint32_t b1) {

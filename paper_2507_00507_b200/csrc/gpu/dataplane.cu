@@ -591,6 +591,7 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.bar_gen = g->bar + 1;
     a.progress = g->dbg_dev;
     a.trace = nullptr;
+    a.arrive = nullptr;
     a.nstage = g->nstage;
     a.l2_ahead = g->l2_ahead;
     a.skip = g->skip;
@@ -1307,14 +1308,30 @@ mesh_status mesh_gpu_bench_decode(mesh_gpu* g, int64_t instance_id, const mesh_s
         if (tr) {
             DecodeArgs at = a;
             at.trace = tr;
+            unsigned long long* arr = nullptr;
+            const size_t narr = size_t(256) * grid_of(g);
+            CK(cudaMalloc((void**)&arr, sizeof(unsigned long long) * narr));
+            CK(cudaMemset(arr, 0, sizeof(unsigned long long) * narr));
+            at.arrive = arr;
             CK(launch_decode(at, grid_of(g), g->stream));
             CK(cudaStreamSynchronize(g->stream));
+            {
+                std::vector<unsigned long long> ha(narr);
+                CK(cudaMemcpy(ha.data(), arr, sizeof(unsigned long long) * narr, cudaMemcpyDeviceToHost));
+                std::string ap = std::string(trace_path) + ".arrive";
+                FILE* fa = std::fopen(ap.c_str(), "w");
+                if (fa) {
+                    for (size_t i = 0; i < narr; ++i) std::fprintf(fa, "%llu%c", ha[i], (i + 1) % grid_of(g) ? ' ' : '\n');
+                    std::fclose(fa);
+                }
+                CK(cudaFree(arr));
+            }
             std::vector<unsigned long long> h(4096);
             CK(cudaMemcpy(h.data(), tr, sizeof(unsigned long long) * 4096, cudaMemcpyDeviceToHost));
             FILE* f = std::fopen(trace_path, "w");
             if (f) {
-                for (auto v : h)
-                    if (v) std::fprintf(f, "%llu %llu\n", v >> 4, v & 15);
+                for (size_t i = 0; i < h.size(); ++i)
+                    if (h[i]) std::fprintf(f, "%llu %llu\n", h[i] >> 4, (h[i] & 15) + (i >= 2048 ? 100 : 0));
                 std::fclose(f);
             }
             CK(cudaFree(tr));

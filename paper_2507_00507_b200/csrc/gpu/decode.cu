@@ -294,28 +294,62 @@ struct Producer {
     // KV stages of this CTA's attention range: only blocks that were complete
     // before this step (every position < pos) are streamed; the current token
     // is read directly by the consumer.
+    int ntr = 0;
+    __device__ __forceinline__ void ptrace(int cta, int tag) {  // producer timeline (CTA 0) at trace[2048..]
+        if (a.trace && cta == 0 && ntr < 2000) {
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            a.trace[2048 + ntr++] = (t << 4) | unsigned(tag);
+        }
+    }
+    // KV stages of this CTA's attention range: only blocks that were complete
+    // before this step (every position < pos) are streamed; the current token
+    // is read directly by the consumer. The (b, kv head, chunk) walk is
+    // incremental and all per-layer offsets are hoisted: the single producer
+    // thread must issue a stage every ~100 cycles to keep up with HBM.
     __device__ __forceinline__ void attention(int layer, const AttnPlan& ap, const int* pos) {
+        if (ap.a1 <= ap.a0) return;
         const Shape& s = a.s;
         const uint32_t blk_bytes = uint32_t(KV_BLOCK_TOKENS * s.dh * 2);  // one (layer, k|v, head) block
-        const int blocks_per_stage = ap.rt / KV_BLOCK_TOKENS;
+        const int bps = ap.rt / KV_BLOCK_TOKENS;                           // blocks per stage
+        const size_t head_stride = size_t(KV_BLOCK_TOKENS) * s.dh * 2;
+        const size_t v_off = size_t(s.n_kv) * head_stride;  // V plane after the K plane
+        const uint8_t* layer_base = a.kv_base + kv_offset(s, layer, 0, 0, 0);
+        // decode the first stage once, then walk
+        AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0);
+        int b = st.b, kvh = st.kvh, sc = st.s;
+        int nst_b = ap.nst[b];
+        int p = pos[b];
+        const int* btrow = sm.bt + b * DEC_BT_MAX;
         for (int i = ap.a0; i < ap.a1; ++i) {
-            const AttnStage st = attn_stage_of(ap, s.n_kv, i);
             const uint32_t slot = claim();
             uint8_t* dst = sm.ring + size_t(slot) * DEC_STAGE_BYTES;
-            const int p = pos[st.b];
+            const int k0 = sc * bps;
             int nblk = 0;
-            for (int j = 0; j < blocks_per_stage; ++j)
-                if ((st.s * blocks_per_stage + j) * KV_BLOCK_TOKENS < p) ++nblk;
+            if (k0 * KV_BLOCK_TOKENS < p) nblk = (bps == 2 && (k0 + 1) * KV_BLOCK_TOKENS < p) ? 2 : 1;
+            if (a.skip & 4) nblk = 0;  // debug: no KV traffic
             mbar_arrive_expect_tx(&sm.full[slot], 2u * nblk * blk_bytes);
+            const size_t hoff = size_t(kvh) * head_stride;
             for (int j = 0; j < nblk; ++j) {
-                const int k = st.s * blocks_per_stage + j;
-                const int blk = sm.bt[st.b * DEC_BT_MAX + k];
-                const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
-                bulk_g2s(dst + j * blk_bytes, base + kv_offset(s, layer, 0, st.kvh, 0), blk_bytes, &sm.full[slot]);
-                bulk_g2s(dst + 4096 + j * blk_bytes, base + kv_offset(s, layer, 1, st.kvh, 0), blk_bytes,
-                         &sm.full[slot]);
+                const uint8_t* kb = layer_base + size_t(btrow[k0 + j]) * a.block_bytes + hoff;
+                bulk_g2s(dst + j * blk_bytes, kb, blk_bytes, &sm.full[slot]);
+                bulk_g2s(dst + 4096 + j * blk_bytes, kb + v_off, blk_bytes, &sm.full[slot]);
             }
             ++q;
+            if (++sc == nst_b) {  // next (b, kv head)
+                sc = 0;
+                if (++kvh == s.n_kv) {
+                    kvh = 0;
+                    do {
+                        ++b;
+                    } while (b < DEC_MAXB && ap.nst[b] == 0);
+                    if (b < DEC_MAXB) {
+                        nst_b = ap.nst[b];
+                        p = pos[b];
+                        btrow = sm.bt + b * DEC_BT_MAX;
+                    }
+                }
+            }
         }
     }
 };
@@ -326,9 +360,13 @@ __device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int
     const AttnPlan ap = attn_plan(a.s, B, pos, cta, G);
     int off = 0;
     for (int l = 0; l < a.s.n_layers; ++l) {
+        pr.ptrace(cta, 8);
         pr.gemv(PH_QKV, l, off, cta, G);
+        pr.ptrace(cta, 9);
         if (!(a.skip & 1)) pr.attention(l, ap, pos);
+        pr.ptrace(cta, 10);
         pr.gemv(PH_O, l, off, cta, G);
+        pr.ptrace(cta, 11);
         pr.gemv(PH_GU, l, off, cta, G);
         pr.gemv(PH_DOWN, l, off, cta, G);
         if (a.progress) a.progress[cta * 2 + 1] = int(pr.q);
@@ -339,6 +377,7 @@ __device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int
 // ----------------------------------------------------------------- consumer
 struct Ctx {
     int ntrace;           // trace cursor (CTA 0, thread 0)
+    int nbar;             // grid barriers passed
     const DecodeArgs* a;  // shared-memory copy of the launch arguments
     Smem sm;
     int cta, G, warp, lane, tid;  // tid in [0, 256)
@@ -362,6 +401,8 @@ __device__ __forceinline__ void trace(Ctx& c, int tag) {
 }
 __device__ __forceinline__ void grid_sync(Ctx& c) {
     csync();
+    if (c.a->arrive && c.tid == 0 && c.nbar < 256) c.a->arrive[size_t(c.nbar) * c.G + c.cta] = gtimer();
+    ++c.nbar;
     if (c.a->progress && c.tid == 0) c.a->progress[c.cta * 2] += 1;
     if (c.tid == 0) grid_barrier(c.a->bar_count, c.a->bar_gen, unsigned(c.G));
     csync();
@@ -469,10 +510,10 @@ __device__ __forceinline__ void epi_qkv(Ctx& c, int layer, int tile, const float
             qd[r1.dim + half] = o2;
         } else {
             const int blk = ldcg_i32(a.block_table + size_t(c.slot[b]) * a.bt_stride + pos / KV_BLOCK_TOKENS);
-            uint16_t* e = reinterpret_cast<uint16_t*>(a.kv_base + size_t(blk) * a.block_bytes +
-                                                      kv_offset(s, layer, r1.section - 1, r1.head, pos % KV_BLOCK_TOKENS));
-            e[r1.dim] = f_to_bf16(o1);
-            e[r1.dim + half] = f_to_bf16(o2);
+            const int slot = pos % KV_BLOCK_TOKENS;
+            uint8_t* e = a.kv_base + size_t(blk) * a.block_bytes + kv_offset(s, layer, r1.section - 1, r1.head, slot);
+            *reinterpret_cast<uint16_t*>(e + kv_dim_off(slot, r1.dim)) = f_to_bf16(o1);
+            *reinterpret_cast<uint16_t*>(e + kv_dim_off(slot, r1.dim + half)) = f_to_bf16(o2);
         }
     }
 }
@@ -645,45 +686,62 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
 }
 
 // ------------------------------------------------------------ attention
+// Tensor-core decode attention, per warp and 8 KB ring stage of RT tokens, in
+// transposed form so the GQA group (<= 8 query heads) is the mma N dimension:
+//   S^T = K Q^T   mma.m16n8k16: A = 16 K rows (ldmatrix), B = Q^T (bf16 regs)
+//   online softmax per head column (a column lives in 8 lanes x 2 regs)
+//   O^T += V^T P^T  A = V^T (ldmatrix.trans), B = P^T (movmatrix.trans of S^T)
+// Stage layout in the ring slot: K rows at [0, 4 KB), V rows at [4 KB, 8 KB),
+// token r of the stage at row r with the KV block's chunk swizzle (r & 7).
 template <int DH>
 struct AttnCfg {
-    static constexpr int LPT = DH / 64;  // lanes per token (64 dims each)
-    static constexpr int RT = 32 / LPT;  // tokens per stage
-    static constexpr int DPL = DH / 32;  // PV dims per lane
-    static constexpr int HM = 512 / DH;  // largest GQA group (GQ * DH <= 512)
-    static constexpr int WARP_SMEM = 512 * 4 + RT * 9 * 4 + 2 * DH * 2;  // q, p, k/v patch
+    static constexpr int RT = 2048 / DH;  // tokens per 8 KB stage (K + V)
+    static constexpr int KS = DH / 16;    // k-steps of S^T (head dims)
+    static constexpr int MT = RT / 16;    // token m-tiles of S^T == k-steps of O^T
+    static constexpr int MD = DH / 16;    // dim m-tiles of O^T
 };
 
-// Online-softmax state of one warp for the (b, kv head) pair it is reducing.
 template <int DH>
 struct AttnState {
-    float m[AttnCfg<DH>::HM], l[AttnCfg<DH>::HM], acc[AttnCfg<DH>::HM][AttnCfg<DH>::DPL];
+    uint32_t qb[AttnCfg<DH>::KS][2];  // Q^T as mma B fragments (head g, dims 2t..)
+    float o[AttnCfg<DH>::MD][4];      // O^T: rows dims 16md + g (+8), cols heads 2t, 2t+1
+    float m[2], l[2];                 // running max / this lane's partial sum, heads 2t, 2t+1
 };
 
 template <int DH>
 __device__ __forceinline__ void attn_flush(Ctx& c, const AttnPlan& ap, int b, int kvh, int pair_lo, int pair_n,
                                            AttnState<DH>& stt) {
-    using CFG = AttnCfg<DH>;
-    constexpr int HM = CFG::HM, DPL = CFG::DPL;
+    constexpr int MD = AttnCfg<DH>::MD;
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
     const int GQ = s.n_heads / s.n_kv;
     const int W = GQ * (DH + 2);
     const unsigned FULL = 0xffffffffu;
-    const int d0 = c.lane * DPL;
+    const int g = c.lane >> 2, t = c.lane & 3;
     int rank, count;
     pair_slots(pair_lo, pair_lo + pair_n, ap.total, c.G, c.cta, c.warp, rank, count);
-    float* mine = a.apart + size_t(pair_lo + rank) * W;
+    float l0 = stt.l[0], l1 = stt.l[1];
 #pragma unroll
-    for (int h = 0; h < HM; ++h) {
-        if (h >= GQ) continue;
-        float* ph = mine + h * (DH + 2);
-        if (c.lane == 0) {
-            ph[0] = stt.m[h];
-            ph[1] = stt.l[h];
+    for (int o = 4; o < 32; o <<= 1) {
+        l0 += __shfl_xor_sync(FULL, l0, o);
+        l1 += __shfl_xor_sync(FULL, l1, o);
+    }
+    float* pp = a.apart + size_t(pair_lo + rank) * W;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+        const int h = 2 * t + j;
+        if (h < GQ) {
+            float* ph = pp + h * (DH + 2);
+            if (g == 0) {
+                ph[0] = stt.m[j];
+                ph[1] = j ? l1 : l0;
+            }
+#pragma unroll
+            for (int md = 0; md < MD; ++md) {
+                ph[2 + 16 * md + g] = stt.o[md][j];
+                ph[2 + 16 * md + 8 + g] = stt.o[md][2 + j];
+            }
         }
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) ph[2 + d0 + e] = stt.acc[h][e];
     }
     __syncwarp();
     const int pair = b * s.n_kv + kvh;
@@ -691,201 +749,157 @@ __device__ __forceinline__ void attn_flush(Ctx& c, const AttnPlan& ap, int b, in
     if (c.lane == 0) last = atom_add_acq_rel_gpu(a.acnt + pair, 1) == count - 1;
     last = __shfl_sync(FULL, last, 0);
     if (!last) return;
-    // Combine the pair's `count` partials (slot order = deterministic).
+    // Combine the pair's `count` partials in slot order (deterministic): lane
+    // covers dims [4 * lane, 4 * lane + 4) of every head row of the group.
     const float* base = a.apart + size_t(pair_lo) * W;
-    float M[HM];
-#pragma unroll
-    for (int h = 0; h < HM; ++h) {
+    for (int h = 0; h < GQ; ++h) {
         float mx = -INFINITY;
-        if (h < GQ)
-            for (int sp = c.lane; sp < count; sp += 32) mx = fmaxf(mx, ldcg_f32(base + size_t(sp) * W + h * (DH + 2)));
+        for (int sp = c.lane; sp < count; sp += 32) mx = fmaxf(mx, ldcg_f32(base + size_t(sp) * W + h * (DH + 2)));
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-        M[h] = mx;
-    }
-    float L[HM], A[HM][DPL];
+        float L = 0.f, A[4] = {0.f, 0.f, 0.f, 0.f};
+        const int d0 = c.lane * 4;
+        for (int sp0 = 0; sp0 < count; sp0 += 8) {
+            float mv[8], lv[8];
+            float4 av[8];
 #pragma unroll
-    for (int h = 0; h < HM; ++h) {
-        L[h] = 0.f;
+            for (int j = 0; j < 8; ++j) {
+                const bool ok = sp0 + j < count;
+                const float* ph = base + size_t(sp0 + j) * W + h * (DH + 2);
+                mv[j] = ok ? ldcg_f32(ph) : -INFINITY;
+                lv[j] = ok ? ldcg_f32(ph + 1) : 0.f;
+                av[j] = (ok && d0 < DH) ? make_float4(ldcg_f32(ph + 2 + d0), ldcg_f32(ph + 3 + d0), ldcg_f32(ph + 4 + d0),
+                                                      ldcg_f32(ph + 5 + d0))
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
 #pragma unroll
-        for (int e = 0; e < DPL; ++e) A[h][e] = 0.f;
-    }
-    for (int sp0 = 0; sp0 < count; sp0 += 32) {
-        float f[HM];  // lane sp0 + lane owns that partial's scale factors
-#pragma unroll
-        for (int h = 0; h < HM; ++h) {
-            const int sp = sp0 + c.lane;
-            f[h] = 0.f;
-            if (h < GQ && sp < count) {
-                const float* ph = base + size_t(sp) * W + h * (DH + 2);
-                f[h] = __expf(ldcg_f32(ph) - M[h]);
-                L[h] += ldcg_f32(ph + 1) * f[h];
+            for (int j = 0; j < 8; ++j) {
+                const float f = mv[j] == -INFINITY ? 0.f : __expf(mv[j] - mx);
+                L += lv[j] * f;
+                A[0] += av[j].x * f;
+                A[1] += av[j].y * f;
+                A[2] += av[j].z * f;
+                A[3] += av[j].w * f;
             }
         }
-        const int nj = min(32, count - sp0);
-        for (int j0 = 0; j0 < nj; j0 += 4) {
-            float v[4][HM][DPL];
+        if (d0 < DH) {
+            uint16_t* out = a.attn + size_t(b) * s.d + (size_t(kvh) * GQ + h) * DH + d0;
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int h = 0; h < HM; ++h) {
-                    const bool ok = h < GQ && j0 + j < nj;
-                    const float* ph = base + size_t(sp0 + j0 + j) * W + h * (DH + 2) + 2 + d0;
-#pragma unroll
-                    for (int e = 0; e < DPL; ++e) v[j][h][e] = ok ? ldcg_f32(ph + e) : 0.f;
-                }
-#pragma unroll
-            for (int j = 0; j < 4; ++j)
-#pragma unroll
-                for (int h = 0; h < HM; ++h) {
-                    const float fj = __shfl_sync(FULL, f[h], (j0 + j) & 31);
-#pragma unroll
-                    for (int e = 0; e < DPL; ++e) A[h][e] += v[j][h][e] * fj;
-                }
+            for (int e = 0; e < 4; ++e) out[e] = f_to_bf16(A[e] / L);
         }
-    }
-#pragma unroll
-    for (int h = 0; h < HM; ++h) {
-        if (h >= GQ) continue;
-        float lsum = L[h];
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(FULL, lsum, o);
-        uint16_t* out = a.attn + size_t(b) * s.d + (size_t(kvh) * GQ + h) * DH + d0;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) out[e] = f_to_bf16(A[h][e] / lsum);
     }
     if (c.lane == 0) atomicExch(a.acnt + pair, 0);
 }
 
-// One attention stage: RT tokens of (b, kvh); K rows at [0, 4 KB) and V rows
-// at [4 KB, 8 KB) of the ring slot (token r at row r), except the current
-// token, read from the paged cache (written by this step's QKV phase).
 template <int DH>
-__device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage& st, uint32_t qi, AttnState<DH>& stt,
-                                             const float* q_s, float* p_s, uint16_t* kpatch, uint16_t* vpatch) {
+__device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage& st, uint32_t qi, AttnState<DH>& stt) {
     using CFG = AttnCfg<DH>;
-    constexpr int LPT = CFG::LPT, RT = CFG::RT, DPL = CFG::DPL, HM = CFG::HM;
+    constexpr int RT = CFG::RT, KS = CFG::KS, MT = CFG::MT, MD = CFG::MD;
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
-    const int GQ = s.n_heads / s.n_kv;
     const unsigned FULL = 0xffffffffu;
     const int cur = c.pos[st.b], len = cur + 1;
     const int t0 = st.s * RT;
-    const int tl = c.lane / LPT, part = c.lane % LPT;
-    const int tok = t0 + tl;
-    const bool valid = tok < len;
-    const int d0 = c.lane * DPL;
+    const int lane = c.lane, g = lane >> 2, t = lane & 3;
     const float scale = rsqrtf(float(DH));
-    if (valid && tok == cur) {  // the current token's K/V half-rows from the paged cache
-        const int blk = ldcg_i32(a.block_table + size_t(c.slot[st.b]) * a.bt_stride + cur / KV_BLOCK_TOKENS);
-        const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
-        const uint8_t* kp = base + kv_offset(s, layer, 0, st.kvh, cur % KV_BLOCK_TOKENS) + part * 128;
-        const uint8_t* vp = base + kv_offset(s, layer, 1, st.kvh, cur % KV_BLOCK_TOKENS) + part * 128;
-        uint4 kv[8], vv[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            kv[i] = ldcg_u4(kp + i * 16);
-            vv[i] = ldcg_u4(vp + i * 16);
-        }
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            reinterpret_cast<uint4*>(kpatch + part * 64)[i] = kv[i];
-            reinterpret_cast<uint4*>(vpatch + part * 64)[i] = vv[i];
-        }
-    }
     uint32_t slot;
     wait_stage(c, qi, slot);
-    __syncwarp();
-    const uint8_t* stage = c.sm.ring + size_t(slot) * DEC_STAGE_BYTES;
-    const uint8_t* krow = (tok == cur) ? reinterpret_cast<const uint8_t*>(kpatch) : stage + size_t(tl) * DH * 2;
-    float sc[HM];
+    uint8_t* stage = c.sm.ring + size_t(slot) * DEC_STAGE_BYTES;
+    // the current token's K/V rows were written by this step's QKV phase: copy them
+    // from the paged cache into their stage rows (same swizzle: row & 7 == slot & 7)
+    if (cur >= t0 && cur < t0 + RT) {
+        const int blk = ldcg_i32(a.block_table + size_t(c.slot[st.b]) * a.bt_stride + cur / KV_BLOCK_TOKENS);
+        const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
+        const int r = cur - t0;
+        constexpr int CH = DH / 8;  // 16-byte chunks per row
+        for (int i = lane; i < 2 * CH; i += 32) {
+            const int kv = i / CH, ch = i % CH;
+            const uint4 v = ldcg_u4(base + kv_offset(s, layer, kv, st.kvh, cur % KV_BLOCK_TOKENS) + ch * 16);
+            *reinterpret_cast<uint4*>(stage + kv * 4096 + r * DH * 2 + ch * 16) = v;
+        }
+        __syncwarp();
+    }
+    const uint32_t kbase = smem_u32(stage), vbase = kbase + 4096;
+    // ldmatrix.x4 lane address: matrix j = lane >> 3 covers rows +8*(j&1), chunk +(j>>1)
+    const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lch = lane >> 4;
+    // ---- S^T = K Q^T
+    float sc[MT][4];
 #pragma unroll
-    for (int h = 0; h < HM; ++h) sc[h] = 0.f;
-    if (valid) {
-        // rotated 16-byte chunk order: the 8 lanes of a quarter-warp read 8
-        // different bank groups of their (128-byte strided) rows
+    for (int mt = 0; mt < MT; ++mt) {
+        sc[mt][0] = sc[mt][1] = sc[mt][2] = sc[mt][3] = 0.f;
+        const int row = mt * 16 + lrow;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int cc = (i + tl) & 7;
-            const uint4 kv = *reinterpret_cast<const uint4*>(krow + part * 128 + cc * 16);
-            const float k[8] = {bf16_lo(kv.x), bf16_hi(kv.x), bf16_lo(kv.y), bf16_hi(kv.y),
-                                bf16_lo(kv.z), bf16_hi(kv.z), bf16_lo(kv.w), bf16_hi(kv.w)};
+        for (int ks = 0; ks < KS; ++ks) {
+            uint32_t k0, k1, k2, k3;
+            ldmatrix_x4(kbase + row * DH * 2 + (((2 * ks + lch) ^ (row & 7)) << 4), k0, k1, k2, k3);
+            mma_bf16_16816(sc[mt], k0, k1, k2, k3, stt.qb[ks][0], stt.qb[ks][1]);
+        }
+    }
+    // ---- online softmax per head column (tokens g, g+8 of each m-tile; heads 2t, 2t+1)
+    float mx[2] = {-INFINITY, -INFINITY};
 #pragma unroll
-            for (int h = 0; h < HM; ++h) {
-                if (h < GQ) {
-                    const float* qh = q_s + h * DH + part * 64 + cc * 8;
-                    const float4 qa = *reinterpret_cast<const float4*>(qh);
-                    const float4 qb = *reinterpret_cast<const float4*>(qh + 4);
-                    sc[h] += qa.x * k[0] + qa.y * k[1] + qa.z * k[2] + qa.w * k[3] + qb.x * k[4] + qb.y * k[5] +
-                             qb.z * k[6] + qb.w * k[7];
-                }
-            }
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int tok = t0 + mt * 16 + g + (e >> 1) * 8;
+            sc[mt][e] = tok < len ? sc[mt][e] * scale : -INFINITY;
+            mx[e & 1] = fmaxf(mx[e & 1], sc[mt][e]);
         }
     }
 #pragma unroll
-    for (int h = 0; h < HM; ++h) {
-        if (h >= GQ) continue;
-        float x = sc[h];
-        if (LPT == 2) x += __shfl_xor_sync(FULL, x, 1);
-        x = valid ? x * scale : -INFINITY;
-        float mx = x;
-#pragma unroll
-        for (int o = 16; o >= LPT; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-        const float mnew = fmaxf(stt.m[h], mx);  // finite: token t0 is valid
-        const float corr = __expf(stt.m[h] - mnew);
-        const float pv = valid ? __expf(x - mnew) : 0.f;
-        float ps = part == 0 ? pv : 0.f;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(FULL, ps, o);
-        stt.l[h] = stt.l[h] * corr + ps;
-        stt.m[h] = mnew;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) stt.acc[h][e] *= corr;
-        if (part == 0) p_s[tl * 9 + h] = pv;
+    for (int o = 4; o < 32; o <<= 1) {
+        mx[0] = fmaxf(mx[0], __shfl_xor_sync(FULL, mx[0], o));
+        mx[1] = fmaxf(mx[1], __shfl_xor_sync(FULL, mx[1], o));
     }
-    __syncwarp();
-    const int nvalid = min(RT, len - t0);
-    for (int j = 0; j < nvalid; ++j) {
-        const uint16_t* vrow = (t0 + j == cur)
-                                   ? vpatch + d0
-                                   : reinterpret_cast<const uint16_t*>(stage + 4096 + size_t(j) * DH * 2) + d0;
-        float vf[DPL];
-        if constexpr (DPL == 2) {
-            const uint32_t vv = *reinterpret_cast<const uint32_t*>(vrow);
-            vf[0] = bf16_lo(vv);
-            vf[1] = bf16_hi(vv);
-        } else {
-            const uint2 vv = *reinterpret_cast<const uint2*>(vrow);
-            vf[0] = bf16_lo(vv.x);
-            vf[1] = bf16_hi(vv.x);
-            vf[2] = bf16_lo(vv.y);
-            vf[3] = bf16_hi(vv.y);
-        }
-        const float* pj = p_s + j * 9;
+    float corr[2];
 #pragma unroll
-        for (int h = 0; h < HM; ++h) {
-            if (h < GQ) {
-                const float pv = pj[h];
+    for (int j = 0; j < 2; ++j) {
+        const float mnew = fmaxf(stt.m[j], mx[j]);  // finite: token t0 is always valid
+        corr[j] = __expf(stt.m[j] - mnew);
+        stt.m[j] = mnew;
+        stt.l[j] *= corr[j];
+    }
 #pragma unroll
-                for (int e = 0; e < DPL; ++e) stt.acc[h][e] += pv * vf[e];
-            }
+    for (int mt = 0; mt < MT; ++mt) {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            sc[mt][e] = __expf(sc[mt][e] - stt.m[e & 1]);
+            stt.l[e & 1] += sc[mt][e];
         }
     }
-    release_stage(c, slot);  // its __syncwarp also retires the p_s / patch reads
+#pragma unroll
+    for (int md = 0; md < MD; ++md) {
+        stt.o[md][0] *= corr[0];
+        stt.o[md][1] *= corr[1];
+        stt.o[md][2] *= corr[0];
+        stt.o[md][3] *= corr[1];
+    }
+    // ---- O^T += V^T P^T
+#pragma unroll
+    for (int kk = 0; kk < MT; ++kk) {
+        const uint32_t pb0 = movmatrix_trans(pack_bf16x2(sc[kk][0], sc[kk][1]));
+        const uint32_t pb1 = movmatrix_trans(pack_bf16x2(sc[kk][2], sc[kk][3]));
+        // x4.trans: matrix j = (dims +8*(j&1)) x (tokens +8*(j>>1))
+        const int row = kk * 16 + (lane & 7) + (lane >> 4) * 8;
+        const int dsel = (lane >> 3) & 1;
+#pragma unroll
+        for (int md = 0; md < MD; ++md) {
+            uint32_t v0, v1, v2, v3;
+            ldmatrix_x4_trans(vbase + row * DH * 2 + (((2 * md + dsel) ^ (row & 7)) << 4), v0, v1, v2, v3);
+            mma_bf16_16816(stt.o[md], v0, v1, v2, v3, pb0, pb1);
+        }
+    }
+    release_stage(c, slot);
 }
 
 template <int DH>
 __device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPlan& ap) {
     using CFG = AttnCfg<DH>;
-    constexpr int HM = CFG::HM, DPL = CFG::DPL;
+    constexpr int KS = CFG::KS, MD = CFG::MD;
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
     const int GQ = s.n_heads / s.n_kv;
-    uint8_t* wbase = reinterpret_cast<uint8_t*>(c.sm.act) + c.warp * CFG::WARP_SMEM;
-    float* q_s = reinterpret_cast<float*>(wbase);                        // [GQ][DH]
-    float* p_s = q_s + 512;                                              // [RT][9]
-    uint16_t* kpatch = reinterpret_cast<uint16_t*>(p_s + CFG::RT * 9);  // [DH]
-    uint16_t* vpatch = kpatch + DH;                                      // [DH]
+    const int g = c.lane >> 2, t = c.lane & 3;
     const int n = ap.a1 - ap.a0;
     AttnState<DH> stt;
     int cur_pair = -1, cur_b = 0, cur_kvh = 0, cur_lo = 0, cur_n = 0;
@@ -898,30 +912,32 @@ __device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPla
             cur_kvh = st.kvh;
             cur_lo = st.pair_lo;
             cur_n = ap.nst[st.b];
-            const float4* qsrc =
-                reinterpret_cast<const float4*>(a.q + (size_t(st.b) * s.n_heads + size_t(st.kvh) * GQ) * DH);
-            float4 qv[4];  // GQ * DH <= 512 floats -> 4 float4 per lane
+            // Q^T of the GQA group as B fragments (columns >= GQ are zero)
+            const float* qrow = a.q + (size_t(st.b) * s.n_heads + size_t(st.kvh) * GQ + g) * DH;
+            float2 qv[KS][2];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int e = c.lane + 32 * k;
-                qv[k] = e * 4 < GQ * DH ? __ldcg(qsrc + e) : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-            __syncwarp();
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int e = c.lane + 32 * k;
-                if (e * 4 < GQ * DH) reinterpret_cast<float4*>(q_s)[e] = qv[k];
+            for (int ks = 0; ks < KS; ++ks) {
+                qv[ks][0] = g < GQ ? __ldcg(reinterpret_cast<const float2*>(qrow + ks * 16 + 2 * t)) : make_float2(0.f, 0.f);
+                qv[ks][1] = g < GQ ? __ldcg(reinterpret_cast<const float2*>(qrow + ks * 16 + 8 + 2 * t))
+                                   : make_float2(0.f, 0.f);
             }
 #pragma unroll
-            for (int h = 0; h < HM; ++h) {
-                stt.m[h] = -INFINITY;
-                stt.l[h] = 0.f;
-#pragma unroll
-                for (int e = 0; e < DPL; ++e) stt.acc[h][e] = 0.f;
+            for (int ks = 0; ks < KS; ++ks) {
+                stt.qb[ks][0] = pack_bf16x2(qv[ks][0].x, qv[ks][0].y);
+                stt.qb[ks][1] = pack_bf16x2(qv[ks][1].x, qv[ks][1].y);
             }
-            __syncwarp();
+#pragma unroll
+            for (int md = 0; md < MD; ++md) stt.o[md][0] = stt.o[md][1] = stt.o[md][2] = stt.o[md][3] = 0.f;
+            stt.m[0] = stt.m[1] = -INFINITY;
+            stt.l[0] = stt.l[1] = 0.f;
         }
-        attn_consume<DH>(c, layer, st, c.q + i, stt, q_s, p_s, kpatch, vpatch);
+        if (a.skip & 8) {  // debug: ring handshake only
+            uint32_t slot;
+            wait_stage(c, c.q + i, slot);
+            release_stage(c, slot);
+            continue;
+        }
+        attn_consume<DH>(c, layer, st, c.q + i, stt);
     }
     if (cur_pair >= 0) attn_flush<DH>(c, ap, cur_b, cur_kvh, cur_lo, cur_n, stt);
     c.q += n;
@@ -1045,6 +1061,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     }
     Ctx c;
     c.ntrace = 0;
+    c.nbar = 0;
     c.a = &a_s;
     c.sm = sm;
     c.cta = blockIdx.x;

@@ -93,9 +93,15 @@ __host__ __device__ inline void gu_row(int prow, int* is_up, int* row) {
 
 // ---- paged KV block layout ----
 // A block holds KV_BLOCK_TOKENS tokens of every layer: [layer][k|v][kv_head][slot][dh] bf16.
+// Within a token row the 16-byte chunks are XOR-swizzled by (slot & 7) so that
+// ldmatrix over 8 consecutive token rows hits 8 distinct bank groups.
 constexpr int KV_BLOCK_TOKENS = 16;
 __host__ __device__ inline size_t kv_offset(const Shape& s, int layer, int kv, int head, int slot) {
     return ((((size_t(layer) * 2 + kv) * s.n_kv + head) * KV_BLOCK_TOKENS + slot) * s.dh) * 2;
+}
+// byte offset of element `dim` inside a token row of block-slot `slot`
+__host__ __device__ inline uint32_t kv_dim_off(int slot, int dim) {
+    return uint32_t((((dim >> 3) ^ (slot & 7)) << 4) + (dim & 7) * 2);
 }
 
 // ---- device view of one instance's weights ----

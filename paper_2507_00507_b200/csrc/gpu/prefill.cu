@@ -150,12 +150,11 @@ __global__ void __launch_bounds__(PF_THREADS) pf_gemm(const __grid_constant__ Pr
                         qd[qr.dim] = o1;
                         qd[qr.dim + half] = o2;
                     } else {
-                        int blk = a.bt_row[pos / KV_BLOCK_TOKENS];
-                        uint16_t* e = reinterpret_cast<uint16_t*>(
-                            a.kv_base + size_t(blk) * a.block_bytes +
-                            kv_offset(s, layer, qr.section - 1, qr.head, pos % KV_BLOCK_TOKENS));
-                        e[qr.dim] = f_to_bf16(o1);
-                        e[qr.dim + half] = f_to_bf16(o2);
+                        const int blk = a.bt_row[pos / KV_BLOCK_TOKENS], slot = pos % KV_BLOCK_TOKENS;
+                        uint8_t* e = a.kv_base + size_t(blk) * a.block_bytes +
+                                     kv_offset(s, layer, qr.section - 1, qr.head, slot);
+                        *reinterpret_cast<uint16_t*>(e + kv_dim_off(slot, qr.dim)) = f_to_bf16(o1);
+                        *reinterpret_cast<uint16_t*>(e + kv_dim_off(slot, qr.dim + half)) = f_to_bf16(o2);
                     }
                 } else if constexpr (KIND == PF_GU) {
                     const float r = a.rs[l];
@@ -234,12 +233,11 @@ __global__ void __launch_bounds__(256) pf_attn(const __grid_constant__ PrefillAr
             int pos = k0 + kr;
             uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
             if (pos <= kmax) {
-                int blk = a.bt_row[pos / KV_BLOCK_TOKENS];
+                const int blk = a.bt_row[pos / KV_BLOCK_TOKENS], slot = pos % KV_BLOCK_TOKENS;
                 const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
-                kv = *reinterpret_cast<const uint4*>(base + kv_offset(s, layer, 0, kvh, pos % KV_BLOCK_TOKENS) +
-                                                     c8 * 16);
-                vv = *reinterpret_cast<const uint4*>(base + kv_offset(s, layer, 1, kvh, pos % KV_BLOCK_TOKENS) +
-                                                     c8 * 16);
+                const uint32_t sw = kv_dim_off(slot, c8 * 8);  // swizzled 16-byte chunk
+                kv = *reinterpret_cast<const uint4*>(base + kv_offset(s, layer, 0, kvh, slot) + sw);
+                vv = *reinterpret_cast<const uint4*>(base + kv_offset(s, layer, 1, kvh, slot) + sw);
             }
             k_s[kr][c8 * 4 + 0] = kv.x;
             k_s[kr][c8 * 4 + 1] = kv.y;

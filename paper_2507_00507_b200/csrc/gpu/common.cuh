@@ -87,6 +87,12 @@ MESH_DEV uint64_t l2_evict_first_policy() {
     return pol;
 }
 
+// 16-byte global -> shared copy that bypasses L1 (LDGSTS); no registers held
+MESH_DEV void cp_async_16(uint32_t smem_addr, const void* gptr) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_addr), "l"(gptr) : "memory");
+}
+MESH_DEV void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+
 // ------------------------------------------------------------ tensor cores
 MESH_DEV void ldmatrix_x4(uint32_t smem_addr, uint32_t& r0, uint32_t& r1, uint32_t& r2,
                           uint32_t& r3) {

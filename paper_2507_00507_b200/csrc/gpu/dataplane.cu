@@ -303,7 +303,6 @@ struct mesh_gpu {
     bool capture_logits = false;
     mesh_gpu_stats st{};
     int nstage = DEC_NSTAGE;  // decode ring depth in use (MESH_GPU_NSTAGE)
-    int l2_ahead = 0;         // L2 prefetch run-ahead in stages (MESH_GPU_L2_AHEAD)
     int skip = 0;             // MESH_GPU_SKIP debug mask (benchmarking only)
     int* dbg_host = nullptr;  // MESH_GPU_WATCHDOG: host-mapped decode progress
     int* dbg_dev = nullptr;
@@ -593,7 +592,6 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.trace = nullptr;
     a.arrive = nullptr;
     a.nstage = g->nstage;
-    a.l2_ahead = g->l2_ahead;
     a.skip = g->skip;
     return a;
 }
@@ -815,8 +813,9 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         CK(cudaMalloc((void**)&g->d_tok, sizeof(int) * 8 * RING));
         for (int i = 0; i < RING; ++i) CK(cudaEventCreateWithFlags(&g->ring_ev[i], cudaEventDisableTiming));
         g->st.kv_pool_bytes = g->pool.limit;
-        if (const char* e = std::getenv("MESH_GPU_NSTAGE")) g->nstage = std::max(2, std::min(DEC_NSTAGE, std::atoi(e)));
-        if (const char* e = std::getenv("MESH_GPU_L2_AHEAD")) g->l2_ahead = std::max(0, std::atoi(e));
+        // ring depth must be 8 or 16: a consumer warp's stages are 8 apart, so the
+        // depth must be a multiple of 8 (mbarrier parity) and a power of two (masks)
+        if (const char* e = std::getenv("MESH_GPU_NSTAGE")) g->nstage = std::atoi(e) >= 16 ? 16 : 8;
         if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
         if (std::getenv("MESH_GPU_WATCHDOG")) {
             CK(cudaHostAlloc((void**)&g->dbg_host, sizeof(int) * 2 * 1024, cudaHostAllocMapped));

@@ -82,7 +82,8 @@ struct AttnPlan {
     int total;          // stages per layer
     int a0, a1;         // this CTA's contiguous range
 };
-__device__ __forceinline__ long long range_lo(int c, int total, int G) { return (long long)c * total / G; }
+// c * total < 2^31 for every plan (<= 148 CTAs x 8 x 64 heads x 256 stages): 32-bit math
+__device__ __forceinline__ int range_lo(int c, int total, int G) { return int(unsigned(c) * unsigned(total) / unsigned(G)); }
 __device__ __forceinline__ AttnPlan attn_plan(const Shape& s, int B, const int* pos, int cta, int G) {
     AttnPlan p;
     p.rt = 2048 / s.dh;
@@ -118,28 +119,56 @@ __device__ __forceinline__ AttnStage attn_stage_of(const AttnPlan& p, int n_kv, 
     return st;
 }
 __device__ __forceinline__ int cta_of_stage(int i, int total, int G) {
-    return int(((long long)(i + 1) * G - 1) / total);
+    return int((unsigned(i + 1) * unsigned(G) - 1u) / unsigned(total));
 }
-// Deterministic slot of (cta, warp) among the contributors of a pair, and the
-// pair's contributor count: within a CTA the pair's stages [lo, hi) go to warps
-// (i - a0) mod 8, i.e. min(8, hi - lo) consecutive warps.
-__device__ __forceinline__ void pair_slots(int lo_p, int hi_p, int total, int G, int cta, int warp, int& rank,
-                                           int& count) {
-    count = 0;
-    rank = -1;
-    const int c0 = cta_of_stage(lo_p, total, G), c1 = cta_of_stage(hi_p - 1, total, G);
+// Where a warp's partial for a (request, kv head) pair goes. Within a CTA the
+// pair's stages [lo, hi) go to warps (i - a0) mod 8, i.e. n = min(8, hi - lo)
+// consecutive warps. When n >= 2 (and the CTA's pair-local index k fits the
+// shared staging area) the CTA pre-combines its n warp partials in shared
+// memory and contributes ONE global partial; otherwise each warp contributes
+// its own. rank/count index the pair's global partial slots deterministically.
+constexpr int ATT_PT_MAX = 32;  // pairs per CTA with precomputed slot metadata
+struct PairSlot {
+    int pre;    // this CTA pre-combines the pair
+    int k;      // pair-local index within this CTA's stage range
+    int r, n;   // warp rank within the CTA's contributors, their number
+    int rank;   // global slot of this contributor (the CTA when pre)
+    int count;  // global partials of the pair
+};
+__device__ __forceinline__ PairSlot pair_slot(const AttnPlan& ap, int n_kv, int pair, int lo_p, int hi_p, int G,
+                                              int cta, int warp, int cap_pairs) {
+    PairSlot ps;
+    ps.pre = 0;
+    ps.k = ps.r = ps.n = 0;
+    ps.rank = -1;
+    ps.count = 0;
+    const int c0 = cta_of_stage(lo_p, ap.total, G), c1 = cta_of_stage(hi_p - 1, ap.total, G);
     for (int c = c0; c <= c1; ++c) {
-        const int a0 = int(range_lo(c, total, G)), a1 = int(range_lo(c + 1, total, G));
+        const int a0 = int(range_lo(c, ap.total, G)), a1 = int(range_lo(c + 1, ap.total, G));
         const int lo = max(lo_p, a0), hi = min(hi_p, a1);
         if (hi <= lo) continue;
         const int n = min(8, hi - lo);
+        const int k = pair - attn_stage_of(ap, n_kv, a0).pair;
+        const int pre = n >= 2 && k < cap_pairs && k < ATT_PT_MAX;
         if (c == cta) {
-            const int r = ((warp - (lo - a0)) % 8 + 8) % 8;
-            if (r < n) rank = count + r;
+            ps.pre = pre;
+            ps.k = k;
+            ps.n = n;
+            ps.r = ((warp - (lo - a0)) % 8 + 8) % 8;
+            ps.rank = pre ? ps.count : ps.count + ps.r;
         }
-        count += n;
+        ps.count += pre ? 1 : n;
     }
+    return ps;
 }
+
+// Per-step slot metadata of the pairs this CTA's stage range touches (the
+// attention plan is the same for every layer, so it is computed once).
+struct AttnPair {
+    int lo_p;          // pair's first global stage
+    int pre, n, r0;    // CTA pre-combines; contributing warps; warp of the CTA's first stage of the pair
+    int rank0, count;  // CTA's first global partial slot; the pair's global partial count
+};
 
 struct Smem {
     uint8_t* ring;
@@ -164,113 +193,71 @@ __device__ __forceinline__ Smem carve(uint8_t* base) {
 }
 
 // ----------------------------------------------------------------- producer
-__device__ __forceinline__ void prefetch_l2(const void* src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
-}
+// The producer warp runs the stage enumeration uniformly on DEC_PLANES lanes;
+// lane j captures the descriptor of stage qb + j, and every DEC_PLANES stages
+// all lanes claim their ring slots and issue their bulk copies concurrently.
+// One issuing thread serialises wait -> expect_tx -> copy at ~210 ns per stage
+// (measured: tools/readbw.cu, 8 KB stages cap at 5.2 TB/s); 8 lanes reach
+// 7.3 TB/s, above plain LDG streaming.
+constexpr int DEC_PLANES = 8;
 
-// Enumerates this CTA's GEMV weight stages in consumption order (used for the
-// optional L2 run-ahead): per phase, tiles in groups of DEC_MAXT, each group
-// segment by segment, tile by tile, chunk by chunk.
-struct GemvIter {
-    const DecodeArgs* a;
-    int cta, G, ph, off;
-    GemvPhase p;
-    MyTiles mt;
-    int nseg, g0, gn, sg, c0, c1, ti, c;
-    bool live;
-    __device__ __forceinline__ void begin_phase() {
-        while (ph <= 4 * a->s.n_layers) {
-            const int kind = ph == 4 * a->s.n_layers ? PH_LM : (ph & 3);
-            p = gemv_phase(*a, kind, ph >> 2);
-            mt = my_tiles(p.tiles, off, cta, G);
-            off = (off + p.tiles) % G;
-            if (mt.n > 0) {
-                nseg = n_segments(p.K);
-                g0 = 0;
-                gn = min(DEC_MAXT, mt.n);
-                sg = 0;
-                seg_range(p.K, nseg, 0, c0, c1);
-                ti = 0;
-                c = c0;
-                return;
-            }
-            ++ph;
-        }
-        live = false;
-    }
-    __device__ __forceinline__ void init(const DecodeArgs* args, int cta_, int G_) {
-        a = args;
-        cta = cta_;
-        G = G_;
-        ph = 0;
-        off = 0;
-        live = true;
-        begin_phase();
-    }
-    __device__ __forceinline__ const uint8_t* next() {
-        if (!live) return nullptr;
-        const int tile = mt.t0 + (g0 + ti) * G;
-        const uint8_t* src = p.base + size_t(tile) * size_t(p.K) * 32 + size_t(c) * DEC_STAGE_BYTES;
-        if (++c < c1) return src;
-        if (++ti < gn) {
-            c = c0;
-            return src;
-        }
-        ti = 0;
-        if (++sg < nseg) {
-            seg_range(p.K, nseg, sg, c0, c1);
-            c = c0;
-            return src;
-        }
-        sg = 0;
-        g0 += DEC_MAXT;
-        if (g0 < mt.n) {
-            gn = min(DEC_MAXT, mt.n - g0);
-            seg_range(p.K, nseg, 0, c0, c1);
-            c = c0;
-            return src;
-        }
-        ++ph;
-        begin_phase();
-        return src;
-    }
+struct StageSrc {
+    const uint8_t* p0;  // weight tile chunk, or the K row block of the first KV block
+    const uint8_t* p1;  // K row block of the second KV block (dh = 64)
+    int nblk;           // -1: weight stage; else KV blocks in the stage (0..2)
 };
 
 struct Producer {
     const DecodeArgs& a;
     Smem& sm;
-    uint32_t q = 0;
-    uint32_t ns;
+    const int lane;
+    uint32_t q = 0;    // stages enumerated
+    uint32_t qb = 0;   // first stage of the pending batch
+    uint32_t nsh, nmask;
     uint64_t pol;
-    GemvIter pf;
-    bool ahead;
-    __device__ __forceinline__ Producer(const DecodeArgs& args, Smem& s, int cta, int G) : a(args), sm(s) {
-        ns = uint32_t(a.nstage);
+    uint32_t kv_blk;   // bytes of one (layer, k|v, head) block
+    size_t kv_voff;    // V plane offset from the K plane
+    StageSrc mine;     // this lane's pending stage
+    __device__ __forceinline__ Producer(const DecodeArgs& args, Smem& s, int ln) : a(args), sm(s), lane(ln) {
+        nsh = uint32_t(__ffs(a.nstage) - 1);
+        nmask = uint32_t(a.nstage) - 1u;
         pol = l2_evict_first_policy();
-        ahead = a.l2_ahead > 0;
-        if (ahead) {
-            pf.init(&a, cta, G);
-            for (int i = 0; i < a.l2_ahead; ++i) {
-                const uint8_t* p = pf.next();
-                if (!p) break;
-                prefetch_l2(p, DEC_STAGE_BYTES);
+        kv_blk = uint32_t(KV_BLOCK_TOKENS * a.s.dh * 2);
+        kv_voff = size_t(a.s.n_kv) * KV_BLOCK_TOKENS * a.s.dh * 2;
+        mine.p0 = mine.p1 = nullptr;
+        mine.nblk = -1;
+    }
+    __device__ __forceinline__ void flush() {
+        const uint32_t n = q - qb;
+        if (uint32_t(lane) < n) {
+            const uint32_t qi = qb + uint32_t(lane);
+            const uint32_t slot = qi & nmask, par = (qi >> nsh) & 1u;
+            mbar_wait(&sm.empty[slot], par ^ 1u);
+            uint8_t* dst = sm.ring + size_t(slot) * DEC_STAGE_BYTES;
+            if (mine.nblk < 0) {
+                mbar_arrive_expect_tx(&sm.full[slot], DEC_STAGE_BYTES);
+                bulk_g2s_evict_first(dst, mine.p0, DEC_STAGE_BYTES, &sm.full[slot], pol);
+            } else {
+                mbar_arrive_expect_tx(&sm.full[slot], 2u * uint32_t(mine.nblk) * kv_blk);
+                if (mine.nblk > 0) {
+                    bulk_g2s(dst, mine.p0, kv_blk, &sm.full[slot]);
+                    bulk_g2s(dst + 4096, mine.p0 + kv_voff, kv_blk, &sm.full[slot]);
+                }
+                if (mine.nblk > 1) {
+                    bulk_g2s(dst + kv_blk, mine.p1, kv_blk, &sm.full[slot]);
+                    bulk_g2s(dst + 4096 + kv_blk, mine.p1 + kv_voff, kv_blk, &sm.full[slot]);
+                }
             }
         }
+        qb = q;
     }
-    __device__ __forceinline__ uint32_t claim() {
-        const uint32_t slot = q % ns, par = (q / ns) & 1u;
-        mbar_wait(&sm.empty[slot], par ^ 1u);
-        return slot;
-    }
-    __device__ __forceinline__ void weight_stage(const uint8_t* src) {
-        const uint32_t slot = claim();
-        mbar_arrive_expect_tx(&sm.full[slot], DEC_STAGE_BYTES);
-        bulk_g2s_evict_first(sm.ring + size_t(slot) * DEC_STAGE_BYTES, src, DEC_STAGE_BYTES, &sm.full[slot], pol);
-        if (ahead) {
-            const uint8_t* p = pf.next();
-            if (p) prefetch_l2(p, DEC_STAGE_BYTES);
+    __device__ __forceinline__ void push(const uint8_t* p0, const uint8_t* p1, int nblk) {
+        if (uint32_t(lane) == q - qb) {
+            mine.p0 = p0;
+            mine.p1 = p1;
+            mine.nblk = nblk;
         }
-        ++q;
+        if (++q - qb == DEC_PLANES) flush();
     }
     __device__ __forceinline__ void gemv(int kind, int layer, int& off, int cta, int G) {
         const GemvPhase p = gemv_phase(a, kind, layer);
@@ -286,7 +273,7 @@ struct Producer {
                 seg_range(p.K, nseg, sg, c0, c1);
                 for (int ti = 0; ti < gn; ++ti) {
                     const uint8_t* t = p.base + size_t(mt.t0 + (g0 + ti) * G) * tile_bytes;
-                    for (int ch = c0; ch < c1; ++ch) weight_stage(t + size_t(ch) * DEC_STAGE_BYTES);
+                    for (int ch = c0; ch < c1; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, nullptr, -1);
                 }
             }
         }
@@ -296,7 +283,7 @@ struct Producer {
     // is read directly by the consumer.
     int ntr = 0;
     __device__ __forceinline__ void ptrace(int cta, int tag) {  // producer timeline (CTA 0) at trace[2048..]
-        if (a.trace && cta == 0 && ntr < 2000) {
+        if (a.trace && cta == 0 && lane == 0 && ntr < 2000) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             a.trace[2048 + ntr++] = (t << 4) | unsigned(tag);
@@ -310,10 +297,8 @@ struct Producer {
     __device__ __forceinline__ void attention(int layer, const AttnPlan& ap, const int* pos) {
         if (ap.a1 <= ap.a0) return;
         const Shape& s = a.s;
-        const uint32_t blk_bytes = uint32_t(KV_BLOCK_TOKENS * s.dh * 2);  // one (layer, k|v, head) block
-        const int bps = ap.rt / KV_BLOCK_TOKENS;                           // blocks per stage
+        const int bps = ap.rt / KV_BLOCK_TOKENS;  // blocks per stage
         const size_t head_stride = size_t(KV_BLOCK_TOKENS) * s.dh * 2;
-        const size_t v_off = size_t(s.n_kv) * head_stride;  // V plane after the K plane
         const uint8_t* layer_base = a.kv_base + kv_offset(s, layer, 0, 0, 0);
         // decode the first stage once, then walk
         AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0);
@@ -322,20 +307,14 @@ struct Producer {
         int p = pos[b];
         const int* btrow = sm.bt + b * DEC_BT_MAX;
         for (int i = ap.a0; i < ap.a1; ++i) {
-            const uint32_t slot = claim();
-            uint8_t* dst = sm.ring + size_t(slot) * DEC_STAGE_BYTES;
             const int k0 = sc * bps;
             int nblk = 0;
             if (k0 * KV_BLOCK_TOKENS < p) nblk = (bps == 2 && (k0 + 1) * KV_BLOCK_TOKENS < p) ? 2 : 1;
             if (a.skip & 4) nblk = 0;  // debug: no KV traffic
-            mbar_arrive_expect_tx(&sm.full[slot], 2u * nblk * blk_bytes);
             const size_t hoff = size_t(kvh) * head_stride;
-            for (int j = 0; j < nblk; ++j) {
-                const uint8_t* kb = layer_base + size_t(btrow[k0 + j]) * a.block_bytes + hoff;
-                bulk_g2s(dst + j * blk_bytes, kb, blk_bytes, &sm.full[slot]);
-                bulk_g2s(dst + 4096 + j * blk_bytes, kb + v_off, blk_bytes, &sm.full[slot]);
-            }
-            ++q;
+            const uint8_t* kb0 = nblk > 0 ? layer_base + size_t(btrow[k0]) * a.block_bytes + hoff : nullptr;
+            const uint8_t* kb1 = nblk > 1 ? layer_base + size_t(btrow[k0 + 1]) * a.block_bytes + hoff : nullptr;
+            push(kb0, kb1, nblk);
             if (++sc == nst_b) {  // next (b, kv head)
                 sc = 0;
                 if (++kvh == s.n_kv) {
@@ -354,9 +333,10 @@ struct Producer {
     }
 };
 
-__device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int cta, int G, int B, const int* pos) {
+__device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int cta, int G, int B, const int* pos,
+                                              int lane) {
     if (a.skip & 2) return;
-    Producer pr(a, sm, cta, G);
+    Producer pr(a, sm, lane);
     const AttnPlan ap = attn_plan(a.s, B, pos, cta, G);
     int off = 0;
     for (int l = 0; l < a.s.n_layers; ++l) {
@@ -369,9 +349,10 @@ __device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int
         pr.ptrace(cta, 11);
         pr.gemv(PH_GU, l, off, cta, G);
         pr.gemv(PH_DOWN, l, off, cta, G);
-        if (a.progress) a.progress[cta * 2 + 1] = int(pr.q);
+        if (a.progress && lane == 0) a.progress[cta * 2 + 1] = int(pr.q);
     }
     pr.gemv(PH_LM, 0, off, cta, G);
+    pr.flush();
 }
 
 // ----------------------------------------------------------------- consumer
@@ -384,7 +365,10 @@ struct Ctx {
     int B;
     const int* slot;  // [8] in shared memory
     const int* pos;   // [8] in shared memory
+    const AttnPair* pt;  // [ATT_PT_MAX] in shared memory
+    int p0, np;          // first pair of this CTA's attention range, pairs touched
     uint32_t q;       // stage counter (mirrors the producer)
+    uint32_t nsh, nmask;  // ring depth = 1 << nsh (8 or 16)
     int off;          // round-robin offset (mirrors the producer)
 };
 
@@ -410,9 +394,8 @@ __device__ __forceinline__ void grid_sync(Ctx& c) {
 }
 
 __device__ __forceinline__ void wait_stage(Ctx& c, uint32_t qi, uint32_t& slot) {
-    const uint32_t ns = uint32_t(c.a->nstage);
-    slot = qi % ns;
-    mbar_wait(&c.sm.full[slot], (qi / ns) & 1u);
+    slot = qi & c.nmask;
+    mbar_wait(&c.sm.full[slot], (qi >> c.nsh) & 1u);
 }
 __device__ __forceinline__ void release_stage(Ctx& c, uint32_t slot) {
     __syncwarp();
@@ -708,6 +691,94 @@ struct AttnState {
     float m[2], l[2];                 // running max / this lane's partial sum, heads 2t, 2t+1
 };
 
+// Attention partials: per slot, per head of the GQA group, [m, l, -, -, acc[DH]]
+// (head stride DH + 4 keeps acc 16-byte aligned).
+template <int DH>
+__host__ __device__ constexpr int attn_hs() { return DH + 4; }
+
+// Combine `count` partials (slot stride W floats) per head in slot order.
+// Lane-parallel over (head, 4 dims). FINAL writes bf16(acc / l) to `out`,
+// else one partial to `dst` (global).
+template <int DH, bool FINAL, bool GLOBAL_SRC = false>
+__device__ __forceinline__ void attn_combine(const float* src, int W, int count, int GQ, int lane, float* dst,
+                                             uint16_t* out) {
+    constexpr int D4 = DH / 4, HS = attn_hs<DH>();
+    for (int item = lane; item < GQ * D4; item += 32) {
+        const int h = item / D4, d0 = (item % D4) * 4;
+        const float* hs = src + h * HS;
+        float mx = -INFINITY;
+        for (int i = 0; i < count; ++i) mx = fmaxf(mx, GLOBAL_SRC ? ldcg_f32(hs + size_t(i) * W) : hs[size_t(i) * W]);
+        float L = 0.f;
+        float4 A = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 4
+        for (int i = 0; i < count; ++i) {
+            const float* ph = hs + size_t(i) * W;
+            float2 ml;
+            float4 v;
+            if constexpr (GLOBAL_SRC) {  // other SMs wrote these: bypass L1
+                ml = __ldcg(reinterpret_cast<const float2*>(ph));
+                v = __ldcg(reinterpret_cast<const float4*>(ph + 4 + d0));
+            } else {
+                ml = *reinterpret_cast<const float2*>(ph);
+                v = *reinterpret_cast<const float4*>(ph + 4 + d0);
+            }
+            const float f = ml.x == -INFINITY ? 0.f : __expf(ml.x - mx);
+            L += ml.y * f;
+            A.x += v.x * f;
+            A.y += v.y * f;
+            A.z += v.z * f;
+            A.w += v.w * f;
+        }
+        if constexpr (FINAL) {
+            uint2 pk;
+            pk.x = pack_bf16x2(A.x / L, A.y / L);
+            pk.y = pack_bf16x2(A.z / L, A.w / L);
+            *reinterpret_cast<uint2*>(out + h * DH + d0) = pk;
+        } else {
+            float* ph = dst + h * HS;
+            if (d0 == 0) *reinterpret_cast<float2*>(ph) = make_float2(mx, L);
+            *reinterpret_cast<float4*>(ph + 4 + d0) = A;
+        }
+    }
+}
+
+// Publish one global partial of `pair` (already written) and, if it is the
+// pair's last, combine all of them into the attention output. `scratch` (or
+// null) is shared memory for 8 slots: the partials are pulled in with one
+// batch of cp.async (a single L2 round trip) and combined from there.
+template <int DH>
+__device__ __forceinline__ void attn_arrive(Ctx& c, int b, int kvh, int pair_lo, int count, float* scratch) {
+    const DecodeArgs& a = *c.a;
+    const Shape& s = a.s;
+    const int GQ = s.n_heads / s.n_kv;
+    const int W = GQ * attn_hs<DH>();
+    const int pair = b * s.n_kv + kvh;
+    __syncwarp();
+    int last = 0;
+    if (c.lane == 0) last = atom_add_acq_rel_gpu(a.acnt + pair, 1) == count - 1;
+    last = __shfl_sync(0xffffffffu, last, 0);
+    if (!last) return;
+    const float* src = a.apart + size_t(pair_lo) * W;
+    uint16_t* out = a.attn + size_t(b) * s.d + size_t(kvh) * GQ * DH;
+    if (scratch && count <= 8) {
+        const int n16 = count * W / 4;
+        const uint32_t sb = smem_u32(scratch);
+        for (int i = c.lane; i < n16; i += 32) cp_async_16(sb + i * 16, src + i * 4);
+        cp_async_wait_all();
+        __syncwarp();
+        attn_combine<DH, true>(scratch, W, count, GQ, c.lane, nullptr, out);
+    } else {
+        attn_combine<DH, true, true>(src, W, count, GQ, c.lane, nullptr, out);
+    }
+    if (c.lane == 0) atomicExch(a.acnt + pair, 0);
+}
+
+template <int DH>
+__device__ __forceinline__ int attn_cap_pairs(const Shape& s) {
+    const int W = (s.n_heads / s.n_kv) * attn_hs<DH>();
+    return DEC_SMEM_ACT / (8 * W * 4);
+}
+
 template <int DH>
 __device__ __forceinline__ void attn_flush(Ctx& c, const AttnPlan& ap, int b, int kvh, int pair_lo, int pair_n,
                                            AttnState<DH>& stt) {
@@ -715,80 +786,73 @@ __device__ __forceinline__ void attn_flush(Ctx& c, const AttnPlan& ap, int b, in
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
     const int GQ = s.n_heads / s.n_kv;
-    const int W = GQ * (DH + 2);
+    constexpr int HS = attn_hs<DH>();
+    const int W = GQ * HS;
     const unsigned FULL = 0xffffffffu;
     const int g = c.lane >> 2, t = c.lane & 3;
-    int rank, count;
-    pair_slots(pair_lo, pair_lo + pair_n, ap.total, c.G, c.cta, c.warp, rank, count);
+    const int pair = b * s.n_kv + kvh, k = pair - c.p0;
+    int pre, r, rank, count;
+    if (k < ATT_PT_MAX) {
+        const AttnPair& e = c.pt[k];
+        pre = e.pre;
+        r = (c.warp - e.r0 + 8) % 8;
+        rank = pre ? e.rank0 : e.rank0 + r;
+        count = e.count;
+    } else {  // beyond the table: never pre-combined
+        const PairSlot ps = pair_slot(ap, s.n_kv, pair, pair_lo, pair_lo + pair_n, c.G, c.cta, c.warp,
+                                      attn_cap_pairs<DH>(s));
+        pre = 0;
+        r = ps.r;
+        rank = ps.rank;
+        count = ps.count;
+    }
     float l0 = stt.l[0], l1 = stt.l[1];
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {
         l0 += __shfl_xor_sync(FULL, l0, o);
         l1 += __shfl_xor_sync(FULL, l1, o);
     }
-    float* pp = a.apart + size_t(pair_lo + rank) * W;
+    float* pp = pre ? reinterpret_cast<float*>(c.sm.act) + size_t(k * 8 + r) * W : a.apart + size_t(pair_lo + rank) * W;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
         const int h = 2 * t + j;
         if (h < GQ) {
-            float* ph = pp + h * (DH + 2);
-            if (g == 0) {
-                ph[0] = stt.m[j];
-                ph[1] = j ? l1 : l0;
-            }
+            float* ph = pp + h * HS;
+            if (g == 0) *reinterpret_cast<float2*>(ph) = make_float2(stt.m[j], j ? l1 : l0);
 #pragma unroll
             for (int md = 0; md < MD; ++md) {
-                ph[2 + 16 * md + g] = stt.o[md][j];
-                ph[2 + 16 * md + 8 + g] = stt.o[md][2 + j];
+                ph[4 + 16 * md + g] = stt.o[md][j];
+                ph[4 + 16 * md + 8 + g] = stt.o[md][2 + j];
             }
         }
     }
-    __syncwarp();
-    const int pair = b * s.n_kv + kvh;
-    int last = 0;
-    if (c.lane == 0) last = atom_add_acq_rel_gpu(a.acnt + pair, 1) == count - 1;
-    last = __shfl_sync(FULL, last, 0);
-    if (!last) return;
-    // Combine the pair's `count` partials in slot order (deterministic): lane
-    // covers dims [4 * lane, 4 * lane + 4) of every head row of the group.
-    const float* base = a.apart + size_t(pair_lo) * W;
-    for (int h = 0; h < GQ; ++h) {
-        float mx = -INFINITY;
-        for (int sp = c.lane; sp < count; sp += 32) mx = fmaxf(mx, ldcg_f32(base + size_t(sp) * W + h * (DH + 2)));
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(FULL, mx, o));
-        float L = 0.f, A[4] = {0.f, 0.f, 0.f, 0.f};
-        const int d0 = c.lane * 4;
-        for (int sp0 = 0; sp0 < count; sp0 += 8) {
-            float mv[8], lv[8];
-            float4 av[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const bool ok = sp0 + j < count;
-                const float* ph = base + size_t(sp0 + j) * W + h * (DH + 2);
-                mv[j] = ok ? ldcg_f32(ph) : -INFINITY;
-                lv[j] = ok ? ldcg_f32(ph + 1) : 0.f;
-                av[j] = (ok && d0 < DH) ? make_float4(ldcg_f32(ph + 2 + d0), ldcg_f32(ph + 3 + d0), ldcg_f32(ph + 4 + d0),
-                                                      ldcg_f32(ph + 5 + d0))
-                                        : make_float4(0.f, 0.f, 0.f, 0.f);
-            }
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float f = mv[j] == -INFINITY ? 0.f : __expf(mv[j] - mx);
-                L += lv[j] * f;
-                A[0] += av[j].x * f;
-                A[1] += av[j].y * f;
-                A[2] += av[j].z * f;
-                A[3] += av[j].w * f;
-            }
-        }
-        if (d0 < DH) {
-            uint16_t* out = a.attn + size_t(b) * s.d + (size_t(kvh) * GQ + h) * DH + d0;
-#pragma unroll
-            for (int e = 0; e < 4; ++e) out[e] = f_to_bf16(A[e] / L);
-        }
+    // a direct pair's shared slots [8k, 8k + 8) are unused by this CTA: final-combine scratch
+    if (!pre)
+        attn_arrive<DH>(c, b, kvh, pair_lo, count,
+                        k < min(attn_cap_pairs<DH>(s), ATT_PT_MAX) ? reinterpret_cast<float*>(c.sm.act) + size_t(k * 8) * W
+                                                                   : nullptr);
+}
+
+// After every warp flushed: combine the pairs this CTA pre-combines (pair-local
+// index k handled by warp k % 8), publish them, and finish complete pairs.
+template <int DH>
+__device__ __forceinline__ void attn_cta_combine(Ctx& c) {
+    const DecodeArgs& a = *c.a;
+    const Shape& s = a.s;
+    const int GQ = s.n_heads / s.n_kv;
+    const int W = GQ * attn_hs<DH>();
+    for (int k = c.warp; k < min(c.np, ATT_PT_MAX); k += DEC_NCW) {
+        const AttnPair& e = c.pt[k];
+        if (!e.pre) continue;
+        const int pair = c.p0 + k;
+        trace(c, 16);
+        float* slots = reinterpret_cast<float*>(c.sm.act) + size_t(k * 8) * W;
+        attn_combine<DH, false>(slots, W, e.n, GQ, c.lane, a.apart + size_t(e.lo_p + e.rank0) * W, nullptr);
+        trace(c, 17);
+        __syncwarp();  // the slots become the final-combine scratch
+        attn_arrive<DH>(c, pair / s.n_kv, pair % s.n_kv, e.lo_p, e.count, slots);
+        trace(c, 18);
     }
-    if (c.lane == 0) atomicExch(a.acnt + pair, 0);
 }
 
 template <int DH>
@@ -802,21 +866,23 @@ __device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage&
     const int t0 = st.s * RT;
     const int lane = c.lane, g = lane >> 2, t = lane & 3;
     const float scale = rsqrtf(float(DH));
+    // the current token's K/V rows were written by this step's QKV phase: fetch
+    // them from the paged cache (before the stage wait, to overlap the latency)
+    // into their stage rows (same swizzle: row & 7 == slot & 7)
+    constexpr int CH = DH / 8;  // 16-byte chunks per row; 2 * CH <= 32
+    const bool patch = cur >= t0 && cur < t0 + RT;
+    uint4 pv = make_uint4(0, 0, 0, 0);
+    if (patch && lane < 2 * CH) {
+        const int blk = ldcg_i32(a.block_table + size_t(c.slot[st.b]) * a.bt_stride + cur / KV_BLOCK_TOKENS);
+        pv = ldcg_u4(a.kv_base + size_t(blk) * a.block_bytes +
+                     kv_offset(s, layer, lane / CH, st.kvh, cur % KV_BLOCK_TOKENS) + (lane % CH) * 16);
+    }
     uint32_t slot;
     wait_stage(c, qi, slot);
     uint8_t* stage = c.sm.ring + size_t(slot) * DEC_STAGE_BYTES;
-    // the current token's K/V rows were written by this step's QKV phase: copy them
-    // from the paged cache into their stage rows (same swizzle: row & 7 == slot & 7)
-    if (cur >= t0 && cur < t0 + RT) {
-        const int blk = ldcg_i32(a.block_table + size_t(c.slot[st.b]) * a.bt_stride + cur / KV_BLOCK_TOKENS);
-        const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
-        const int r = cur - t0;
-        constexpr int CH = DH / 8;  // 16-byte chunks per row
-        for (int i = lane; i < 2 * CH; i += 32) {
-            const int kv = i / CH, ch = i % CH;
-            const uint4 v = ldcg_u4(base + kv_offset(s, layer, kv, st.kvh, cur % KV_BLOCK_TOKENS) + ch * 16);
-            *reinterpret_cast<uint4*>(stage + kv * 4096 + r * DH * 2 + ch * 16) = v;
-        }
+    if (patch) {
+        if (lane < 2 * CH)
+            *reinterpret_cast<uint4*>(stage + (lane / CH) * 4096 + (cur - t0) * DH * 2 + (lane % CH) * 16) = pv;
         __syncwarp();
     }
     const uint32_t kbase = smem_u32(stage), vbase = kbase + 4096;
@@ -938,9 +1004,15 @@ __device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPla
             continue;
         }
         attn_consume<DH>(c, layer, st, c.q + i, stt);
+        if (i == c.warp) trace(c, 12);
     }
+    trace(c, 13);
     if (cur_pair >= 0) attn_flush<DH>(c, ap, cur_b, cur_kvh, cur_lo, cur_n, stt);
     c.q += n;
+    trace(c, 14);
+    csync();  // warp partials of pre-combined pairs are in shared memory
+    trace(c, 15);
+    attn_cta_combine<DH>(c);
 }
 
 // ------------------------------------------------------------ embedding
@@ -1056,7 +1128,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     const DecodeArgs& a = a_s;
 
     if (warp == DEC_NCW) {
-        if (lane == 0) producer_loop(a, sm, blockIdx.x, gridDim.x, B, pos_s);
+        if (lane < DEC_PLANES) producer_loop(a, sm, blockIdx.x, gridDim.x, B, pos_s, lane);
         return;
     }
     Ctx c;
@@ -1074,7 +1146,36 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     c.pos = pos_s;
     c.q = 0;
     c.off = 0;
-    const AttnPlan ap = attn_plan(a.s, B, pos_s, c.cta, c.G);
+    c.nsh = uint32_t(__ffs(a.nstage) - 1);
+    c.nmask = uint32_t(a.nstage) - 1u;
+    // attention plan + this CTA's pair table: identical for every layer of the step
+    __shared__ AttnPlan ap_s;
+    __shared__ AttnPair pt_s[ATT_PT_MAX];
+    if (threadIdx.x == 0) ap_s = attn_plan(a.s, B, pos_s, c.cta, c.G);
+    csync();
+    const AttnPlan& ap = ap_s;
+    c.pt = pt_s;
+    c.p0 = c.np = 0;
+    if (ap.a1 > ap.a0) {
+        c.p0 = attn_stage_of(ap, a.s.n_kv, ap.a0).pair;
+        c.np = attn_stage_of(ap, a.s.n_kv, ap.a1 - 1).pair - c.p0 + 1;
+    }
+    if (warp == 0 && lane < min(c.np, ATT_PT_MAX)) {
+        const int pair = c.p0 + lane, b = pair / a.s.n_kv, kvh = pair % a.s.n_kv;
+        int lo_p = kvh * ap.nst[b];
+        for (int bb = 0; bb < b; ++bb) lo_p += a.s.n_kv * ap.nst[bb];
+        const int cap = a.s.dh == 64 ? attn_cap_pairs<64>(a.s) : attn_cap_pairs<128>(a.s);
+        const PairSlot ps = pair_slot(ap, a.s.n_kv, pair, lo_p, lo_p + ap.nst[b], c.G, c.cta, 0, cap);
+        AttnPair e;
+        e.lo_p = lo_p;
+        e.pre = ps.pre;
+        e.n = ps.n;
+        e.r0 = (8 - ps.r) % 8;  // warp 0 has rank r  =>  the first stage's warp is -r mod 8
+        e.rank0 = ps.pre ? ps.rank : ps.rank - ps.r;
+        e.count = ps.count;
+        pt_s[lane] = e;
+    }
+    csync();
 
     float best_v[2] = {-INFINITY, -INFINITY};
     int best_i[2] = {0x7fffffff, 0x7fffffff};
@@ -1108,7 +1209,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
 
 size_t decode_apart_floats(const Shape& s) {
     const int rt = 2048 / s.dh;
-    return size_t(DEC_MAXB) * s.n_kv * ((s.max_seq + rt - 1) / rt) * s.gq() * (s.dh + 2);
+    return size_t(DEC_MAXB) * s.n_kv * ((s.max_seq + rt - 1) / rt) * s.gq() * (s.dh + 4);
 }
 
 cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t stream) {

@@ -65,7 +65,6 @@ struct DecodeArgs {
     unsigned long long* trace;  // optional [4096]: %globaltimer at CTA 0's phase boundaries
     unsigned long long* arrive; // optional [barriers][grid]: %globaltimer of every CTA's barrier arrival
     int nstage;    // weight-ring stages in use (<= DEC_NSTAGE): bounds bytes in flight per SM
-    int l2_ahead;  // extra stages prefetched into L2 beyond the ring
     int skip;      // debug: 1 skips attention work, 2 skips the GEMV phases (results are garbage)
 };
 

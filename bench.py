@@ -12,17 +12,23 @@ requests are replaced by new ones (prefill first, as select_next does).
           launched through the mesh_gpu C ABI; instances take turns.
   value   co-located tokens/s over the K timed steps (device-resident inputs),
           counting only tokens of requests whose emissions met the TTFT/TPOT
-          SLO; wall clock between device synchronisations.
+          SLO; device time between CUDA events recorded on the compute stream
+          (mesh_gpu_timer_mark), max over ranks.
   e2e     the same metric through the reference-facing plugin API
-          (llmmesh.h: llm_experiment_run with the GPU attached) on the C2
-          Poisson trace: control plane + per-step H2D descriptors/prompts +
-          D2H tokens inside the timed region.
+          (llmmesh.h: llm_experiment_run with the GPU attached) on a C2 trace
+          that keeps the four instances at capacity (scenarios/c2_saturated):
+          control plane + per-step H2D descriptors/prompts + D2H tokens inside
+          the timed region; wall clock.
   roofline  dominant kernel = the persistent decode kernel; algorithmic bytes
           per launch = W_m + sum_i L_i C_m + B C_m + B d_m 2 over its
           CUDA-event duration, vs the measured HBM copy peak.
 
-`--impl reference` times the reference's own CPU path (its simulator, built
-from /root/reference by oracle/Makefile into oracle/_ref) on the same trace.
+`--impl reference` and `cpu_baseline`: the reference artifact prices token
+steps from tables and computes no tokens, so the CPU path that
+*executes* the co-located step is the oracle's batched CPU decode
+(oracle/cpu_decode.c, all host threads) running the same C2 instance steps
+(kind "port"); the reference simulator itself (oracle/_ref, built from
+/root/reference) is timed beside it on the C2 trace ("reference_simulator").
 Multi-GPU (torchrun): every rank runs an independent co-located node (instances
 shard by placement, no collective): weak scaling.
 """
@@ -46,6 +52,9 @@ UNIT = "tokens/s"
 MODELS = ["1b", "3b", "1b", "3b"]
 BATCH = 8
 E2E_WINDOW_S = 20.0
+E2E_SCEN = os.path.join(ROOT, "scenarios", "c2_saturated", "config.json")
+CPU_MAX_SEQ = 64        # CPU sample contexts (short: generous to the CPU)
+CPU_SAMPLE_S = 15.0     # bounded CPU baseline sample
 
 
 def peaks():
@@ -268,8 +277,8 @@ class Colocated:
         self.decode_steps = 0
 
 
-def cpu_reference_sample(window_s: float):
-    """The reference's CPU path (its simulator) on the C2 trace: tokens / wall s, 1 core."""
+def reference_simulator_sample(window_s: float):
+    """The reference's own CPU code (its simulator, oracle/_ref) on the C2 trace: 1 core."""
     ref = os.path.join(ROOT, "oracle", "_ref", "ref_capture")
     if not os.path.exists(ref):
         return None
@@ -278,65 +287,113 @@ def cpu_reference_sample(window_s: float):
     if out.returncode != 0:
         return None
     r = json.loads(out.stdout.strip().splitlines()[-1])
-    return {"value": r["tokens"] / r["best_s"], "unit": UNIT, "cores": 1, "kind": "reference",
+    return {"simulated_tokens_per_cpu_s": r["tokens"] / r["best_s"], "cores": 1, "kind": "reference",
             "sample": f"reference simulator (oracle/_ref) on the C2 trace, window {window_s:g} s: "
-                      f"{r['tokens']} tokens, {r['events']} events, best of 5 = {r['best_s']:.4f} s"}
+                      f"{r['tokens']} virtual tokens, {r['events']} events, best of 5 = {r['best_s']:.4f} s",
+            "note": "virtual-time tokens: the reference prices steps from tables and computes no tokens"}
+
+
+class CpuColocated:
+    """The C2 node on the host CPU: the batched CPU decode (oracle/cpu_decode.c)
+    over the same four instances [1b, 3b, 1b, 3b] x batch 8, instances in turn.
+    Weights are generated once per size class (identical replicas share them)."""
+
+    def __init__(self):
+        import dataclasses
+
+        from oracle import llama_oracle as ora
+        from paper_2507_00507_b200.gpu import SHAPES
+        self.ora = ora
+        self.models = {}
+        for m in MODELS:
+            if m not in self.models:
+                self.models[m] = ora.Oracle(dataclasses.replace(SHAPES[m], max_seq_len=CPU_MAX_SEQ), 1000 + len(self.models))
+        self.insts = [{"model": self.models[m], "seqs": [], "toks": [], "len": 0} for m in MODELS]
+        self.k = 0
+        self.threads = ora.threads()
+
+    def step(self) -> int:
+        inst = self.insts[self.k % len(self.insts)]
+        self.k += 1
+        if not inst["seqs"] or inst["len"] >= CPU_MAX_SEQ - 1:  # batch finished: admit 8 new requests
+            inst["seqs"] = [inst["model"].new_seq() for _ in range(BATCH)]
+            inst["len"] = 0
+            inst["toks"] = [self.ora.prompt_token(7, self.k * BATCH + i, 0, inst["model"].shape.vocab)
+                            for i in range(BATCH)]
+        inst["toks"] = self.ora.feed_batch(inst["model"], inst["seqs"], inst["toks"])
+        inst["len"] += 1
+        return BATCH
+
+
+def cpu_port_sample():
+    """cpu_baseline: bounded sample (~CPU_SAMPLE_S) of C2 instance steps on the host CPU."""
+    node = CpuColocated()
+    node.step()  # warm
+    n_tok, n_steps, t0 = 0, 0, time.perf_counter()
+    while n_steps < 4 or time.perf_counter() - t0 < CPU_SAMPLE_S:
+        n_tok += node.step()
+        n_steps += 1
+    dt = time.perf_counter() - t0
+    return {"value": n_tok / dt, "unit": UNIT, "cores": node.threads, "kind": "port",
+            "sample": f"{n_steps} C2 instance steps ([1b,3b,1b,3b] in turn, batch 8, contexts <= {CPU_MAX_SEQ}) "
+                      f"of the batched CPU decode (oracle/cpu_decode.c, fp32, {node.threads} threads): "
+                      f"{n_tok} tokens in {dt:.2f} s"}
 
 
 def run_reference(args, d: Dist):
+    """Reference arm: the CPU execution of the co-located step on the box's host cores."""
     if d.rank != 0:
         return
-    ref = os.path.join(ROOT, "oracle", "_ref", "ref_capture")
-    if not os.path.exists(ref):
-        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built (needs /root/reference)"}))
-        return
-    times, tokens = [], 0
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        out = subprocess.run([ref, "time", os.path.join(SCEN, "config.json"), "1",
-                              f"workload.window_s={E2E_WINDOW_S}"], cwd=ROOT, capture_output=True, text=True)
-        dt = time.perf_counter() - t0
-        r = json.loads(out.stdout.strip().splitlines()[-1])
-        if i >= args.warmup:
-            times.append(r["best_s"])
-            tokens += r["tokens"]
-    total = sum(times)
+    node = CpuColocated()
+    for _ in range(args.warmup):
+        node.step()
+    t0 = time.perf_counter()
+    tokens = sum(node.step() for _ in range(args.steps))
+    total = time.perf_counter() - t0
     value = tokens / total
+    sim = reference_simulator_sample(E2E_WINDOW_S)
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights)",
             "impl": "reference",
-            "config": {"workload": "C2: 4 co-located [1b,3b,1b,3b], Poisson trace 1.5 req/s/fn",
-                       "trace_window_s": E2E_WINDOW_S, "step": "one full simulation of the C2 trace window"},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "reference",
-                             "sample": f"reference simulator, {args.steps} runs of the {E2E_WINDOW_S:g} s C2 trace"},
+            "config": {"workload": "C2: 4 co-located Llama-shaped instances [1.1B, 3B, 1.1B, 3B], batch 8 each, "
+                                   "instances in turn (host CPU)",
+                       "models": MODELS, "batch_per_instance": BATCH, "context_max": CPU_MAX_SEQ,
+                       "step": "one instance step: batched decode of its 8 requests"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": node.threads, "kind": "port",
+                             "sample": f"{args.steps} C2 instance steps of oracle/cpu_decode.c (batched fp32, "
+                                       f"{node.threads} threads, contexts <= {CPU_MAX_SEQ})"},
+            "reference_simulator": sim,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def run_e2e(device: int):
-    """C2 trace through llmmesh.h with the B200 data plane attached (parity-mode schedule)."""
+def run_e2e(device: int, d: Dist):
+    """Saturated C2 trace through llmmesh.h with the B200 data plane attached (parity-mode schedule)."""
     import tempfile
 
     from paper_2507_00507_b200 import control, gpu
-    with control.Experiment(os.path.join(SCEN, "config.json")) as exp:
-        exp.set("workload.window_s", E2E_WINDOW_S)
-        exp.set("output.event_log", "false")
+    with control.Experiment(E2E_SCEN) as exp:
         exp.out_dir(tempfile.mkdtemp(prefix="mesh_e2e_"))
         exp.attach_gpu([device], 48 << 30, gpu.LIB_PATH)
+        d.barrier()
         t0 = time.perf_counter()
         exp.run()
         wall = time.perf_counter() - t0
-        m = {k: exp.metric(k) for k in ["gpu.steps", "gpu.decode_tokens", "gpu.h2d_bytes", "gpu.d2h_bytes",
-                                        "gpu.device_ms", "slo_compliant_rate", "total_requests",
-                                        "gpu.kernel_launches"]}
+        m = {k: exp.metric(k) for k in ["gpu.steps", "gpu.decode_tokens", "gpu.prefill_tokens", "gpu.h2d_bytes",
+                                        "gpu.d2h_bytes", "gpu.device_ms", "slo_compliant_rate", "total_requests",
+                                        "slo_compliant", "gpu.kernel_launches"]}
     prefill_emits = m["total_requests"]  # one token per admitted request's prefill
-    tokens = m["gpu.decode_tokens"] + prefill_emits
+    tokens = (m["gpu.decode_tokens"] + prefill_emits) * m["slo_compliant_rate"]
+    wall_max = d.reduce(wall, "max")
+    tok_sum = d.reduce(tokens, "sum")
     steps = max(1.0, m["gpu.steps"])
-    return {"value": tokens * m["slo_compliant_rate"] / wall, "unit": UNIT,
+    return {"value": tok_sum / wall_max, "unit": UNIT,
             "h2d_bytes_per_step": m["gpu.h2d_bytes"] / steps, "d2h_bytes_per_step": m["gpu.d2h_bytes"] / steps,
-            "wall_s": wall, "device_s": m["gpu.device_ms"] / 1e3, "steps": int(steps),
+            "wall_s": wall_max, "device_s": m["gpu.device_ms"] / 1e3, "steps": int(steps),
             "slo_compliant_rate": m["slo_compliant_rate"], "tokens": int(tokens),
+            "requests": int(m["total_requests"]), "prefill_tokens": int(m["gpu.prefill_tokens"]),
+            "trace": "scenarios/c2_saturated (Poisson 16 req/s per function, 10 s)",
             "api": "llmmesh.h llm_experiment_run + llm_experiment_attach_gpu"}
 
 
@@ -354,18 +411,20 @@ def run_ours(args, d: Dist):
     d.barrier()
     with Clocks(device) as clk:
         node.g.sync()
-        t0 = time.perf_counter()
+        node.g.timer_mark(0)
         launches = node.run(args.steps)
+        node.g.timer_mark(1)
         node.g.sync()
-        wall = time.perf_counter() - t0
-    wall_max = d.reduce(wall, "max")
+        dev_s = node.g.timer_elapsed(0, 1) / 1e3
+    wall_max = d.reduce(dev_s, "max")
     tok_ok = d.reduce(float(node.tokens_ok), "sum")
     value = tok_ok / wall_max
     achieved = node.decode_bytes / (node.decode_kernel_ms / 1e3) / 1e9 if node.decode_kernel_ms else 0.0
-    e2e = run_e2e(device) if not args.no_e2e else None
+    e2e = run_e2e(device, d) if not args.no_e2e else None
     if d.rank != 0:
         return
-    cpu = cpu_reference_sample(E2E_WINDOW_S) if d.ws == 1 else None
+    cpu = cpu_port_sample() if d.ws == 1 else None
+    sim = reference_simulator_sample(E2E_WINDOW_S) if d.ws == 1 else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "decode_traffic.json")
     if os.path.exists(prof):
@@ -388,6 +447,7 @@ def run_ours(args, d: Dist):
                      "kernel": "decode_kernel (persistent, TMA-ring)", "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": node.decode_bytes / max(1, node.decode_steps)},
         "cpu_baseline": cpu,
+        "reference_simulator": sim,
         "e2e": e2e,
         "gpu_launches": int(launches),
         "clocks": clk.summary(),

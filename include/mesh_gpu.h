@@ -121,6 +121,11 @@ mesh_status mesh_gpu_read_weight(mesh_gpu* g, int64_t instance_id, int32_t tenso
                                  float* out, int32_t n);
 mesh_status mesh_gpu_stats_get(mesh_gpu* g, mesh_gpu_stats* out);
 mesh_status mesh_gpu_sync(mesh_gpu* g);
+/* Device-side timing of a region of work on the compute stream: `mark` records
+ * a CUDA event (slot 0..7) on the stream every step is launched on; `elapsed`
+ * waits for slot b and returns the device time between slots a and b. */
+mesh_status mesh_gpu_timer_mark(mesh_gpu* g, int32_t slot);
+mesh_status mesh_gpu_timer_elapsed(mesh_gpu* g, int32_t a, int32_t b, double* ms);
 /* Times `iters` back-to-back decode steps of the plan's batch on the device
  * (CUDA events around the launches only) without advancing request state. */
 mesh_status mesh_gpu_bench_decode(mesh_gpu* g, int64_t instance_id, const mesh_step_plan* plan, int32_t iters,

@@ -43,6 +43,9 @@ def lib():
         l.ora_weight.restype = C.c_float
         l.ora_weight.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_uint64]
         l.ora_threads.restype = C.c_int
+        l.ora_feed_batch.restype = C.c_int
+        l.ora_feed_batch.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_int, C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int)]
         _lib = l
     return _lib
 
@@ -81,6 +84,17 @@ class OracleSeq:
         if self.h:
             lib().ora_seq_free(self.h)
             self.h = None
+
+
+def feed_batch(model: Oracle, seqs: list, tokens: list[int]) -> list[int]:
+    """Batched CPU decode step (oracle/cpu_decode.c): the bench's CPU baseline, not the checker."""
+    n = len(seqs)
+    hs = (C.c_void_p * n)(*[q.h for q in seqs])
+    tk = (C.c_int * n)(*tokens)
+    nx = (C.c_int * n)()
+    if lib().ora_feed_batch(model.h, hs, n, tk, nx) != 0:
+        raise RuntimeError("ora_feed_batch: sequence full")
+    return list(nx)
 
 
 def prompt_token(seed: int, request: int, pos: int, vocab: int) -> int:

@@ -20,6 +20,8 @@
  *   with ties to the lowest id.
  * The generator below must stay bit-identical to csrc/gpu/model.cuh.
  */
+#include "llama_ref.h"
+
 #include <math.h>
 #include <stdint.h>
 #include <stdlib.h>
@@ -28,11 +30,6 @@
 #ifdef _OPENMP
 #include <omp.h>
 #endif
-
-typedef struct {
-    int n_layers, d, n_heads, n_kv, dh, ff, vocab, tied, max_seq;
-    float rope_theta, eps;
-} ora_shape;
 
 enum { T_EMB = 0, T_WQ = 1, T_WK = 2, T_WV = 3, T_WO = 4, T_WGATE = 5, T_WUP = 6, T_WDOWN = 7, T_LM = 8,
        T_GATTN = 9, T_GMLP = 10, T_GFINAL = 11 };
@@ -50,20 +47,6 @@ static int32_t elem_i24(uint64_t key, uint64_t index) { return (int32_t)(splitmi
 static float weight_value(uint64_t key, uint64_t index) { return (float)elem_i24(key, index) * (1.0f / 268435456.0f); }
 static float gain_value(uint64_t key, uint64_t index) { return 1.0f + (float)elem_i24(key, index) * (1.0f / 134217728.0f); }
 
-static uint16_t f2bf(float f) { /* round to nearest even */
-    uint32_t u;
-    memcpy(&u, &f, 4);
-    if ((u & 0x7f800000u) == 0x7f800000u) return (uint16_t)(u >> 16); /* inf / nan passthrough */
-    uint32_t lsb = (u >> 16) & 1u;
-    u += 0x7fffu + lsb;
-    return (uint16_t)(u >> 16);
-}
-static float bf2f(uint16_t b) {
-    uint32_t u = (uint32_t)b << 16;
-    float f;
-    memcpy(&f, &u, 4);
-    return f;
-}
 static float rbf(float f) { return bf2f(f2bf(f)); }
 
 int ora_prompt_token(uint64_t seed, int64_t request, int pos, int vocab) {
@@ -75,29 +58,6 @@ float ora_weight(uint64_t seed, int tensor, int layer, uint64_t index) {
     if (tensor >= T_GATTN) return gain_value(key, index);
     return rbf(weight_value(key, index));
 }
-
-typedef struct {
-    uint16_t *wq, *wk, *wv, *wo, *wg, *wu, *wd; /* logical row-major per layer */
-    float *ga, *gm;
-} ora_layer;
-
-typedef struct ora_model {
-    ora_shape s;
-    uint64_t seed;
-    int round_act;
-    uint16_t* emb;
-    uint16_t* lm; /* == emb when tied */
-    float* gf;
-    ora_layer* layers;
-    float* cosv; /* [max_seq][dh/2] */
-    float* sinv;
-} ora_model;
-
-typedef struct ora_seq {
-    int len;
-    float* k; /* [L][max_seq][n_kv][dh] (values already rounded when round_act) */
-    float* v;
-} ora_seq;
 
 static uint16_t* gen_matrix(uint64_t seed, int tensor, int layer, size_t n) {
     uint16_t* m = (uint16_t*)malloc(n * sizeof(uint16_t));

@@ -260,6 +260,9 @@ struct mesh_gpu {
     int sms = 0;
     cudaStream_t stream = nullptr;   // compute
     cudaStream_t side = nullptr;     // swap / migration copies
+    cudaEvent_t timer[8] = {};       // mesh_gpu_timer_mark slots
+    bool check = false;              // MESH_GPU_CHECK: synchronous per-step validation (debug)
+    bool poison = false;             // MESH_GPU_POISON: NaN-fill newly mapped KV granules (debug)
     PhysPool pool;
     std::map<int64_t, std::unique_ptr<Instance>> insts;
     // decode / prefill scratch (sized for the largest registered shape)
@@ -397,6 +400,9 @@ void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
         acc.location.id = g->cfg.device;
         acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
         CU(d.set_access(in.va + off, gran, &acc, 1), "cuMemSetAccess");
+        // debug (MESH_GPU_POISON): recycled KV memory may hold any bit pattern; fill
+        // new granules with bf16 NaN so reads of unwritten KV cannot go unnoticed
+        if (g->poison) CK(cudaMemsetAsync(reinterpret_cast<void*>(in.va + off), 0xff, gran, g->stream));
         in.granules.push_back(h);
     }
     while (in.granules.size() > want) {
@@ -815,6 +821,8 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->st.kv_pool_bytes = g->pool.limit;
         // ring depth must be 8 or 16: a consumer warp's stages are 8 apart, so the
         // depth must be a multiple of 8 (mbarrier parity) and a power of two (masks)
+        g->check = std::getenv("MESH_GPU_CHECK") != nullptr;
+        g->poison = std::getenv("MESH_GPU_POISON") != nullptr;
         if (const char* e = std::getenv("MESH_GPU_NSTAGE")) g->nstage = std::atoi(e) >= 16 ? 16 : 8;
         if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
         if (std::getenv("MESH_GPU_WATCHDOG")) {
@@ -862,6 +870,8 @@ void mesh_gpu_close(mesh_gpu* g) {
         if (g->ring_ev[i]) cudaEventDestroy(g->ring_ev[i]);
     if (g->stream) cudaStreamDestroy(g->stream);
     if (g->side) cudaStreamDestroy(g->side);
+    for (cudaEvent_t e : g->timer)
+        if (e) cudaEventDestroy(e);
     delete g;
 }
 
@@ -995,6 +1005,53 @@ mesh_status mesh_gpu_kv_resize(mesh_gpu* g, int64_t instance_id, int64_t from_by
     });
 }
 
+// Debug (MESH_GPU_CHECK): block-table consistency and a NaN/Inf scan of a request's KV.
+std::string debug_request_state(mesh_gpu* g, Instance& in, int64_t rid) {
+    std::string m;
+    auto it = in.reqs.find(rid);
+    if (it == in.reqs.end()) return " [request not resident]";
+    const ReqState& r = it->second;
+    m += " | cap_blocks " + std::to_string(in.cap_blocks) + " live " + std::to_string(in.live_blocks) + " free " +
+         std::to_string(in.free_blocks.size()) + " blocks:";
+    std::vector<int> dev(size_t(in.bt_stride));
+    CK(cudaMemcpy(dev.data(), in.d_block_table + size_t(r.slot) * in.bt_stride, sizeof(int) * in.bt_stride,
+                  cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < r.blocks.size(); ++i) {
+        m += " " + std::to_string(r.blocks[i]);
+        if (dev[i] != r.blocks[i]) m += "(dev " + std::to_string(dev[i]) + ")";
+        if (in.h_block_table[size_t(r.slot) * in.bt_stride + i] != r.blocks[i]) m += "(mirror!)";
+        if (in.free_blocks.count(r.blocks[i])) m += "(FREE!)";
+        for (auto& [o, os] : in.reqs)
+            if (o != rid && std::find(os.blocks.begin(), os.blocks.end(), r.blocks[i]) != os.blocks.end())
+                m += "(shared with " + std::to_string(o) + ")";
+    }
+    // scan K/V of every resident position for non-finite values
+    std::vector<uint16_t> blk(size_t(in.block_bytes) / 2);
+    int bad_pos = -1, bad_layer = -1, nbad = 0;
+    for (int p = 0; p < r.ctx; ++p) {
+        if (p % KV_BLOCK_TOKENS == 0)
+            CK(cudaMemcpy(blk.data(), reinterpret_cast<uint8_t*>(in.va) + size_t(r.blocks[p / KV_BLOCK_TOKENS]) *
+                                                                           in.block_bytes,
+                          in.block_bytes, cudaMemcpyDeviceToHost));
+        for (int l = 0; l < in.s.n_layers; ++l)
+            for (int kv = 0; kv < 2; ++kv)
+                for (int h = 0; h < in.s.n_kv; ++h) {
+                    const uint16_t* row = blk.data() + kv_offset(in.s, l, kv, h, p % KV_BLOCK_TOKENS) / 2;
+                    for (int e = 0; e < in.s.dh; ++e)
+                        if ((row[e] & 0x7f80) == 0x7f80) {
+                            if (bad_pos < 0) {
+                                bad_pos = p;
+                                bad_layer = l;
+                            }
+                            ++nbad;
+                        }
+                }
+    }
+    m += " | non-finite KV values " + std::to_string(nbad);
+    if (bad_pos >= 0) m += " first at pos " + std::to_string(bad_pos) + " layer " + std::to_string(bad_layer);
+    return m;
+}
+
 mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan* plan, int64_t* ticket) {
     if (!g || !plan || !ticket) return MESH_ERR_ARG;
     return guarded(g, [&] {
@@ -1029,6 +1086,27 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
         CK(cudaEventRecord(t.end, g->stream));
         CK(cudaEventRecord(g->ring_ev[t.ring], g->stream));
         g->st.steps++;
+        if (g->check) {  // debug (MESH_GPU_CHECK=1): validate every step synchronously
+            CK(cudaStreamSynchronize(g->stream));
+            const int n = t.prefill ? 1 : plan->n_decode;
+            for (int i = 0; i < n; ++i) {
+                const int tok = g->h_tok[t.ring * 8 + i];
+                if (tok < 0 || tok >= in.s.vocab) {
+                    std::string msg = std::string(t.prefill ? "prefill" : "decode") + " step " +
+                                      std::to_string(g->st.steps) + " of instance " + std::to_string(instance_id) +
+                                      " (d=" + std::to_string(in.s.d) + ") produced token " + std::to_string(tok) +
+                                      " for column " + std::to_string(i) + "; requests:";
+                    for (int64_t r : t.reqs) {
+                        const ReqState& rs = in.reqs[r];
+                        msg += " " + std::to_string(r) + "@slot" + std::to_string(rs.slot) + "/ctx" +
+                               std::to_string(rs.ctx) + "/blocks" + std::to_string(rs.blocks.size());
+                    }
+                    if (t.prefill) msg += " prefill_len " + std::to_string(plan->prefill_len);
+                    msg += debug_request_state(g, in, t.reqs[t.prefill ? 0 : i]);
+                    throw MeshError(MESH_ERR_RUNTIME, msg);
+                }
+            }
+        }
         *ticket = g->next_ticket++;
         g->tickets.emplace(*ticket, std::move(t));
     });
@@ -1266,6 +1344,25 @@ mesh_status mesh_gpu_sync(mesh_gpu* g) {
     return guarded(g, [&] {
         CK(cudaStreamSynchronize(g->stream));
         CK(cudaStreamSynchronize(g->side));
+    });
+}
+
+mesh_status mesh_gpu_timer_mark(mesh_gpu* g, int32_t slot) {
+    if (!g || slot < 0 || slot >= 8) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        if (!g->timer[slot]) CK(cudaEventCreate(&g->timer[slot]));
+        CK(cudaEventRecord(g->timer[slot], g->stream));
+    });
+}
+
+mesh_status mesh_gpu_timer_elapsed(mesh_gpu* g, int32_t a, int32_t b, double* ms) {
+    if (!g || !ms || a < 0 || a >= 8 || b < 0 || b >= 8) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        if (!g->timer[a] || !g->timer[b]) throw MeshError(MESH_ERR_ARG, "timer slot not marked");
+        CK(cudaEventSynchronize(g->timer[b]));
+        float f = 0.f;
+        CK(cudaEventElapsedTime(&f, g->timer[a], g->timer[b]));
+        *ms = f;
     });
 }
 

@@ -883,6 +883,12 @@ __device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage&
     if (patch) {
         if (lane < 2 * CH)
             *reinterpret_cast<uint4*>(stage + (lane / CH) * 4096 + (cur - t0) * DH * 2 + (lane % CH) * 16) = pv;
+        // V rows past the current token hold stale memory (the unwritten tail of the
+        // block, or a previous stage): their softmax weight is 0, but 0 x NaN would
+        // still reach O through the PV mma, so clear them
+        for (int i = lane; i < (RT - 1 - (cur - t0)) * CH; i += 32)
+            *reinterpret_cast<uint4*>(stage + 4096 + (cur - t0 + 1 + i / CH) * DH * 2 + (i % CH) * 16) =
+                make_uint4(0, 0, 0, 0);
         __syncwarp();
     }
     const uint32_t kbase = smem_u32(stage), vbase = kbase + 4096;

@@ -138,6 +138,8 @@ def _load() -> C.CDLL:
         "mesh_gpu_stats_get": (C.c_int, [C.c_void_p, P(GpuStats)]),
         "mesh_gpu_sync": (C.c_int, [C.c_void_p]),
         "mesh_gpu_bench_decode": (C.c_int, [C.c_void_p, C.c_int64, P(StepPlan), C.c_int32, P(C.c_double)]),
+        "mesh_gpu_timer_mark": (C.c_int, [C.c_void_p, C.c_int32]),
+        "mesh_gpu_timer_elapsed": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, P(C.c_double)]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -272,6 +274,16 @@ class MeshGpu:
 
     def sync(self) -> None:
         self._ck(self._l.mesh_gpu_sync(self.h))
+
+    def timer_mark(self, slot: int) -> None:
+        """Records a CUDA event on the compute stream (device-side timing)."""
+        self._ck(self._l.mesh_gpu_timer_mark(self.h, slot))
+
+    def timer_elapsed(self, a: int, b: int) -> float:
+        """Device milliseconds between two marks (waits for mark b)."""
+        ms = C.c_double()
+        self._ck(self._l.mesh_gpu_timer_elapsed(self.h, a, b, C.byref(ms)))
+        return ms.value
 
     def bench_decode(self, iid: int, rids: list[int], iters: int) -> float:
         arr = (C.c_int64 * len(rids))(*rids)

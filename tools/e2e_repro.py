@@ -1,0 +1,18 @@
+"""Runs a C2 scenario through llmmesh.h with the GPU attached (debug helper)."""
+import os, sys, tempfile, time
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+os.chdir(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2507_00507_b200 import control, gpu
+cfg = sys.argv[1] if len(sys.argv) > 1 else "scenarios/c2_saturated/config.json"
+window = float(sys.argv[2]) if len(sys.argv) > 2 else None
+with control.Experiment(cfg) as exp:
+    if window:
+        exp.set("workload.window_s", window)
+    exp.out_dir(tempfile.mkdtemp(prefix="mesh_e2e_"))
+    exp.attach_gpu([0], 48 << 30, gpu.LIB_PATH)
+    t0 = time.time()
+    try:
+        exp.run()
+        print("ok", time.time() - t0, {k: exp.metric(k) for k in ["gpu.steps", "gpu.decode_tokens", "slo_compliant_rate"]})
+    except Exception as e:
+        print("FAIL after", time.time() - t0, e)

@@ -1,22 +1,27 @@
 // Prefill step for one request (L tokens starting at absolute position p0).
 //
-// GEMMs are C^T = W . X^T with the weight rows as the M operand so that the
-// decode kernel's row permutations (RoPE pairs, gate/up interleave) put both
-// members of a pair in one thread's accumulator here too; the weights are
-// streamed straight from their T16xSW128 tiled layout (each 16x64 block is a
-// contiguous, pre-swizzled 2 KB run) and the activation tile is staged with a
-// matching software swizzle, so every ldmatrix is bank-conflict free. The
-// epilogues are the decode ones applied per token: RoPE + paged KV write, the
-// residual add, silu(gate)*up. Attention is causal over the paged cache.
+// GEMMs are C^T = W . X^T on tcgen05 with the weight rows as the M operand, so
+// the decode kernel's row permutations (RoPE pairs, gate/up interleave) put both
+// members of a pair in lanes l and l^8 of one epilogue warp. The weights are
+// streamed straight from their T16xSW128 tiled layout: each 16x64 block is a
+// contiguous, pre-swizzled 2 KB run, which is exactly the canonical SW128
+// K-major UMMA operand layout, so they need no tensor map. The token rows come
+// in through a TMA tensor map with the hardware 128-byte swizzle. The epilogues
+// are the decode ones applied per token: RoPE + paged KV write, the residual
+// add, silu(gate)*up. Attention is causal over the paged cache.
 #include "prefill.cuh"
 
+#include <cuda.h>
 #include <math.h>
+#include <stdlib.h>
+
+#include <algorithm>
 
 namespace meshgpu {
 
 namespace {
 
-enum PfKind { PF_QKV = 0, PF_O = 1, PF_GU = 2, PF_DOWN = 3, PF_LM = 4 };
+enum PfKind { PF_QKV = 0, PF_O = 1, PF_GU = 2, PF_DOWN = 3 };
 
 constexpr int PF_BM = 128, PF_BN = 64, PF_BK = 64, PF_STAGES = 4, PF_THREADS = 256;
 constexpr int PF_A_STAGE = PF_BM * PF_BK * 2;  // 16 KB
@@ -33,11 +38,11 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int KIND>
-__global__ void __launch_bounds__(PF_THREADS) pf_gemm(const __grid_constant__ PrefillArgs a,
-                                                      const uint8_t* __restrict__ W, int K,
-                                                      const uint16_t* __restrict__ X, int ldx, int Lrows,
-                                                      int layer) {
+// lm_head of the last prefill position: logits[V] = W_lm . act (one token), an
+// mma.sync tile kernel (a single-column GEMM has no use for the tcgen05 path).
+__global__ void __launch_bounds__(PF_THREADS) pf_lm_gemm(const __grid_constant__ PrefillArgs a,
+                                                         const uint8_t* __restrict__ W, int K,
+                                                         const uint16_t* __restrict__ X, int ldx, int Lrows) {
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* As = smem;
     uint8_t* Bs = smem + PF_STAGES * PF_A_STAGE;
@@ -120,57 +125,242 @@ __global__ void __launch_bounds__(PF_THREADS) pf_gemm(const __grid_constant__ Pr
     }
     cp_async_wait<0>();
 
-    // ---- fused epilogue
-    const Shape& s = a.s;
+    // ---- epilogue: rms-scaled logits of the single token
     const int g = lane >> 2, t = lane & 3;
 #pragma unroll
     for (int mi = 0; mi < 2; ++mi) {
         const int row = (row_tile0 + 2 * warp_m + mi) * 16 + g;  // rows row and row + 8
-        const int tile = row >> 4;
 #pragma unroll
         for (int ni = 0; ni < 4; ++ni) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) {
                 const int l = tok0 + warp_n * 32 + ni * 8 + 2 * t + j;
                 if (l >= Lrows) continue;
-                const float v1 = acc[mi][ni][j], v2 = acc[mi][ni][2 + j];
-                if constexpr (KIND == PF_QKV) {
-                    const float r = a.rs[l];
-                    QkvRow qr = qkv_row(s, row);
-                    const int half = s.dh / 2;
-                    const int pos = a.p0 + l;
-                    float x1 = v1 * r, x2 = v2 * r, o1 = x1, o2 = x2;
-                    if (qr.section < 2) {
-                        float2 cs = a.w.rope[size_t(pos) * half + qr.dim];
-                        o1 = x1 * cs.x - x2 * cs.y;
-                        o2 = x2 * cs.x + x1 * cs.y;
-                    }
-                    if (qr.section == 0) {
-                        float* qd = a.q + (size_t(l) * s.n_heads + qr.head) * s.dh;
-                        qd[qr.dim] = o1;
-                        qd[qr.dim + half] = o2;
-                    } else {
-                        const int blk = a.bt_row[pos / KV_BLOCK_TOKENS], slot = pos % KV_BLOCK_TOKENS;
-                        uint8_t* e = a.kv_base + size_t(blk) * a.block_bytes +
-                                     kv_offset(s, layer, qr.section - 1, qr.head, slot);
-                        *reinterpret_cast<uint16_t*>(e + kv_dim_off(slot, qr.dim)) = f_to_bf16(o1);
-                        *reinterpret_cast<uint16_t*>(e + kv_dim_off(slot, qr.dim + half)) = f_to_bf16(o2);
-                    }
-                } else if constexpr (KIND == PF_GU) {
-                    const float r = a.rs[l];
-                    float gt = v1 * r, up = v2 * r;
-                    float act = gt / (1.f + __expf(-gt)) * up;
-                    a.abuf[size_t(l) * s.ff + tile * 8 + g] = f_to_bf16(act);
-                } else if constexpr (KIND == PF_O || KIND == PF_DOWN) {
-                    a.h[size_t(l) * s.d + row] += v1;
-                    a.h[size_t(l) * s.d + row + 8] += v2;
-                } else {  // PF_LM, single row
-                    const float r = a.rs[0];
-                    a.logits[row] = v1 * r;
-                    a.logits[row + 8] = v2 * r;
+                const float r = a.rs[0];
+                a.logits[row] = acc[mi][ni][j] * r;
+                a.logits[row + 8] = acc[mi][ni][2 + j] * r;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// tcgen05 GEMM: C^T[N x L] = W[N x K] . X[L x K]^T on the 5th-gen tensor cores.
+//
+// Persistent, one CTA per SM. Tiles are 128 weight rows x BN tokens, ordered
+// token-block fastest so the CTAs that share a weight tile run together and the
+// tile is fetched from HBM once. Warp roles (192 threads):
+//   warp 0  producer: per 64-deep K block, 8 bulk copies of the pre-swizzled
+//           16x64 weight blocks (A, 16 KB) + one TMA tensor load of the token
+//           rows with the 128-byte swizzle (B, BN x 128 B)
+//   warp 1  TMEM owner + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
+//   warps 2-5 epilogue: tcgen05.ld 32x32b (thread = weight row) -> the fused
+//           decode epilogues per token, double-buffered TMEM accumulators so
+//           the epilogue of tile i overlaps the main loop of tile i+1.
+// ---------------------------------------------------------------------------
+constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 192;
+constexpr int TC_A_STAGE = TC_BM * TC_BK * 2;  // 16 KB
+
+template <int BN>
+struct TcCfg {
+    static constexpr int B_STAGE = BN * TC_BK * 2;
+    static constexpr int STAGES = (196608) / (TC_A_STAGE + B_STAGE);
+    static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
+    static constexpr int SMEM = 1024 + STAGES * (TC_A_STAGE + B_STAGE) + 256;
+    static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation must be 2^k");
+};
+
+// Epilogue for one weight row `row` and 32 consecutive tokens [l0, l0 + 32).
+// Every global load of a chunk (per-token rms scale, RoPE table, block-table
+// entries, the residual) is issued before the first store: the loads are
+// independent, so they overlap instead of paying one memory round trip per
+// token behind a possibly-aliasing store. Per-token scalars are loaded once by
+// lane j and broadcast with shuffles.
+template <int KIND>
+__device__ __forceinline__ void tc_epilogue(const PrefillArgs& a, int row, int l0, const uint32_t (&v)[32],
+                                            int Lrows, int layer, int lane) {
+    const Shape& s = a.s;
+    const int nvalid = min(32, Lrows - l0);
+    if constexpr (KIND == PF_QKV || KIND == PF_GU) {
+        const float rs_l = lane < nvalid ? a.rs[l0 + lane] : 0.f;
+        if constexpr (KIND == PF_QKV) {
+            const QkvRow qr = qkv_row(s, row);
+            const bool hi = (row & 8) != 0;  // partner row (row ^ 8) sits in lane ^ 8
+            const int half = s.dh / 2;
+            const int d0 = hi ? qr.dim - half : qr.dim;
+            const int pos_l = a.p0 + l0 + lane;
+            const int blk_l = (qr.section > 0 && lane < nvalid) ? a.bt_row[pos_l / KV_BLOCK_TOKENS] : 0;
+            float2 cs[32];
+            if (qr.section < 2) {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                    cs[j] = j < nvalid ? a.w.rope[size_t(a.p0 + l0 + j) * half + d0] : make_float2(1.f, 0.f);
+            }
+            float* qd = a.q + (size_t(l0) * s.n_heads + qr.head) * s.dh + qr.dim;
+            uint8_t* kvh = a.kv_base + kv_offset(s, layer, qr.section > 0 ? qr.section - 1 : 0, qr.head, 0);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float x = __uint_as_float(v[j]);
+                const float p = __shfl_xor_sync(0xffffffffu, x, 8);
+                const float r = __shfl_sync(0xffffffffu, rs_l, j);
+                const int blk = __shfl_sync(0xffffffffu, blk_l, j);
+                if (j >= nvalid) continue;  // warp-uniform
+                const float xs = x * r, ps = p * r;
+                float o = xs;
+                if (qr.section < 2) o = hi ? (xs * cs[j].x + ps * cs[j].y) : (xs * cs[j].x - ps * cs[j].y);
+                if (qr.section == 0) {
+                    qd[size_t(j) * s.n_heads * s.dh] = o;
+                } else {
+                    const int slot = (a.p0 + l0 + j) % KV_BLOCK_TOKENS;
+                    *reinterpret_cast<uint16_t*>(kvh + size_t(blk) * a.block_bytes + size_t(slot) * s.dh * 2 +
+                                                 kv_dim_off(slot, qr.dim)) = f_to_bf16(o);
+                }
+            }
+        } else {
+            const bool hi = (row & 8) != 0;  // up rows; gate rows in the lower half
+            uint16_t* out = a.abuf + size_t(l0) * s.ff + (row >> 4) * 8 + (row & 7);
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float x = __uint_as_float(v[j]);
+                const float up = __shfl_xor_sync(0xffffffffu, x, 8);
+                const float r = __shfl_sync(0xffffffffu, rs_l, j);
+                if (j < nvalid && !hi) {
+                    const float gt = x * r, u = up * r;
+                    out[size_t(j) * s.ff] = f_to_bf16(gt / (1.f + __expf(-gt)) * u);
                 }
             }
         }
+    } else {  // PF_O / PF_DOWN: residual add, one coalesced 128-B row segment per token
+        float* hp = a.h + size_t(l0) * s.d + row;
+        float hv[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) hv[j] = j < nvalid ? hp[size_t(j) * s.d] : 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nvalid) hp[size_t(j) * s.d] = hv[j] + __uint_as_float(v[j]);
+    }
+}
+
+template <int KIND, int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    pf_gemm_tc(const __grid_constant__ PrefillArgs a, const __grid_constant__ CUtensorMap xmap,
+               const uint8_t* __restrict__ W, int N, int K, int Lrows, int layer) {
+    using C = TcCfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t* As = smem;
+    uint8_t* Bs = smem + C::STAGES * TC_A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + C::STAGES * C::B_STAGE);
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;  // [2] accumulator ready
+    uint64_t* tempty = tfull + 2;         // [2] accumulator drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nN = (Lrows + BN - 1) / BN, ntiles = (N / TC_BM) * nN, nk = K / TC_BK;
+    const size_t tile_bytes = size_t(K) * 32;  // one 16-row weight tile
+
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull + i, 1);
+            mbar_init(tempty + i, 4);
+        }
+        fence_mbar_init();
+        prefetch_tmap(&xmap);
+    }
+    if (warp == 1) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- producer
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int mt = t / nN, nt = t % nN;
+                const uint8_t* wt = W + size_t(mt) * (TC_BM / 16) * tile_bytes;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(empty + stage, phase ^ 1);
+                    mbar_arrive_expect_tx(full + stage, TC_A_STAGE + C::B_STAGE);
+                    uint8_t* ad = As + stage * TC_A_STAGE;
+#pragma unroll
+                    for (int i = 0; i < TC_BM / 16; ++i)
+                        bulk_g2s(ad + i * 2048, wt + i * tile_bytes + size_t(kb) * 2048, 2048, full + stage);
+                    tma_load_2d(Bs + stage * C::B_STAGE, &xmap, kb * TC_BK, nt * BN, full + stage);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            constexpr uint32_t idesc = umma_idesc_bf16(TC_BM, BN);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                mbar_wait(tempty + acc, aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + uint32_t(acc * BN);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(full + stage, phase);
+                    tc_fence_after();
+                    const uint64_t ad = umma_desc_sw128(smem_u32(As + stage * TC_A_STAGE));
+                    const uint64_t bd = umma_desc_sw128(smem_u32(Bs + stage * C::B_STAGE));
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k)  // +32 B along the swizzled row per K=16
+                        umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                    umma_commit(empty + stage);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit(tfull + acc);
+                if (++acc == 2) {
+                    acc = 0;
+                    aphase ^= 1;
+                }
+            }
+        }
+    } else {  // ---- epilogue warps 2..5: warp w reads TMEM lanes [32(w%4), 32(w%4)+32)
+        const int sub = warp & 3;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int mt = t / nN, nt = t % nN;
+            mbar_wait(tfull + acc, aphase);
+            tc_fence_after();
+            const int row = mt * TC_BM + sub * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                const int l0 = nt * BN + c * 32;
+                if (l0 >= Lrows) break;
+                uint32_t v[32];
+                tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + uint32_t(acc * BN + c * 32), v);
+                tc_epilogue<KIND>(a, row, l0, v, Lrows, layer, lane);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(tempty + acc);
+            if (++acc == 2) {
+                acc = 0;
+                aphase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
     }
 }
 
@@ -196,108 +386,192 @@ __global__ void pf_rownorm(const float* __restrict__ h, const float* __restrict_
     if (lane == 0) rs[row] = rsqrtf(ss / float(d) + eps);
 }
 
-// Causal attention over the paged cache. Block = (16 queries, one head).
-constexpr int PA_Q = 16, PA_KC = 64;
+// Causal attention over the paged cache on the tensor cores (mma.sync
+// m16n8k16, flash-attention style). Block = 64 queries of one head, 4 warps x
+// 16 query rows. Keys stream in 64-token chunks: every 16-token KV block of a
+// (layer, k|v, kv-head) is a contiguous run whose 16-byte chunks are already
+// XOR-swizzled by (slot & 7), so the chunk is copied raw with cp.async (double
+// buffered) and read conflict-free by ldmatrix (K) / ldmatrix.trans (V).
+// S = Q.K^T, online softmax in fp32 (exp2 with the scale folded), O += P.V
+// with P re-packed from the S accumulators as the A operand.
+constexpr int PA_QT = 64, PA_KC = 64, PA_THREADS = 128;
 template <int DH>
-__global__ void __launch_bounds__(256) pf_attn(const __grid_constant__ PrefillArgs a, int layer) {
+constexpr int pa_smem() { return 2 * 2 * PA_KC * DH * 2; }  // 2 stages x (K, V)
+
+template <int DH>
+__global__ void __launch_bounds__(PA_THREADS) pf_attn(const __grid_constant__ PrefillArgs a, int layer) {
+    constexpr int ROWB = DH * 2, TILE = PA_KC * ROWB, NT = PA_KC / 8, DT = DH / 8;
+    extern __shared__ __align__(128) uint8_t sm[];
     const Shape& s = a.s;
-    __shared__ float q_s[PA_Q][DH];
-    __shared__ uint32_t k_s[PA_KC][DH / 2 + 1];
-    __shared__ uint16_t v_s[PA_KC][DH];
-    __shared__ float p_s[8][PA_KC];
+    const int nqt = (a.L + PA_QT - 1) / PA_QT;
+    const int qt = nqt - 1 - int(blockIdx.x);  // longest rows first
     const int head = blockIdx.y, kvh = head / s.gq();
-    const int i0 = blockIdx.x * PA_Q;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    for (int i = tid; i < PA_Q * DH; i += 256) {
-        int qi = i / DH, dd = i % DH;
-        int l = i0 + qi;
-        q_s[qi][dd] = l < a.L ? a.q[(size_t(l) * s.n_heads + head) * DH + dd] : 0.f;
-    }
-    const int last_q = min(i0 + PA_Q, a.L) - 1;
-    const int kmax = a.p0 + last_q;  // inclusive key position
-    constexpr int DPL = DH / 32;
-    float m_[2], l_[2], acc[2][DPL];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, t = lane & 3;
+    const int q0 = qt * PA_QT;
+    const int kmax = a.p0 + min(q0 + PA_QT, a.L) - 1;  // last key any query of the block sees
+    const int nchunks = kmax / PA_KC + 1;
+    const size_t koff = kv_offset(s, layer, 0, kvh, 0), voff = kv_offset(s, layer, 1, kvh, 0);
+    const uint8_t* blk0 = a.kv_base + size_t(a.bt_row[0]) * a.block_bytes;  // mapped; zero-fill source
+
+    auto load_chunk = [&](int c, int stage) {
+        const uint32_t ks = smem_u32(sm + stage * 2 * TILE), vs = ks + TILE;
 #pragma unroll
-    for (int qq = 0; qq < 2; ++qq) {
-        m_[qq] = -INFINITY;
-        l_[qq] = 0.f;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e) acc[qq][e] = 0.f;
-    }
-    const float scale = rsqrtf(float(DH));
-    for (int k0 = 0; k0 <= kmax; k0 += PA_KC) {
-        __syncthreads();
-        // stage K (padded u32 rows) and V
-        for (int i = tid; i < PA_KC * (DH / 8); i += 256) {
-            int kr = i / (DH / 8), c8 = i % (DH / 8);
-            int pos = k0 + kr;
-            uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
-            if (pos <= kmax) {
-                const int blk = a.bt_row[pos / KV_BLOCK_TOKENS], slot = pos % KV_BLOCK_TOKENS;
-                const uint8_t* base = a.kv_base + size_t(blk) * a.block_bytes;
-                const uint32_t sw = kv_dim_off(slot, c8 * 8);  // swizzled 16-byte chunk
-                kv = *reinterpret_cast<const uint4*>(base + kv_offset(s, layer, 0, kvh, slot) + sw);
-                vv = *reinterpret_cast<const uint4*>(base + kv_offset(s, layer, 1, kvh, slot) + sw);
-            }
-            k_s[kr][c8 * 4 + 0] = kv.x;
-            k_s[kr][c8 * 4 + 1] = kv.y;
-            k_s[kr][c8 * 4 + 2] = kv.z;
-            k_s[kr][c8 * 4 + 3] = kv.w;
-            *reinterpret_cast<uint4*>(&v_s[kr][c8 * 8]) = vv;
+        for (int i = threadIdx.x; i < TILE / 16; i += PA_THREADS) {
+            const int r = i / (ROWB / 16), cc = i % (ROWB / 16);
+            const int pos = c * PA_KC + r;
+            const bool ok = pos <= kmax;  // rows past the last key are zero-filled (no stale NaN)
+            const uint8_t* base =
+                ok ? a.kv_base + size_t(a.bt_row[pos / KV_BLOCK_TOKENS]) * a.block_bytes +
+                         size_t(pos % KV_BLOCK_TOKENS) * ROWB + cc * 16
+                   : blk0;
+            cp_async16(ks + r * ROWB + cc * 16, ok ? base + koff : blk0, ok ? 16 : 0);
+            cp_async16(vs + r * ROWB + cc * 16, ok ? base + voff : blk0, ok ? 16 : 0);
         }
+    };
+
+    // Q fragments (bf16) for this warp's 16 rows, straight from the fp32 q buffer
+    const int r0 = q0 + warp * 16 + g, r1 = r0 + 8;
+    uint32_t qa[DH / 16][4];
+    {
+        const float* qp0 = a.q + (size_t(r0) * s.n_heads + head) * DH;
+        const float* qp1 = a.q + (size_t(r1) * s.n_heads + head) * DH;
+        const bool v0 = r0 < a.L, v1 = r1 < a.L;
+#pragma unroll
+        for (int kc = 0; kc < DH / 16; ++kc) {
+            const int c0 = kc * 16 + 2 * t;
+            float2 x00 = v0 ? *reinterpret_cast<const float2*>(qp0 + c0) : make_float2(0.f, 0.f);
+            float2 x10 = v1 ? *reinterpret_cast<const float2*>(qp1 + c0) : make_float2(0.f, 0.f);
+            float2 x01 = v0 ? *reinterpret_cast<const float2*>(qp0 + c0 + 8) : make_float2(0.f, 0.f);
+            float2 x11 = v1 ? *reinterpret_cast<const float2*>(qp1 + c0 + 8) : make_float2(0.f, 0.f);
+            qa[kc][0] = pack_bf16x2(x00.x, x00.y);
+            qa[kc][1] = pack_bf16x2(x10.x, x10.y);
+            qa[kc][2] = pack_bf16x2(x01.x, x01.y);
+            qa[kc][3] = pack_bf16x2(x11.x, x11.y);
+        }
+    }
+    const int qpos0 = a.p0 + r0, qpos1 = a.p0 + r1;
+    const int warp_last = a.p0 + q0 + warp * 16 + 15;
+    const float sl2 = rsqrtf(float(DH)) * 1.4426950408889634f;
+
+    float o[DT][4];
+#pragma unroll
+    for (int i = 0; i < DT; ++i) o[i][0] = o[i][1] = o[i][2] = o[i][3] = 0.f;
+    float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+
+    load_chunk(0, 0);
+    cp_async_commit();
+    for (int c = 0; c < nchunks; ++c) {
+        if (c + 1 < nchunks) load_chunk(c + 1, (c + 1) & 1);
+        cp_async_commit();
+        cp_async_wait<1>();
         __syncthreads();
+        const int kbase = c * PA_KC;
+        if (kbase <= warp_last) {  // warp-uniform: some key of the chunk is visible to some row
+            const uint32_t ks = smem_u32(sm + (c & 1) * 2 * TILE), vs = ks + TILE;
+            float sc[NT][4];
 #pragma unroll
-        for (int qq = 0; qq < 2; ++qq) {
-            const int qi = warp * 2 + qq;
-            const int l = i0 + qi;
-            if (l >= a.L) continue;
-            const int qpos = a.p0 + l;
-            float sc[2];
+            for (int i = 0; i < NT; ++i) sc[i][0] = sc[i][1] = sc[i][2] = sc[i][3] = 0.f;
 #pragma unroll
-            for (int h2 = 0; h2 < 2; ++h2) {
-                int kr = lane + 32 * h2;
-                float d = 0.f;
-#pragma unroll 8
-                for (int c2 = 0; c2 < DH / 2; ++c2) {
-                    uint32_t kk = k_s[kr][c2];
-                    d += q_s[qi][2 * c2] * bf16_lo(kk) + q_s[qi][2 * c2 + 1] * bf16_hi(kk);
+            for (int kc = 0; kc < DH / 16; ++kc) {
+#pragma unroll
+                for (int np = 0; np < NT / 2; ++np) {
+                    const int r = np * 16 + (lane & 7) + ((lane >> 4) << 3);
+                    const int ch = kc * 2 + ((lane >> 3) & 1);
+                    uint32_t b0, b1, b2, b3;
+                    ldmatrix_x4(ks + r * ROWB + ((ch ^ (r & 7)) << 4), b0, b1, b2, b3);
+                    mma_bf16_16816(sc[2 * np], qa[kc][0], qa[kc][1], qa[kc][2], qa[kc][3], b0, b1);
+                    mma_bf16_16816(sc[2 * np + 1], qa[kc][0], qa[kc][1], qa[kc][2], qa[kc][3], b2, b3);
                 }
-                sc[h2] = (k0 + kr <= qpos) ? d * scale : -INFINITY;
             }
-            float mx = fmaxf(sc[0], sc[1]);
+            // causal mask + scale (log2 domain), row maxima over the quad
+            float mx0 = -INFINITY, mx1 = -INFINITY;
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-            float mnew = fmaxf(m_[qq], mx);
-            if (mnew == -INFINITY) continue;  // no visible key in this chunk yet
-            float corr = __expf(m_[qq] - mnew);
-            float p0v = __expf(sc[0] - mnew), p1v = __expf(sc[1] - mnew);
-            float ps = p0v + p1v;
+            for (int nt = 0; nt < NT; ++nt) {
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-            l_[qq] = l_[qq] * corr + ps;
-            m_[qq] = mnew;
-            p_s[warp][lane] = p0v;
-            p_s[warp][lane + 32] = p1v;
-            __syncwarp();
-#pragma unroll
-            for (int e = 0; e < DPL; ++e) acc[qq][e] *= corr;
-            int nk = min(PA_KC, qpos - k0 + 1);
-            for (int j = 0; j < nk; ++j) {
-                float pj = p_s[warp][j];
-#pragma unroll
-                for (int e = 0; e < DPL; ++e) acc[qq][e] += pj * bf16_to_f(v_s[j][lane * DPL + e]);
+                for (int e = 0; e < 4; ++e) {
+                    const int key = kbase + nt * 8 + 2 * t + (e & 1);
+                    const int qp = e < 2 ? qpos0 : qpos1;
+                    const float v = key <= qp ? sc[nt][e] * sl2 : -INFINITY;
+                    sc[nt][e] = v;
+                    if (e < 2) mx0 = fmaxf(mx0, v); else mx1 = fmaxf(mx1, v);
+                }
             }
-            __syncwarp();
+#pragma unroll
+            for (int off = 1; off < 4; off <<= 1) {
+                mx0 = fmaxf(mx0, __shfl_xor_sync(0xffffffffu, mx0, off));
+                mx1 = fmaxf(mx1, __shfl_xor_sync(0xffffffffu, mx1, off));
+            }
+            const float mn0 = fmaxf(m0, mx0), mn1 = fmaxf(m1, mx1);
+            // a row with nothing visible yet keeps m = -inf: use 0 as the reference so exp2 gives 0
+            const float b0r = mn0 == -INFINITY ? 0.f : mn0, b1r = mn1 == -INFINITY ? 0.f : mn1;
+            const float cr0 = exp2f(m0 - b0r), cr1 = exp2f(m1 - b1r);
+            m0 = mn0;
+            m1 = mn1;
+            l0 *= cr0;
+            l1 *= cr1;
+#pragma unroll
+            for (int i = 0; i < DT; ++i) {
+                o[i][0] *= cr0;
+                o[i][1] *= cr0;
+                o[i][2] *= cr1;
+                o[i][3] *= cr1;
+            }
+#pragma unroll
+            for (int nt = 0; nt < NT; ++nt) {
+                sc[nt][0] = exp2f(sc[nt][0] - b0r);
+                sc[nt][1] = exp2f(sc[nt][1] - b0r);
+                sc[nt][2] = exp2f(sc[nt][2] - b1r);
+                sc[nt][3] = exp2f(sc[nt][3] - b1r);
+                l0 += sc[nt][0] + sc[nt][1];
+                l1 += sc[nt][2] + sc[nt][3];
+            }
+            // O += P.V
+#pragma unroll
+            for (int kk = 0; kk < PA_KC / 16; ++kk) {
+                const uint32_t p0 = pack_bf16x2(sc[2 * kk][0], sc[2 * kk][1]);
+                const uint32_t p1 = pack_bf16x2(sc[2 * kk][2], sc[2 * kk][3]);
+                const uint32_t p2 = pack_bf16x2(sc[2 * kk + 1][0], sc[2 * kk + 1][1]);
+                const uint32_t p3 = pack_bf16x2(sc[2 * kk + 1][2], sc[2 * kk + 1][3]);
+                const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+#pragma unroll
+                for (int dp = 0; dp < DT / 2; ++dp) {
+                    const int ch = dp * 2 + (lane >> 4);
+                    uint32_t v0, v1, v2, v3;
+                    ldmatrix_x4_trans(vs + key * ROWB + ((ch ^ (key & 7)) << 4), v0, v1, v2, v3);
+                    mma_bf16_16816(o[2 * dp], p0, p1, p2, p3, v0, v1);
+                    mma_bf16_16816(o[2 * dp + 1], p0, p1, p2, p3, v2, v3);
+                }
+            }
         }
+        __syncthreads();  // the stage is refilled next iteration
     }
 #pragma unroll
-    for (int qq = 0; qq < 2; ++qq) {
-        const int l = i0 + warp * 2 + qq;
-        if (l >= a.L) continue;
-#pragma unroll
-        for (int e = 0; e < DPL; ++e)
-            a.attn[size_t(l) * s.d + size_t(head) * DH + lane * DPL + e] = f_to_bf16(acc[qq][e] / l_[qq]);
+    for (int off = 1; off < 4; off <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, off);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, off);
     }
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+    for (int dt = 0; dt < DT; ++dt) {
+        const int col = head * DH + dt * 8 + 2 * t;
+        if (r0 < a.L)
+            *reinterpret_cast<uint32_t*>(a.attn + size_t(r0) * s.d + col) = pack_bf16x2(o[dt][0] * i0, o[dt][1] * i0);
+        if (r1 < a.L)
+            *reinterpret_cast<uint32_t*>(a.attn + size_t(r1) * s.d + col) = pack_bf16x2(o[dt][2] * i1, o[dt][3] * i1);
+    }
+}
+
+template <int DH>
+cudaError_t attn_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
+    static bool cfg = false;
+    if (!cfg) {
+        cudaError_t e = cudaFuncSetAttribute(pf_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, pa_smem<DH>());
+        if (e != cudaSuccess) return e;
+        cfg = true;
+    }
+    dim3 grid((a.L + PA_QT - 1) / PA_QT, a.s.n_heads);
+    pf_attn<DH><<<grid, PA_THREADS, pa_smem<DH>(), st>>>(a, layer);
+    return cudaGetLastError();
 }
 
 __global__ void pf_argmax(const __grid_constant__ PrefillArgs a) {
@@ -339,18 +613,105 @@ __global__ void pf_argmax(const __grid_constant__ PrefillArgs a) {
     }
 }
 
-template <int KIND>
-cudaError_t gemm(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows,
-                 int layer, cudaStream_t st) {
+// Single-token lm_head (the last position only): the mma.sync tile kernel.
+cudaError_t lm_gemm(const PrefillArgs& a, cudaStream_t st) {
     static bool cfg = false;
     if (!cfg) {
-        cudaError_t e = cudaFuncSetAttribute(pf_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
+        cudaError_t e = cudaFuncSetAttribute(pf_lm_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
         if (e != cudaSuccess) return e;
         cfg = true;
     }
-    dim3 grid(N / PF_BM, (rows + PF_BN - 1) / PF_BN);
-    pf_gemm<KIND><<<grid, PF_THREADS, PF_SMEM, st>>>(a, W, K, X, ldx, rows, layer);
+    pf_lm_gemm<<<dim3(a.s.vocab / PF_BM, 1), PF_THREADS, PF_SMEM, st>>>(a, a.w.lm, a.s.d, a.act, a.s.d, 1);
     return cudaGetLastError();
+}
+
+// ---- host side of the tcgen05 GEMM
+using EncodeTiledFn = decltype(&cuTensorMapEncodeTiled);
+EncodeTiledFn encode_tiled() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            p = nullptr;
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// Token rows X[rows][ld] bf16, box = 64 columns (128 B, swizzled) x BN rows;
+// rows past the end are zero-filled by the TMA unit.
+bool make_xmap(CUtensorMap* m, const uint16_t* X, int K, int ld, int rows, int BN) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {cuuint64_t(K), cuuint64_t(rows)};
+    cuuint64_t strides[1] = {cuuint64_t(ld) * 2};
+    cuuint32_t box[2] = {cuuint32_t(TC_BK), cuuint32_t(BN)};
+    cuuint32_t es[2] = {1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t*>(X), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int num_sms() {
+    static int n = [] {
+        int dev = 0, v = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v;
+    }();
+    return n;
+}
+
+// Token-tile width: minimise waves x per-K-block time, where a K block costs
+// max(MMA = 2*BN cycles, shared-memory operand reads = 128 + BN cycles).
+// MESH_PREFILL_BN=64|128|256 pins the width (parity tests cover every variant).
+int pick_bn(int N, int rows) {
+    if (const char* f = getenv("MESH_PREFILL_BN")) {
+        const int v = atoi(f);
+        if (v == 64 || v == 128 || v == 256) return v;
+    }
+    const int cand[3] = {256, 128, 64};
+    int best = 256;
+    long long best_cost = -1;
+    for (int bn : cand) {
+        long long tiles = (long long)(N / TC_BM) * ((rows + bn - 1) / bn);
+        long long waves = (tiles + num_sms() - 1) / num_sms();
+        long long cost = waves * std::max(2 * bn, 128 + bn);
+        if (best_cost < 0 || cost < best_cost) {
+            best_cost = cost;
+            best = bn;
+        }
+    }
+    return best;
+}
+
+template <int KIND, int BN>
+cudaError_t gemm_tc_bn(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows,
+                       int layer, cudaStream_t st) {
+    using C = TcCfg<BN>;
+    static bool cfg = false;
+    if (!cfg) {
+        cudaError_t e = cudaFuncSetAttribute(pf_gemm_tc<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        cfg = true;
+    }
+    CUtensorMap m;
+    if (!make_xmap(&m, X, K, ldx, rows, BN)) return cudaErrorInvalidValue;
+    const int tiles = (N / TC_BM) * ((rows + BN - 1) / BN);
+    pf_gemm_tc<KIND, BN><<<std::min(tiles, num_sms()), TC_THREADS, C::SMEM, st>>>(a, m, W, N, K, rows, layer);
+    return cudaGetLastError();
+}
+
+template <int KIND>
+cudaError_t gemm(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows,
+                 int layer, cudaStream_t st) {
+    if (N % TC_BM || K % TC_BK) return cudaErrorInvalidValue;
+    switch (pick_bn(N, rows)) {
+        case 256: return gemm_tc_bn<KIND, 256>(a, W, N, K, X, ldx, rows, layer, st);
+        case 128: return gemm_tc_bn<KIND, 128>(a, W, N, K, X, ldx, rows, layer, st);
+        default: return gemm_tc_bn<KIND, 64>(a, W, N, K, X, ldx, rows, layer, st);
+    }
 }
 
 }  // namespace
@@ -365,11 +726,7 @@ cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t st) {
         pf_rownorm<<<norm_blocks, 256, 0, st>>>(a.h, a.w.g_attn + size_t(layer) * s.d, a.act, a.rs, L, s.d, s.eps);
         if ((e = gemm<PF_QKV>(a, a.w.qkv + layer * a.w.qkv_layer, s.qkv_rows(), s.d, a.act, s.d, L, layer, st)))
             return e;
-        dim3 ag((L + PA_Q - 1) / PA_Q, s.n_heads);
-        if (s.dh == 64)
-            pf_attn<64><<<ag, 256, 0, st>>>(a, layer);
-        else
-            pf_attn<128><<<ag, 256, 0, st>>>(a, layer);
+        if ((e = s.dh == 64 ? attn_launch<64>(a, layer, st) : attn_launch<128>(a, layer, st))) return e;
         if ((e = gemm<PF_O>(a, a.w.o + layer * a.w.o_layer, s.d, s.n_heads * s.dh, a.attn, s.d, L, layer, st)))
             return e;
         pf_rownorm<<<norm_blocks, 256, 0, st>>>(a.h, a.w.g_mlp + size_t(layer) * s.d, a.act, a.rs, L, s.d, s.eps);
@@ -379,7 +736,7 @@ cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t st) {
     }
     // final norm of the last token -> lm_head -> greedy token
     pf_rownorm<<<1, 32, 0, st>>>(a.h + size_t(L - 1) * s.d, a.w.g_final, a.act, a.rs, 1, s.d, s.eps);
-    if ((e = gemm<PF_LM>(a, a.w.lm, s.vocab, s.d, a.act, s.d, 1, 0, st))) return e;
+    if ((e = lm_gemm(a, st))) return e;
     pf_argmax<<<1, 1024, 0, st>>>(a);
     return cudaGetLastError();
 }

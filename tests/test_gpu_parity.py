@@ -229,3 +229,29 @@ def test_1b_shape_prefill_decode(gpu):
     finally:
         model.close()
         gpu.destroy_instance(iid)
+
+
+@pytest.mark.parametrize("bn", ["64", "128", "256"])
+def test_long_prefill_every_tile_width(gpu, bn, monkeypatch):
+    """tcgen05 prefill GEMMs at every token-tile width, with several token tiles
+    and a ragged last tile (700 = 2x256 + 188), then decode over the whole KV."""
+    monkeypatch.setenv("MESH_PREFILL_BN", bn)
+    shape = SHAPES["tiny128"]
+    iid = 800 + int(bn)
+    gpu.create_instance(iid, shape, seed=21)
+    gpu.kv_resize(iid, 0, 1024 * shape.kv_bytes_per_token)
+    model = ora.Oracle(shape, 21)
+    try:
+        rid, n = 11, 700
+        toks, lg = gpu.step(iid, prefill=rid, prefill_len=n, vocab=shape.vocab, with_logits=True)
+        seq, ol = _oracle_prefill(model, rid, n)
+        _check(lg[0], toks[0], ol, f"BN={bn} prefill {n}")
+        last = toks[0]
+        for step in range(3):
+            toks, lg = gpu.step(iid, decode=[rid], vocab=shape.vocab, with_logits=True)
+            _, ol = seq.feed(last)
+            _check(lg[0], toks[0], ol, f"BN={bn} decode {step}")
+            last = toks[0]
+    finally:
+        model.close()
+        gpu.destroy_instance(iid)

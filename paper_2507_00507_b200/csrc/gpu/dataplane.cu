@@ -732,7 +732,7 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     a.h = g->p_h;
     a.act = g->p_act;
     a.rs = g->p_rs;
-    a.q = g->p_q;
+    a.q = reinterpret_cast<uint16_t*>(g->p_q);  // bf16 view of the fp32-sized buffer
     a.attn = g->p_attn;
     a.abuf = g->p_abuf;
     a.logits = g->p_logits;

@@ -184,36 +184,51 @@ __device__ __forceinline__ void tc_epilogue(const PrefillArgs& a, int row, int l
     if constexpr (KIND == PF_QKV || KIND == PF_GU) {
         const float rs_l = lane < nvalid ? a.rs[l0 + lane] : 0.f;
         if constexpr (KIND == PF_QKV) {
+            // a 128-row tile lies inside one section (section sizes are multiples of 128 rows)
             const QkvRow qr = qkv_row(s, row);
             const bool hi = (row & 8) != 0;  // partner row (row ^ 8) sits in lane ^ 8
             const int half = s.dh / 2;
             const int d0 = hi ? qr.dim - half : qr.dim;
-            const int pos_l = a.p0 + l0 + lane;
-            const int blk_l = (qr.section > 0 && lane < nvalid) ? a.bt_row[pos_l / KV_BLOCK_TOKENS] : 0;
-            float2 cs[32];
-            if (qr.section < 2) {
+            const int p0 = a.p0 + l0;
+            if (qr.section == 0) {  // q: RoPE, bf16 [l][head][dh]
+                float2 cs[32];
 #pragma unroll
                 for (int j = 0; j < 32; ++j)
-                    cs[j] = j < nvalid ? a.w.rope[size_t(a.p0 + l0 + j) * half + d0] : make_float2(1.f, 0.f);
-            }
-            float* qd = a.q + (size_t(l0) * s.n_heads + qr.head) * s.dh + qr.dim;
-            uint8_t* kvh = a.kv_base + kv_offset(s, layer, qr.section > 0 ? qr.section - 1 : 0, qr.head, 0);
+                    cs[j] = j < nvalid ? a.w.rope[size_t(p0 + j) * half + d0] : make_float2(1.f, 0.f);
+                uint16_t* qd = a.q + (size_t(l0) * s.n_heads + qr.head) * s.dh + qr.dim;
+                const size_t qstride = size_t(s.n_heads) * s.dh;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float x = __uint_as_float(v[j]);
-                const float p = __shfl_xor_sync(0xffffffffu, x, 8);
-                const float r = __shfl_sync(0xffffffffu, rs_l, j);
-                const int blk = __shfl_sync(0xffffffffu, blk_l, j);
-                if (j >= nvalid) continue;  // warp-uniform
-                const float xs = x * r, ps = p * r;
-                float o = xs;
-                if (qr.section < 2) o = hi ? (xs * cs[j].x + ps * cs[j].y) : (xs * cs[j].x - ps * cs[j].y);
-                if (qr.section == 0) {
-                    qd[size_t(j) * s.n_heads * s.dh] = o;
-                } else {
-                    const int slot = (a.p0 + l0 + j) % KV_BLOCK_TOKENS;
-                    *reinterpret_cast<uint16_t*>(kvh + size_t(blk) * a.block_bytes + size_t(slot) * s.dh * 2 +
-                                                 kv_dim_off(slot, qr.dim)) = f_to_bf16(o);
+                for (int j = 0; j < 32; ++j) {
+                    const float r = __shfl_sync(0xffffffffu, rs_l, j);
+                    const float xs = __uint_as_float(v[j]) * r;
+                    const float ps = __shfl_xor_sync(0xffffffffu, xs, 8);
+                    const float o = hi ? (xs * cs[j].x + ps * cs[j].y) : (xs * cs[j].x - ps * cs[j].y);
+                    if (j < nvalid) qd[j * qstride] = f_to_bf16(o);
+                }
+            } else {  // k (RoPE) / v: bf16 into the paged cache
+                const bool rope = qr.section == 1;
+                float2 cs[32];
+                if (rope) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        cs[j] = j < nvalid ? a.w.rope[size_t(p0 + j) * half + d0] : make_float2(1.f, 0.f);
+                }
+                // lane j: byte offset of token l0 + j's row (block base + slot row) in the head's run
+                const int pos_l = p0 + lane;
+                const long long off_l = lane < nvalid ? (long long)a.bt_row[pos_l / KV_BLOCK_TOKENS] * a.block_bytes +
+                                                            (pos_l % KV_BLOCK_TOKENS) * s.dh * 2
+                                                      : 0;
+                uint8_t* kvh = a.kv_base + kv_offset(s, layer, qr.section - 1, qr.head, 0);
+#pragma unroll
+                for (int j = 0; j < 32; ++j) {
+                    const float r = __shfl_sync(0xffffffffu, rs_l, j);
+                    const float xs = __uint_as_float(v[j]) * r;
+                    const float ps = __shfl_xor_sync(0xffffffffu, xs, 8);
+                    const long long off = __shfl_sync(0xffffffffu, off_l, j);
+                    float o = xs;
+                    if (rope) o = hi ? (xs * cs[j].x + ps * cs[j].y) : (xs * cs[j].x - ps * cs[j].y);
+                    if (j < nvalid)
+                        *reinterpret_cast<uint16_t*>(kvh + off + kv_dim_off(p0 + j, qr.dim)) = f_to_bf16(o);
                 }
             }
         } else {
@@ -241,11 +256,13 @@ __device__ __forceinline__ void tc_epilogue(const PrefillArgs& a, int row, int l
     }
 }
 
-template <int KIND, int BN>
+template <int KIND, int BN, int CS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
-    pf_gemm_tc(const __grid_constant__ PrefillArgs a, const __grid_constant__ CUtensorMap xmap,
-               const uint8_t* __restrict__ W, int N, int K, int Lrows, int layer) {
+    pf_gemm_tc(const __grid_constant__ PrefillArgs a, const __grid_constant__ CUtensorMap wmap,
+               const __grid_constant__ CUtensorMap xmap, int N, int K, int Lrows, int layer) {
     using C = TcCfg<BN>;
+    constexpr int B_PART = C::B_STAGE / CS;      // token rows this CTA fetches for the whole cluster
+    constexpr uint16_t MASK = (1u << CS) - 1u;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint8_t* As = smem;
@@ -257,24 +274,26 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nN = (Lrows + BN - 1) / BN, ntiles = (N / TC_BM) * nN, nk = K / TC_BK;
-    const size_t tile_bytes = size_t(K) * 32;  // one 16-row weight tile
-
+    const int rank = CS > 1 ? int(cluster_ctarank()) : 0;
+    const int cluster = blockIdx.x / CS, nclusters = gridDim.x / CS;
+    // a cluster owns CS consecutive weight tiles and one token tile
+    const int nN = (Lrows + BN - 1) / BN, ntiles = (N / TC_BM / CS) * nN, nk = K / TC_BK;
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(full + s, 1);
-            mbar_init(empty + s, 1);
+            mbar_init(empty + s, CS);  // a B stage is free once every CTA of the cluster consumed it
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(tfull + i, 1);
             mbar_init(tempty + i, 4);
         }
         fence_mbar_init();
+        prefetch_tmap(&wmap);
         prefetch_tmap(&xmap);
     }
     if (warp == 1) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CS > 1) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -282,17 +301,19 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         if (lane == 0) {  // ---- producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int mt = t / nN, nt = t % nN;
-                const uint8_t* wt = W + size_t(mt) * (TC_BM / 16) * tile_bytes;
+            for (int t = cluster; t < ntiles; t += nclusters) {
+                const int mt = (t / nN) * CS + rank, nt = t % nN;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1);
                     mbar_arrive_expect_tx(full + stage, TC_A_STAGE + C::B_STAGE);
-                    uint8_t* ad = As + stage * TC_A_STAGE;
-#pragma unroll
-                    for (int i = 0; i < TC_BM / 16; ++i)
-                        bulk_g2s(ad + i * 2048, wt + i * tile_bytes + size_t(kb) * 2048, 2048, full + stage);
-                    tma_load_2d(Bs + stage * C::B_STAGE, &xmap, kb * TC_BK, nt * BN, full + stage);
+                    // eight pre-swizzled 16x64 blocks, one TMA instruction
+                    tma_load_4d(As + stage * TC_A_STAGE, &wmap, 0, 0, kb, mt * (TC_BM / 16), full + stage);
+                    uint8_t* bd = Bs + stage * C::B_STAGE + rank * B_PART;
+                    const int row0 = nt * BN + rank * (BN / CS);
+                    if constexpr (CS > 1)
+                        tma_load_2d_mc(bd, &xmap, kb * TC_BK, row0, full + stage, MASK);
+                    else
+                        tma_load_2d(bd, &xmap, kb * TC_BK, row0, full + stage);
                     if (++stage == C::STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -305,7 +326,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             constexpr uint32_t idesc = umma_idesc_bf16(TC_BM, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, aphase = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int t = cluster; t < ntiles; t += nclusters) {
                 mbar_wait(tempty + acc, aphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + uint32_t(acc * BN);
@@ -317,7 +338,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < TC_BK / 16; ++k)  // +32 B along the swizzled row per K=16
                         umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
-                    umma_commit(empty + stage);
+                    if constexpr (CS > 1)
+                        umma_commit_mc(empty + stage, MASK);
+                    else
+                        umma_commit(empty + stage);
                     if (++stage == C::STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -334,8 +358,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int sub = warp & 3;
         int acc = 0;
         uint32_t aphase = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            const int mt = t / nN, nt = t % nN;
+        for (int t = cluster; t < ntiles; t += nclusters) {
+            const int mt = (t / nN) * CS + rank, nt = t % nN;
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
             const int row = mt * TC_BM + sub * 32 + lane;
@@ -357,7 +381,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
     }
     tc_fence_before();
-    __syncthreads();
+    // no CTA may leave while a peer can still multicast into its smem / barriers
+    if constexpr (CS > 1) cluster_sync_all(); else __syncthreads();
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc(tmem, C::TMEM_COLS);
@@ -433,20 +458,16 @@ __global__ void __launch_bounds__(PA_THREADS) pf_attn(const __grid_constant__ Pr
     const int r0 = q0 + warp * 16 + g, r1 = r0 + 8;
     uint32_t qa[DH / 16][4];
     {
-        const float* qp0 = a.q + (size_t(r0) * s.n_heads + head) * DH;
-        const float* qp1 = a.q + (size_t(r1) * s.n_heads + head) * DH;
+        const uint16_t* qp0 = a.q + (size_t(r0) * s.n_heads + head) * DH;
+        const uint16_t* qp1 = a.q + (size_t(r1) * s.n_heads + head) * DH;
         const bool v0 = r0 < a.L, v1 = r1 < a.L;
 #pragma unroll
         for (int kc = 0; kc < DH / 16; ++kc) {
             const int c0 = kc * 16 + 2 * t;
-            float2 x00 = v0 ? *reinterpret_cast<const float2*>(qp0 + c0) : make_float2(0.f, 0.f);
-            float2 x10 = v1 ? *reinterpret_cast<const float2*>(qp1 + c0) : make_float2(0.f, 0.f);
-            float2 x01 = v0 ? *reinterpret_cast<const float2*>(qp0 + c0 + 8) : make_float2(0.f, 0.f);
-            float2 x11 = v1 ? *reinterpret_cast<const float2*>(qp1 + c0 + 8) : make_float2(0.f, 0.f);
-            qa[kc][0] = pack_bf16x2(x00.x, x00.y);
-            qa[kc][1] = pack_bf16x2(x10.x, x10.y);
-            qa[kc][2] = pack_bf16x2(x01.x, x01.y);
-            qa[kc][3] = pack_bf16x2(x11.x, x11.y);
+            qa[kc][0] = v0 ? *reinterpret_cast<const uint32_t*>(qp0 + c0) : 0u;
+            qa[kc][1] = v1 ? *reinterpret_cast<const uint32_t*>(qp1 + c0) : 0u;
+            qa[kc][2] = v0 ? *reinterpret_cast<const uint32_t*>(qp0 + c0 + 8) : 0u;
+            qa[kc][3] = v1 ? *reinterpret_cast<const uint32_t*>(qp1 + c0 + 8) : 0u;
         }
     }
     const int qpos0 = a.p0 + r0, qpos1 = a.p0 + r1;
@@ -653,6 +674,21 @@ bool make_xmap(CUtensorMap* m, const uint16_t* X, int K, int ld, int rows, int B
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Tiled weights [N][K] (T16 x SW128) as a 4-D tensor {64 cols, 16 rows, K/64
+// blocks, N/16 tiles}; the box {64, 16, 1, 8} is one 128-row x 64-column
+// A stage, copied verbatim (the bytes are already in the SW128 UMMA layout).
+bool make_wmap(CUtensorMap* m, const uint8_t* W, int N, int K) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {64, 16, cuuint64_t(K / 64), cuuint64_t(N / 16)};
+    cuuint64_t strides[3] = {128, 2048, cuuint64_t(K) * 32};
+    cuuint32_t box[4] = {64, 16, 1, TC_BM / 16};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint8_t*>(W), dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 int num_sms() {
     static int n = [] {
         int dev = 0, v = 148;
@@ -686,21 +722,56 @@ int pick_bn(int N, int rows) {
     return best;
 }
 
+template <int KIND, int BN, int CS>
+cudaError_t gemm_tc_launch(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx,
+                           int rows, int layer, cudaStream_t st) {
+    using C = TcCfg<BN>;
+    static int max_clusters = 0;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (!max_clusters) {
+        cudaError_t e = cudaFuncSetAttribute(pf_gemm_tc<KIND, BN, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             C::SMEM);
+        if (e != cudaSuccess) return e;
+        cfg.gridDim = dim3(CS * (num_sms() / CS));
+        e = cudaOccupancyMaxActiveClusters(&max_clusters, pf_gemm_tc<KIND, BN, CS>, &cfg);
+        if (e != cudaSuccess) return e;
+        if (max_clusters < 1) return cudaErrorInvalidConfiguration;
+    }
+    CUtensorMap wm, xm;
+    if (!make_wmap(&wm, W, N, K) || !make_xmap(&xm, X, K, ldx, rows, BN / CS)) return cudaErrorInvalidValue;
+    const int ctiles = (N / TC_BM / CS) * ((rows + BN - 1) / BN);
+    cfg.gridDim = dim3(CS * std::min(ctiles, max_clusters));
+    return cudaLaunchKernelEx(&cfg, pf_gemm_tc<KIND, BN, CS>, a, wm, xm, N, K, rows, layer);
+}
+
+// Cluster size along the weight rows: the CTAs of a cluster share (multicast)
+// the token tile, cutting the L2->SM operand traffic from 48 KB to 16 + 32/CS
+// KB per 64-deep K block; the L2 read bandwidth, not the tensor pipe, bounds
+// the single-CTA 128x256 tile.
 template <int KIND, int BN>
 cudaError_t gemm_tc_bn(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows,
                        int layer, cudaStream_t st) {
-    using C = TcCfg<BN>;
-    static bool cfg = false;
-    if (!cfg) {
-        cudaError_t e = cudaFuncSetAttribute(pf_gemm_tc<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-        if (e != cudaSuccess) return e;
-        cfg = true;
+    const int nM = N / TC_BM;
+    int cs = 1;
+    if (const char* f = getenv("MESH_PREFILL_CLUSTER")) {
+        const int v = atoi(f);
+        if ((v == 1 || v == 2 || v == 4) && nM % v == 0) cs = v;
     }
-    CUtensorMap m;
-    if (!make_xmap(&m, X, K, ldx, rows, BN)) return cudaErrorInvalidValue;
-    const int tiles = (N / TC_BM) * ((rows + BN - 1) / BN);
-    pf_gemm_tc<KIND, BN><<<std::min(tiles, num_sms()), TC_THREADS, C::SMEM, st>>>(a, m, W, N, K, rows, layer);
-    return cudaGetLastError();
+    switch (cs) {
+        case 4: return gemm_tc_launch<KIND, BN, 4>(a, W, N, K, X, ldx, rows, layer, st);
+        case 2: return gemm_tc_launch<KIND, BN, 2>(a, W, N, K, X, ldx, rows, layer, st);
+        default: return gemm_tc_launch<KIND, BN, 1>(a, W, N, K, X, ldx, rows, layer, st);
+    }
 }
 
 template <int KIND>
@@ -719,6 +790,8 @@ cudaError_t gemm(const PrefillArgs& a, const uint8_t* W, int N, int K, const uin
 cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t st) {
     const Shape& s = a.s;
     const int L = a.L;
+    // the QKV epilogue treats every 128-row weight tile as lying inside one of q / k / v
+    if ((s.n_heads * s.dh) % TC_BM || (s.n_kv * s.dh) % TC_BM) return cudaErrorInvalidValue;
     pf_embed<<<L, 256, 0, st>>>(a);
     const int norm_blocks = (L + 7) / 8;
     cudaError_t e;

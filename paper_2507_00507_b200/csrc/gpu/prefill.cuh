@@ -20,7 +20,7 @@ struct PrefillArgs {
     float* h;           // [L][d]
     uint16_t* act;      // [L][d]
     float* rs;          // [L]
-    float* q;           // [L][H][dh]
+    uint16_t* q;        // [L][H][dh] bf16 (RoPE applied; the attention MMA operand)
     uint16_t* attn;     // [L][d]
     uint16_t* abuf;     // [L][ff]
     float* logits;      // [vocab] (last token)

@@ -231,13 +231,17 @@ def test_1b_shape_prefill_decode(gpu):
         gpu.destroy_instance(iid)
 
 
-@pytest.mark.parametrize("bn", ["64", "128", "256"])
-def test_long_prefill_every_tile_width(gpu, bn, monkeypatch):
-    """tcgen05 prefill GEMMs at every token-tile width, with several token tiles
-    and a ragged last tile (700 = 2x256 + 188), then decode over the whole KV."""
+@pytest.mark.parametrize("bn,cluster", [("64", ""), ("128", ""), ("256", ""), ("256", "1"), ("128", "2")])
+def test_long_prefill_every_tile_width(gpu, bn, cluster, monkeypatch):
+    """tcgen05 prefill GEMMs at every token-tile width and token-tile multicast
+    cluster size (default: 4 where the weight-tile count allows, else 2), with
+    several token tiles and a ragged last tile (700 = 2x256 + 188), then
+    decode over the whole KV."""
     monkeypatch.setenv("MESH_PREFILL_BN", bn)
+    if cluster:
+        monkeypatch.setenv("MESH_PREFILL_CLUSTER", cluster)
     shape = SHAPES["tiny128"]
-    iid = 800 + int(bn)
+    iid = 800 + int(bn) + 1000 * int(cluster or 0)
     gpu.create_instance(iid, shape, seed=21)
     gpu.kv_resize(iid, 0, 1024 * shape.kv_bytes_per_token)
     model = ora.Oracle(shape, 21)

@@ -10,9 +10,11 @@ def run(name, B=8, ctx=1024, iters=20, pf_len=512):
         g.create_instance(1, s, seed=1)
         g.kv_resize(1, 0, (B + 2) * (ctx + 64) * s.kv_bytes_per_token)
         t0 = time.time()
+        pfs = []
         for r in range(B):
             g.step(1, prefill=r, prefill_len=ctx)
-        pf = g.stats()['last_step_ms']
+            pfs.append(g.stats()['last_step_ms'])
+        pf = sorted(pfs)[len(pfs) // 2]  # median of the B prefills
         rids = list(range(B))
         ms = g.bench_decode(1, rids, iters)
         W = s.weight_bytes_streamed

@@ -190,59 +190,59 @@ __device__ __forceinline__ void tc_epilogue(const PrefillArgs& a, int row, int l
             const int half = s.dh / 2;
             const int d0 = hi ? qr.dim - half : qr.dim;
             const int p0 = a.p0 + l0;
-            if (qr.section == 0) {  // q: RoPE, bf16 [l][head][dh]
-                float2 cs[32];
+            // RoPE (cos, sin) per token; v rows rotate by (1, 0), which is exact
+            float2 cs[32];
+            if (qr.section < 2) {
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    cs[j] = j < nvalid ? a.w.rope[size_t(p0 + j) * half + d0] : make_float2(1.f, 0.f);
+                for (int j = 0; j < 32; ++j) cs[j] = a.w.rope[size_t(p0 + min(j, nvalid - 1)) * half + d0];
+            } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j) cs[j] = make_float2(1.f, 0.f);
+            }
+            float o[32];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+                const float r = __shfl_sync(0xffffffffu, rs_l, j);
+                const float xs = __uint_as_float(v[j]) * r;
+                const float ps = __shfl_xor_sync(0xffffffffu, xs, 8);
+                o[j] = hi ? (xs * cs[j].x + ps * cs[j].y) : (xs * cs[j].x - ps * cs[j].y);
+            }
+            if (qr.section == 0) {  // q: bf16 [l][head][dh]
                 uint16_t* qd = a.q + (size_t(l0) * s.n_heads + qr.head) * s.dh + qr.dim;
                 const size_t qstride = size_t(s.n_heads) * s.dh;
 #pragma unroll
-                for (int j = 0; j < 32; ++j) {
-                    const float r = __shfl_sync(0xffffffffu, rs_l, j);
-                    const float xs = __uint_as_float(v[j]) * r;
-                    const float ps = __shfl_xor_sync(0xffffffffu, xs, 8);
-                    const float o = hi ? (xs * cs[j].x + ps * cs[j].y) : (xs * cs[j].x - ps * cs[j].y);
-                    if (j < nvalid) qd[j * qstride] = f_to_bf16(o);
-                }
-            } else {  // k (RoPE) / v: bf16 into the paged cache
-                const bool rope = qr.section == 1;
-                float2 cs[32];
-                if (rope) {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        cs[j] = j < nvalid ? a.w.rope[size_t(p0 + j) * half + d0] : make_float2(1.f, 0.f);
-                }
-                // lane j: byte offset of token l0 + j's row (block base + slot row) in the head's run
-                const int pos_l = p0 + lane;
-                const long long off_l = lane < nvalid ? (long long)a.bt_row[pos_l / KV_BLOCK_TOKENS] * a.block_bytes +
-                                                            (pos_l % KV_BLOCK_TOKENS) * s.dh * 2
-                                                      : 0;
+                for (int j = 0; j < 32; ++j)
+                    if (j < nvalid) qd[j * qstride] = f_to_bf16(o[j]);
+            } else {  // k / v: bf16 into the paged cache
+                // lane j: byte offset of token l0 + j's slot row inside the head's block run
+                const int pos_l = p0 + min(lane, nvalid - 1);
+                const long long off_l = (long long)a.bt_row[pos_l / KV_BLOCK_TOKENS] * a.block_bytes +
+                                        (pos_l % KV_BLOCK_TOKENS) * s.dh * 2;
                 uint8_t* kvh = a.kv_base + kv_offset(s, layer, qr.section - 1, qr.head, 0);
 #pragma unroll
                 for (int j = 0; j < 32; ++j) {
-                    const float r = __shfl_sync(0xffffffffu, rs_l, j);
-                    const float xs = __uint_as_float(v[j]) * r;
-                    const float ps = __shfl_xor_sync(0xffffffffu, xs, 8);
                     const long long off = __shfl_sync(0xffffffffu, off_l, j);
-                    float o = xs;
-                    if (rope) o = hi ? (xs * cs[j].x + ps * cs[j].y) : (xs * cs[j].x - ps * cs[j].y);
                     if (j < nvalid)
-                        *reinterpret_cast<uint16_t*>(kvh + off + kv_dim_off(p0 + j, qr.dim)) = f_to_bf16(o);
+                        *reinterpret_cast<uint16_t*>(kvh + off + kv_dim_off(p0 + j, qr.dim)) = f_to_bf16(o[j]);
                 }
             }
         } else {
-            const bool hi = (row & 8) != 0;  // up rows; gate rows in the lower half
-            uint16_t* out = a.abuf + size_t(l0) * s.ff + (row >> 4) * 8 + (row & 7);
+            // gate rows sit in lanes 0-7 / 16-23, up rows in lanes 8-15 / 24-31. Lane
+            // pairs (l, l^8) split the chunk: the gate lane finishes tokens 0-15, the up
+            // lane tokens 16-31, so every lane stores and no lane idles.
+            const bool hi = (row & 8) != 0;
+            const int grow = (row >> 4) * 8 + (row & 7);  // output column of the pair
+            uint16_t* out = a.abuf + size_t(l0) * s.ff + grow;
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-                const float x = __uint_as_float(v[j]);
-                const float up = __shfl_xor_sync(0xffffffffu, x, 8);
-                const float r = __shfl_sync(0xffffffffu, rs_l, j);
-                if (j < nvalid && !hi) {
-                    const float gt = x * r, u = up * r;
-                    out[size_t(j) * s.ff] = f_to_bf16(gt / (1.f + __expf(-gt)) * u);
-                }
+            for (int j = 0; j < 16; ++j) {
+                const float mine = __uint_as_float(hi ? v[16 + j] : v[j]);
+                const float give = __uint_as_float(hi ? v[j] : v[16 + j]);
+                const float peer = __shfl_xor_sync(0xffffffffu, give, 8);
+                const int tok = hi ? 16 + j : j;
+                const float r = __shfl_sync(0xffffffffu, rs_l, tok);
+                const float gt = (hi ? peer : mine) * r, up = (hi ? mine : peer) * r;
+                const float act = __fdividef(gt, 1.f + __expf(-gt)) * up;
+                if (tok < nvalid) out[size_t(tok) * s.ff] = f_to_bf16(act);
             }
         }
     } else {  // PF_O / PF_DOWN: residual add, one coalesced 128-B row segment per token

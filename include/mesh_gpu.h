@@ -54,8 +54,9 @@ typedef struct mesh_model_shape {
 typedef struct mesh_gpu_cfg {
     int32_t device;         /* CUDA ordinal */
     int32_t sm_quota;       /* CTAs of the persistent decode kernel; 0 = all SMs */
-    int64_t kv_pool_bytes;  /* physical HBM the KV pool may map (VMM, 2 MiB granules) */
+    int64_t kv_pool_bytes;  /* physical HBM the KV pool may map (VMM granules) */
     uint64_t prompt_seed;   /* synthetic prompt ids: hash(seed, request, position) */
+    int64_t kv_granule_bytes; /* physical chunk per cuMemCreate/cuMemMap, multiple of 2 MiB; 0 = 32 MiB */
 } mesh_gpu_cfg;
 
 typedef struct mesh_step_plan {
@@ -78,6 +79,10 @@ typedef struct mesh_gpu_stats {
     double last_kernel_ms;        /* device time of its kernels (descriptor copy excluded) */
     int64_t kernel_launches;      /* kernels launched by steps */
     int64_t h2d_bytes, d2h_bytes; /* per-step host<->device traffic (descriptors, prompts, tokens) */
+    int64_t kv_granule_bytes;     /* physical chunk size of the KV pool */
+    int64_t vmm_calls;            /* cuMemMap / cuMemUnmap / cuMemSetAccess calls */
+    double vmm_ms;                /* host time inside them */
+    int64_t kv_reclaims;          /* lazy-shrink slack reclaims (each drains the streams once) */
 } mesh_gpu_stats;
 
 const char* mesh_gpu_version(void);
@@ -92,9 +97,11 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
 mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id);
 
 /* Physically applies a KV ScaleOp at issue time: grow maps
- * granules, shrink compacts live blocks below the new high-water mark with a
- * batched block-copy kernel and unmaps the tail. `from` must equal the
- * instance's current target. */
+ * granules (one access grant per grow), shrink compacts live blocks below the
+ * new high-water mark with a batched block-copy kernel. Shrinks release lazily:
+ * the tail granules stay mapped (no host/device sync) until another grow would
+ * exceed the pool limit, which drains the streams once and unmaps every
+ * instance's slack. `from` must equal the instance's current target. */
 mesh_status mesh_gpu_kv_resize(mesh_gpu* g, int64_t instance_id, int64_t from_bytes, int64_t to_bytes);
 
 mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan* plan, int64_t* ticket);

@@ -2,6 +2,7 @@
 
 #include <dlfcn.h>
 
+#include <chrono>
 #include <cstring>
 
 #include "../../../include/mesh_gpu.h"
@@ -36,6 +37,12 @@ struct GpuExecutor::Api {
 };
 
 namespace {
+struct HostTimer {  // adds the scope's wall time (ms) to `acc`
+    double& acc;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit HostTimer(double& a) : acc(a) {}
+    ~HostTimer() { acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+};
 uint64_t weight_seed(const std::string& model_id) {  // every instance of a model is the same replica
     uint64_t h = 1469598103934665603ULL;
     for (unsigned char ch : model_id) {
@@ -98,6 +105,8 @@ mesh_gpu* GpuExecutor::handle_for_node(NodeId node) {
 }
 
 void GpuExecutor::instance_start(const Cluster&, const Instance& inst) {
+    HostTimer ht(host_ms_create_);
+    ++instance_starts_;
     const LlamaShape& L = llama_shape_for(inst.model->size_class);
     mesh_model_shape s{L.n_layers, L.d_model, L.n_heads, L.n_kv_heads, L.d_head, L.d_ff, L.vocab, L.tied,
                        std::min(L.max_seq_len, inst.model->max_seq_len), L.rope_theta, L.rms_eps};
@@ -107,11 +116,13 @@ void GpuExecutor::instance_start(const Cluster&, const Instance& inst) {
 }
 
 void GpuExecutor::kv_issue(const Cluster&, const Instance& inst, const ScaleOp& op) {
+    HostTimer ht(host_ms_kv_);
     mesh_gpu* h = handle_for_node(inst.node_id);
     check(h, api_->kv_resize(h, inst.id, op.from_bytes, op.to_bytes), "kv_resize");
 }
 
 void GpuExecutor::iteration_start(const Cluster& c, const Node& nd, const Instance& inst, const IterationPlan& p) {
+    HostTimer ht(host_ms_step_);
     mesh_gpu* h = handle_for_node(nd.id);
     std::vector<long long>& tk = tickets_[nd.id];
     if (p.is_prefill) {
@@ -147,6 +158,7 @@ void GpuExecutor::iteration_done(const Cluster&, const Node& nd, const Iteration
 }
 
 void GpuExecutor::retire_one() {
+    HostTimer ht(host_ms_wait_);
     auto [h, t] = pending_.front();
     pending_.pop_front();
     int32_t toks[8];
@@ -180,6 +192,7 @@ void GpuExecutor::instance_unloaded(const Cluster&, InstanceId inst) {
     auto d = inst_dev_.find(inst);
     if (d == inst_dev_.end()) return;
     drain();  // retire outstanding tickets before the instance (and its tickets) go away
+    HostTimer ht(host_ms_destroy_);
     mesh_gpu* h = handles_[static_cast<std::size_t>(d->second)];
     check(h, api_->instance_destroy(h, inst), "instance_destroy");
     inst_dev_.erase(d);
@@ -191,7 +204,13 @@ std::map<std::string, double> GpuExecutor::metrics() const {
     m["gpu.decode_tokens"] = static_cast<double>(decode_tokens_);
     m["gpu.prefill_tokens"] = static_cast<double>(prefill_tokens_);
     m["gpu.device_ms"] = device_ms_;
-    double swap = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0;
+    m["gpu.instance_starts"] = static_cast<double>(instance_starts_);
+    m["gpu.host_ms.instance_create"] = host_ms_create_;
+    m["gpu.host_ms.instance_destroy"] = host_ms_destroy_;
+    m["gpu.host_ms.kv_resize"] = host_ms_kv_;
+    m["gpu.host_ms.step_issue"] = host_ms_step_;
+    m["gpu.host_ms.step_wait"] = host_ms_wait_;
+    double swap = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0, vmm_calls = 0, vmm_ms = 0, reclaims = 0;
     for (mesh_gpu* h : handles_) {
         mesh_gpu_stats st{};
         api_->stats_get(h, &st);
@@ -201,7 +220,13 @@ std::map<std::string, double> GpuExecutor::metrics() const {
         launches += static_cast<double>(st.kernel_launches);
         h2d += static_cast<double>(st.h2d_bytes);
         d2h += static_cast<double>(st.d2h_bytes);
+        vmm_calls += static_cast<double>(st.vmm_calls);
+        vmm_ms += st.vmm_ms;
+        reclaims += static_cast<double>(st.kv_reclaims);
     }
+    m["gpu.vmm_calls"] = vmm_calls;
+    m["gpu.host_ms.vmm"] = vmm_ms;
+    m["gpu.kv_reclaims"] = reclaims;
     m["gpu.swap_out_bytes"] = swap;
     m["gpu.migrate_bytes"] = mig;
     m["gpu.blocks_moved"] = moved;

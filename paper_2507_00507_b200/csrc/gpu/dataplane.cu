@@ -22,6 +22,7 @@
 #include <unistd.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -386,31 +387,76 @@ int blocks_for_target(const Instance& in, long long target) {
     return int(blocks) + DEC_MAXB;  // one partial tail block per resident request
 }
 
-void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
-    size_t gran = g->pool.gran;
-    size_t want = (bytes + gran - 1) / gran;
-    Driver& d = drv();
-    while (in.granules.size() < want) {
-        size_t off = in.granules.size() * gran;
-        if (off + gran > in.va_size) throw MeshError(MESH_ERR_NOMEM, "instance KV VA range exhausted");
-        CUmemGenericAllocationHandle h = g->pool.take();
-        CU(d.map(in.va + off, gran, 0, h, 0), "cuMemMap");
-        CUmemAccessDesc acc = {};
-        acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-        acc.location.id = g->cfg.device;
-        acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-        CU(d.set_access(in.va + off, gran, &acc, 1), "cuMemSetAccess");
-        // debug (MESH_GPU_POISON): recycled KV memory may hold any bit pattern; fill
-        // new granules with bf16 NaN so reads of unwritten KV cannot go unnoticed
-        if (g->poison) CK(cudaMemsetAsync(reinterpret_cast<void*>(in.va + off), 0xff, gran, g->stream));
-        in.granules.push_back(h);
+size_t granules_for(const mesh_gpu* g, long long bytes) {
+    return size_t((bytes + (long long)g->pool.gran - 1) / (long long)g->pool.gran);
+}
+
+// Unmaps an instance's granules from the top of its VA range down to `keep`.
+// The caller guarantees no queued work touches the tail (streams drained).
+struct VmmTimer {  // host time of VMM driver calls -> stats
+    mesh_gpu* g;
+    std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+    explicit VmmTimer(mesh_gpu* gg) : g(gg) {}
+    ~VmmTimer() {
+        g->st.vmm_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
-    while (in.granules.size() > want) {
-        size_t off = (in.granules.size() - 1) * gran;
-        CU(d.unmap(in.va + off, gran), "cuMemUnmap");
+};
+
+void unmap_tail(mesh_gpu* g, Instance& in, size_t keep) {
+    Driver& d = drv();
+    VmmTimer vt(g);
+    while (in.granules.size() > keep) {
+        size_t off = (in.granules.size() - 1) * g->pool.gran;
+        CU(d.unmap(in.va + off, g->pool.gran), "cuMemUnmap");
+        g->st.vmm_calls++;
         g->pool.give(in.granules.back());
         in.granules.pop_back();
     }
+}
+
+// Shrinks are lazy: a shrink compacts the live blocks below the new capacity
+// but leaves the tail granules mapped, so a later grow of the same instance
+// costs nothing and a shrink never stalls the host on the device. Granules go
+// back to the pool only when another grow needs them: one drain of the streams,
+// then every instance's slack above its capacity is unmapped.
+void reclaim_slack(mesh_gpu* g) {
+    g->st.kv_reclaims++;
+    CK(cudaStreamSynchronize(g->stream));
+    CK(cudaStreamSynchronize(g->side));
+    for (auto& [id, ip] : g->insts) unmap_tail(g, *ip, granules_for(g, (long long)ip->cap_blocks * ip->block_bytes));
+}
+
+// Grow-only: maps granules until `bytes` of the instance's VA range are backed.
+void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
+    const size_t gran = g->pool.gran;
+    const size_t want = granules_for(g, (long long)bytes), first = in.granules.size();
+    if (want <= first) return;
+    if (want * gran > in.va_size) throw MeshError(MESH_ERR_NOMEM, "instance KV VA range exhausted");
+    if (g->pool.mapped + (long long)((want - first) * gran) > g->pool.limit) reclaim_slack(g);
+    Driver& d = drv();
+    VmmTimer vt(g);
+    while (in.granules.size() < want) {
+        const size_t off = in.granules.size() * gran;
+        CUmemGenericAllocationHandle h = g->pool.take();
+        CUresult r = d.map(in.va + off, gran, 0, h, 0);
+        if (r != CUDA_SUCCESS) {
+            g->pool.give(h);
+            throw MeshError(MESH_ERR_RUNTIME, "cuMemMap failed: " + std::to_string(int(r)));
+        }
+        in.granules.push_back(h);
+        g->st.vmm_calls++;
+    }
+    // one access grant for the whole newly mapped range
+    CUmemAccessDesc acc = {};
+    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+    acc.location.id = g->cfg.device;
+    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    CU(d.set_access(in.va + first * gran, (want - first) * gran, &acc, 1), "cuMemSetAccess");
+    g->st.vmm_calls++;
+    // debug (MESH_GPU_POISON): recycled KV memory may hold any bit pattern; fill
+    // new granules with bf16 NaN so reads of unwritten KV cannot go unnoticed
+    if (g->poison)
+        CK(cudaMemsetAsync(reinterpret_cast<void*>(in.va + first * gran), 0xff, (want - first) * gran, g->stream));
 }
 
 void write_bt_entry(Instance& in, int slot, int idx, int block) {
@@ -458,13 +504,10 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
         g->st.blocks_moved += (long long)moves.size();
         g->st.bytes_moved += 2LL * (long long)moves.size() * in.block_bytes;
     }
-    // everything that may still touch the tail must finish before unmapping it
-    CK(cudaStreamSynchronize(g->stream));
-    CK(cudaStreamSynchronize(g->side));
+    // the tail stays mapped (lazy shrink, see reclaim_slack); queued work may still read it
     in.free_blocks = low_free;
     in.cap_blocks = new_cap;
     in.target = to;
-    map_to(g, in, size_t(new_cap) * in.block_bytes);
 }
 
 int alloc_block(mesh_gpu* g, Instance& in) {
@@ -807,7 +850,13 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         prop2.location.id = cfg->device;
         size_t gran = 0;
         CU(drv().granularity(&gran, &prop2, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED), "cuMemGetAllocationGranularity");
-        g->pool.gran = std::max<size_t>(gran, 2u << 20);
+        // large physical chunks: every cuMemMap / cuMemUnmap costs host time (and a
+        // TLB shoot-down), so fewer, larger granules make grows and releases cheap
+        const size_t want = cfg->kv_granule_bytes > 0 ? size_t(cfg->kv_granule_bytes) : size_t(32) << 20;
+        gran = std::max<size_t>(gran, 2u << 20);
+        if (want % gran) throw MeshError(MESH_ERR_ARG, "kv_granule_bytes must be a multiple of " + std::to_string(gran));
+        g->pool.gran = want;
+        g->st.kv_granule_bytes = (long long)want;
         g->pool.limit = cfg->kv_pool_bytes > 0 ? cfg->kv_pool_bytes : (long long)(prop.totalGlobalMem / 2);
         dalloc(&g->bar, 2);
         dalloc(&g->arg_val, size_t(8) * g->sms);
@@ -849,7 +898,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (auto& [id, t] : g->tickets) destroy_ticket(t);
     for (auto& [id, in] : g->insts) {
         try {
-            map_to(g, *in, 0);
+            unmap_tail(g, *in, 0);
         } catch (...) {
         }
         if (in->va) drv().addr_free(in->va, in->va_size);
@@ -975,7 +1024,7 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
         Instance& in = inst_of(g, instance_id);
         CK(cudaStreamSynchronize(g->stream));
         CK(cudaStreamSynchronize(g->side));
-        map_to(g, in, 0);
+        unmap_tail(g, in, 0);
         CU(drv().addr_free(in.va, in.va_size), "cuMemAddressFree");
         CK(cudaFree(in.wmem));
         CK(cudaFree(in.d_block_table));

@@ -184,7 +184,7 @@ __device__ __forceinline__ void tc_epilogue(const PrefillArgs& a, int row, int l
     if constexpr (KIND == PF_QKV || KIND == PF_GU) {
         const float rs_l = lane < nvalid ? a.rs[l0 + lane] : 0.f;
         if constexpr (KIND == PF_QKV) {
-            // a 128-row tile lies inside one section (section sizes are multiples of 128 rows)
+            // a warp's 32 rows lie inside one section (q / k / v sizes are multiples of 32 rows)
             const QkvRow qr = qkv_row(s, row);
             const bool hi = (row & 8) != 0;  // partner row (row ^ 8) sits in lane ^ 8
             const int half = s.dh / 2;
@@ -790,8 +790,8 @@ cudaError_t gemm(const PrefillArgs& a, const uint8_t* W, int N, int K, const uin
 cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t st) {
     const Shape& s = a.s;
     const int L = a.L;
-    // the QKV epilogue treats every 128-row weight tile as lying inside one of q / k / v
-    if ((s.n_heads * s.dh) % TC_BM || (s.n_kv * s.dh) % TC_BM) return cudaErrorInvalidValue;
+    // the QKV epilogue branches on q / k / v per warp (32 weight rows; the k/v store shuffles)
+    if ((s.n_heads * s.dh) % 32 || (s.n_kv * s.dh) % 32) return cudaErrorInvalidValue;
     pf_embed<<<L, 256, 0, st>>>(a);
     const int norm_blocks = (L + 7) / 8;
     cudaError_t e;

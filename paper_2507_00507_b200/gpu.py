@@ -33,7 +33,7 @@ class ModelShape(C.Structure):
 
 class GpuCfg(C.Structure):
     _fields_ = [("device", C.c_int32), ("sm_quota", C.c_int32), ("kv_pool_bytes", C.c_int64),
-                ("prompt_seed", C.c_uint64)]
+                ("prompt_seed", C.c_uint64), ("kv_granule_bytes", C.c_int64)]
 
 
 class StepPlan(C.Structure):
@@ -47,7 +47,9 @@ class GpuStats(C.Structure):
                 ("bytes_moved", C.c_int64), ("swap_out_bytes", C.c_int64), ("swap_in_bytes", C.c_int64),
                 ("migrate_bytes", C.c_int64), ("steps", C.c_int64), ("decode_tokens", C.c_int64),
                 ("prefill_tokens", C.c_int64), ("last_step_ms", C.c_double), ("last_kernel_ms", C.c_double),
-                ("kernel_launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64)]
+                ("kernel_launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
+                ("kv_granule_bytes", C.c_int64), ("vmm_calls", C.c_int64), ("vmm_ms", C.c_double),
+                ("kv_reclaims", C.c_int64)]
 
 
 @dataclass(frozen=True)
@@ -168,9 +170,10 @@ EXPORTED = ["mesh_gpu_version", "mesh_gpu_device_count", "mesh_gpu_open", "mesh_
 class MeshGpu:
     """One B200 (one handle of the C ABI)."""
 
-    def __init__(self, device: int = 0, sm_quota: int = 0, kv_pool_bytes: int = 0, prompt_seed: int = 1234):
+    def __init__(self, device: int = 0, sm_quota: int = 0, kv_pool_bytes: int = 0, prompt_seed: int = 1234,
+                 kv_granule_bytes: int = 0):
         self._l = lib()
-        cfg = GpuCfg(device, sm_quota, kv_pool_bytes, prompt_seed)
+        cfg = GpuCfg(device, sm_quota, kv_pool_bytes, prompt_seed, kv_granule_bytes)
         h = C.c_void_p()
         st = self._l.mesh_gpu_open(C.byref(cfg), C.byref(h))
         if st != MESH_OK:

@@ -11,7 +11,7 @@ import numpy as np
 import pytest
 
 from oracle import llama_oracle as ora
-from paper_2507_00507_b200.gpu import SHAPES, T_LM, T_WDOWN, T_WGATE, T_WK, T_WO, T_WQ, T_WUP, T_WV, MeshGpu
+from paper_2507_00507_b200.gpu import SHAPES, MeshGpuError, T_LM, T_WDOWN, T_WGATE, T_WK, T_WO, T_WQ, T_WUP, T_WV, MeshGpu
 
 pytestmark = pytest.mark.gpu
 
@@ -259,3 +259,37 @@ def test_long_prefill_every_tile_width(gpu, bn, cluster, monkeypatch):
     finally:
         model.close()
         gpu.destroy_instance(iid)
+
+
+def test_lazy_shrink_slack_reclaimed_by_other_grow():
+    """Shrink keeps the tail granules mapped (no stall); a grow of another
+    instance that needs them past the pool limit reclaims the slack, and the
+    shrunk instance's compacted KV still decodes exactly."""
+    shape = SHAPES["tiny"]
+    C = shape.kv_bytes_per_token  # 1 KiB/token: a 2 MiB granule holds 128 blocks of 16 tokens
+    gran = 2 << 20
+    with MeshGpu(0, kv_pool_bytes=4 * gran, prompt_seed=SEED_PROMPT, kv_granule_bytes=gran) as g:
+        g.capture_logits(True)
+        g.create_instance(1, shape, seed=3)
+        g.create_instance(2, shape, seed=4)
+        model = ora.Oracle(shape, 3)
+        g.kv_resize(1, 0, 3000 * C)  # 196 blocks -> 2 granules
+        toks, lg = g.step(1, prefill=5, prefill_len=60, vocab=shape.vocab, with_logits=True)
+        seq, ol = _oracle_prefill(model, 5, 60)
+        _check(lg[0], toks[0], ol, "prefill")
+        g.kv_resize(1, 3000 * C, 200 * C)  # 21 blocks -> needs 1 granule, keeps 2 mapped
+        assert g.instance_kv(1)["mapped"] == 2 * gran
+        g.kv_resize(2, 0, 4000 * C)  # 258 blocks -> 3 granules: 2 + 3 > 4 forces the reclaim
+        assert g.instance_kv(1)["mapped"] == gran
+        assert g.instance_kv(2)["mapped"] == 3 * gran
+        assert g.stats()["kv_mapped_bytes"] == 4 * gran
+        last = toks[0]
+        for step in range(3):
+            toks, lg = g.step(1, decode=[5], vocab=shape.vocab, with_logits=True)
+            _, ol = seq.feed(last)
+            _check(lg[0], toks[0], ol, f"decode after reclaim {step}")
+            last = toks[0]
+        assert g.stats()["kv_reclaims"] == 1
+        with pytest.raises(MeshGpuError):
+            g.kv_resize(2, 4000 * C, 10000 * C)  # 633 blocks -> 5 granules: beyond the pool
+        model.close()

@@ -57,6 +57,11 @@ typedef struct mesh_gpu_cfg {
     int64_t kv_pool_bytes;  /* physical HBM the KV pool may map (VMM granules) */
     uint64_t prompt_seed;   /* synthetic prompt ids: hash(seed, request, position) */
     int64_t kv_granule_bytes; /* physical chunk per cuMemCreate/cuMemMap, multiple of 2 MiB; 0 = 32 MiB */
+    int32_t lanes;          /* concurrent execution lanes (stream + scratch + an even share of the SM
+                               quota); instances bind to the lane with the fewest weight bytes and
+                               co-located instances on different lanes step concurrently.
+                               0 = MESH_GPU_LANES from the environment, else 1 */
+    int32_t reserved;
 } mesh_gpu_cfg;
 
 typedef struct mesh_step_plan {
@@ -122,6 +127,9 @@ mesh_status mesh_gpu_request_info(mesh_gpu* g, int64_t instance_id, int64_t requ
                                   int32_t* blocks, int32_t* block_ids, int32_t cap);
 mesh_status mesh_gpu_request_tokens(mesh_gpu* g, int64_t instance_id, int64_t request_id, int32_t* tokens,
                                     int32_t cap, int32_t* n_out);
+/* Execution lane an instance is bound to and that lane's SM quota (CTAs). */
+mesh_status mesh_gpu_instance_lane(mesh_gpu* g, int64_t instance_id, int32_t* lane, int32_t* ctas);
+
 mesh_status mesh_gpu_instance_kv(mesh_gpu* g, int64_t instance_id, int64_t* target_bytes, int64_t* mapped_bytes,
                                  int32_t* capacity_blocks, int32_t* live_blocks);
 mesh_status mesh_gpu_read_weight(mesh_gpu* g, int64_t instance_id, int32_t tensor, int32_t layer, int32_t row,

@@ -237,6 +237,8 @@ struct Instance {
     int bt_stride = 0;
     int* d_last_tok = nullptr;     // [MAX_SLOTS]
     std::vector<int> h_block_table;
+    int lane = 0;
+    double weight_bytes = 0;
 };
 
 struct Ticket {
@@ -244,6 +246,7 @@ struct Ticket {
     bool prefill = false;
     std::vector<int64_t> reqs;
     int ring = -1;
+    int lane = 0;
     cudaEvent_t start = nullptr, kend = nullptr, end = nullptr;
     bool logits = false;
     int vocab = 0;
@@ -253,21 +256,15 @@ struct Ticket {
 
 constexpr int RING = 64;
 
-}  // namespace
-
-struct mesh_gpu {
-    mesh_gpu_cfg cfg{};
-    std::string err;
-    int sms = 0;
-    cudaStream_t stream = nullptr;   // compute
-    cudaStream_t side = nullptr;     // swap / migration copies
-    cudaEvent_t timer[8] = {};       // mesh_gpu_timer_mark slots
-    bool check = false;              // MESH_GPU_CHECK: synchronous per-step validation (debug)
-    bool poison = false;             // MESH_GPU_POISON: NaN-fill newly mapped KV granules (debug)
-    PhysPool pool;
-    std::map<int64_t, std::unique_ptr<Instance>> insts;
-    // decode / prefill scratch (sized for the largest registered shape)
-    size_t cap_d = 0, cap_ff = 0, cap_vocab = 0, cap_q = 0, cap_ap = 0, cap_seq = 0;
+// An execution lane: one stream, its own decode/prefill scratch and grid
+// barrier, and a share of the SMs. Instances are bound to a lane; lanes run
+// concurrently, so co-located instances step at the same time on disjoint SM
+// quotas (the persistent decode grids of all lanes sum to <= the SM count, so
+// they can always be co-resident).
+struct Lane {
+    cudaStream_t stream = nullptr;
+    int ctas = 0;  // SM quota: decode grid and prefill GEMM grid
+    // decode scratch
     float* h = nullptr;
     uint16_t* act = nullptr;
     uint16_t* attn = nullptr;
@@ -291,7 +288,25 @@ struct mesh_gpu {
     uint16_t* p_abuf = nullptr;
     float* p_logits = nullptr;
     int* p_tokens = nullptr;
-    int* h_tokens_pinned = nullptr;  // (unused) legacy staging
+    double weight_bytes = 0;  // bound instances (placement balance)
+};
+
+}  // namespace
+
+struct mesh_gpu {
+    mesh_gpu_cfg cfg{};
+    std::string err;
+    int sms = 0;
+    cudaStream_t side = nullptr;     // swap / migration copies
+    cudaEvent_t timer[8] = {};       // mesh_gpu_timer_mark slots
+    cudaEvent_t lane_join = nullptr; // timer marks: joins lanes into lane 0
+    bool check = false;              // MESH_GPU_CHECK: synchronous per-step validation (debug)
+    bool poison = false;             // MESH_GPU_POISON: NaN-fill newly mapped KV granules (debug)
+    PhysPool pool;
+    std::map<int64_t, std::unique_ptr<Instance>> insts;
+    std::vector<Lane> lanes;         // concurrent execution lanes (>= 1)
+    // scratch capacities (sized for the largest registered shape, every lane)
+    size_t cap_d = 0, cap_ff = 0, cap_vocab = 0, cap_q = 0, cap_ap = 0, cap_seq = 0;
     int* h_pf_stage = nullptr;       // [RING][pf_stage_ints] pinned prefill staging (block row + tokens)
     size_t pf_stage_ints = 0;
     // step rings
@@ -328,6 +343,13 @@ uint64_t shape_key_of(const Shape& s, uint64_t seed) {
 
 void device_guard(mesh_gpu* g) { CK(cudaSetDevice(g->cfg.device)); }
 
+Lane& lane_of(mesh_gpu* g, const Instance& in) { return g->lanes[size_t(in.lane)]; }
+cudaStream_t stream_of(mesh_gpu* g, const Instance& in) { return lane_of(g, in).stream; }
+void sync_all(mesh_gpu* g) {
+    for (Lane& l : g->lanes) CK(cudaStreamSynchronize(l.stream));
+    CK(cudaStreamSynchronize(g->side));
+}
+
 template <typename T>
 void dalloc(T** p, size_t n) {
     if (*p) CK(cudaFree(*p));
@@ -340,34 +362,36 @@ void ensure_scratch(mesh_gpu* g, const Shape& s) {
     size_t nd = std::max(g->cap_d, size_t(s.d)), nff = std::max(g->cap_ff, size_t(s.ff)),
            nv = std::max(g->cap_vocab, size_t(s.vocab)), nq = std::max(g->cap_q, size_t(s.n_heads) * s.dh),
            nap = std::max(g->cap_ap, decode_apart_floats(s)), nseq = std::max(g->cap_seq, size_t(s.max_seq));
-    if (g->h && nd == g->cap_d && nff == g->cap_ff && nv == g->cap_vocab && nq == g->cap_q && nap == g->cap_ap &&
+    if (g->lanes[0].h && nd == g->cap_d && nff == g->cap_ff && nv == g->cap_vocab && nq == g->cap_q && nap == g->cap_ap &&
         nseq == g->cap_seq)
         return;
-    CK(cudaStreamSynchronize(g->stream));
+    sync_all(g);
     g->cap_d = nd;
     g->cap_ff = nff;
     g->cap_vocab = nv;
     g->cap_q = nq;
     g->cap_ap = nap;
     g->cap_seq = nseq;
-    dalloc(&g->h, 8 * nd);
-    dalloc(&g->act, 8 * nd);
-    dalloc(&g->attn, 8 * nd);
-    dalloc(&g->abuf, 8 * nff);
-    dalloc(&g->q, 8 * nq);
-    dalloc(&g->ssA, 8 * (nd / 16));
-    dalloc(&g->ssB, 8 * (nd / 16));
-    dalloc(&g->apart, nap);
-    dalloc(&g->acnt, size_t(8) * 64);
-    dalloc(&g->logits, 8 * nv);
-    dalloc(&g->p_h, nseq * nd);
-    dalloc(&g->p_act, nseq * nd);
-    dalloc(&g->p_rs, nseq);
-    dalloc(&g->p_q, nseq * nq);
-    dalloc(&g->p_attn, nseq * nd);
-    dalloc(&g->p_abuf, nseq * nff);
-    dalloc(&g->p_logits, nv);
-    dalloc(&g->p_tokens, nseq);
+    for (Lane& l : g->lanes) {
+        dalloc(&l.h, 8 * nd);
+        dalloc(&l.act, 8 * nd);
+        dalloc(&l.attn, 8 * nd);
+        dalloc(&l.abuf, 8 * nff);
+        dalloc(&l.q, 8 * nq);
+        dalloc(&l.ssA, 8 * (nd / 16));
+        dalloc(&l.ssB, 8 * (nd / 16));
+        dalloc(&l.apart, nap);
+        dalloc(&l.acnt, size_t(8) * 64);
+        dalloc(&l.logits, 8 * nv);
+        dalloc(&l.p_h, nseq * nd);
+        dalloc(&l.p_act, nseq * nd);
+        dalloc(&l.p_rs, nseq);
+        dalloc(&l.p_q, nseq * nq);
+        dalloc(&l.p_attn, nseq * nd);
+        dalloc(&l.p_abuf, nseq * nff);
+        dalloc(&l.p_logits, nv);
+        dalloc(&l.p_tokens, nseq);
+    }
     if (g->h_pf_stage) CK(cudaFreeHost(g->h_pf_stage));
     g->pf_stage_ints = nseq + DEC_BT_MAX;
     CK(cudaHostAlloc((void**)&g->h_pf_stage, g->pf_stage_ints * RING * sizeof(int), cudaHostAllocDefault));
@@ -421,8 +445,7 @@ void unmap_tail(mesh_gpu* g, Instance& in, size_t keep) {
 // then every instance's slack above its capacity is unmapped.
 void reclaim_slack(mesh_gpu* g) {
     g->st.kv_reclaims++;
-    CK(cudaStreamSynchronize(g->stream));
-    CK(cudaStreamSynchronize(g->side));
+    sync_all(g);
     for (auto& [id, ip] : g->insts) unmap_tail(g, *ip, granules_for(g, (long long)ip->cap_blocks * ip->block_bytes));
 }
 
@@ -456,7 +479,8 @@ void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
     // debug (MESH_GPU_POISON): recycled KV memory may hold any bit pattern; fill
     // new granules with bf16 NaN so reads of unwritten KV cannot go unnoticed
     if (g->poison)
-        CK(cudaMemsetAsync(reinterpret_cast<void*>(in.va + first * gran), 0xff, (want - first) * gran, g->stream));
+        CK(cudaMemsetAsync(reinterpret_cast<void*>(in.va + first * gran), 0xff, (want - first) * gran,
+                           stream_of(g, in)));
 }
 
 void write_bt_entry(Instance& in, int slot, int idx, int block) {
@@ -493,14 +517,15 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
     }
     if (!moves.empty()) {
         int2* dpairs = nullptr;
-        CK(cudaMallocAsync((void**)&dpairs, moves.size() * sizeof(int2), g->stream));
-        CK(cudaMemcpyAsync(dpairs, moves.data(), moves.size() * sizeof(int2), cudaMemcpyHostToDevice, g->stream));
+        cudaStream_t st = stream_of(g, in);
+        CK(cudaMallocAsync((void**)&dpairs, moves.size() * sizeof(int2), st));
+        CK(cudaMemcpyAsync(dpairs, moves.data(), moves.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
         dim3 grid(std::max(1, int(std::min<long long>(64, in.block_bytes / (16 * 256)))), unsigned(moves.size()));
-        kv_block_copy<<<grid, 256, 0, g->stream>>>(reinterpret_cast<uint8_t*>(in.va), in.block_bytes, dpairs);
+        kv_block_copy<<<grid, 256, 0, st>>>(reinterpret_cast<uint8_t*>(in.va), in.block_bytes, dpairs);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(in.d_block_table, in.h_block_table.data(), in.h_block_table.size() * sizeof(int),
-                           cudaMemcpyHostToDevice, g->stream));
-        CK(cudaFreeAsync(dpairs, g->stream));
+                           cudaMemcpyHostToDevice, st));
+        CK(cudaFreeAsync(dpairs, st));
         g->st.blocks_moved += (long long)moves.size();
         g->st.bytes_moved += 2LL * (long long)moves.size() * in.block_bytes;
     }
@@ -621,22 +646,23 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.bt_stride = in.bt_stride;
     a.last_tok = in.d_last_tok;
     a.desc = d_desc;
-    a.h = g->h;
-    a.act = g->act;
-    a.attn = g->attn;
-    a.abuf = g->abuf;
-    a.q = g->q;
-    a.ssA = g->ssA;
-    a.ssB = g->ssB;
-    a.apart = g->apart;
-    a.acnt = g->acnt;
-    a.arg_val = g->arg_val;
-    a.arg_idx = g->arg_idx;
-    a.arg_cnt = g->arg_cnt;
-    a.logits = g->capture_logits ? g->logits : nullptr;
+    Lane& ln = lane_of(g, in);
+    a.h = ln.h;
+    a.act = ln.act;
+    a.attn = ln.attn;
+    a.abuf = ln.abuf;
+    a.q = ln.q;
+    a.ssA = ln.ssA;
+    a.ssB = ln.ssB;
+    a.apart = ln.apart;
+    a.acnt = ln.acnt;
+    a.arg_val = ln.arg_val;
+    a.arg_idx = ln.arg_idx;
+    a.arg_cnt = ln.arg_cnt;
+    a.logits = g->capture_logits ? ln.logits : nullptr;
     a.tok_out = g->d_tok + ring * 8;
-    a.bar_count = g->bar;
-    a.bar_gen = g->bar + 1;
+    a.bar_count = ln.bar;
+    a.bar_gen = ln.bar + 1;
     a.progress = g->dbg_dev;
     a.trace = nullptr;
     a.arrive = nullptr;
@@ -645,7 +671,7 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     return a;
 }
 
-int grid_of(mesh_gpu* g) { return g->cfg.sm_quota > 0 ? std::min(g->cfg.sm_quota, g->sms) : g->sms; }
+int grid_of(mesh_gpu* g, const Instance& in) { return lane_of(g, in).ctas; }
 
 // Build the decode descriptor for `rids` (allocating blocks for new positions).
 void build_decode_desc(mesh_gpu* g, Instance& in, const int64_t* rids, int n, StepDesc& d) {
@@ -675,11 +701,12 @@ void build_decode_desc(mesh_gpu* g, Instance& in, const int64_t* rids, int n, St
 void launch_decode_step(mesh_gpu* g, Instance& in, const int64_t* rids, int n, Ticket& t) {
     StepDesc& hd = g->h_desc[t.ring];
     build_decode_desc(g, in, rids, n, hd);
-    CK(cudaMemcpyAsync(g->d_desc + t.ring, &hd, sizeof(StepDesc), cudaMemcpyHostToDevice, g->stream));
-    CK(cudaEventRecord(t.start, g->stream));
+    cudaStream_t st = stream_of(g, in);
+    CK(cudaMemcpyAsync(g->d_desc + t.ring, &hd, sizeof(StepDesc), cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(t.start, st));
     DecodeArgs a = decode_args(g, in, g->d_desc + t.ring, t.ring);
-    CK(launch_decode(a, grid_of(g), g->stream));
-    CK(cudaEventRecord(t.kend, g->stream));
+    CK(launch_decode(a, grid_of(g, in), st));
+    CK(cudaEventRecord(t.kend, st));
     g->st.kernel_launches += 1;
     g->st.h2d_bytes += (long long)sizeof(StepDesc);
     for (int i = 0; i < n; ++i) {
@@ -700,7 +727,7 @@ void restore_from_swap(mesh_gpu* g, Instance& in, int64_t rid, ReqState& r, Swap
         write_bt_entry(in, r.slot, i, b);
         CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(in.va) + size_t(b) * in.block_bytes,
                            static_cast<uint8_t*>(e.host) + size_t(i) * in.block_bytes, in.block_bytes,
-                           cudaMemcpyHostToDevice, g->stream));
+                           cudaMemcpyHostToDevice, stream_of(g, in)));
     }
     r.ctx = e.ctx;
     r.tokens = e.tokens;
@@ -758,9 +785,10 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     int* stage = g->h_pf_stage + size_t(t.ring) * g->pf_stage_ints;
     std::memcpy(stage, in.h_block_table.data() + size_t(r.slot) * in.bt_stride, sizeof(int) * in.bt_stride);
     std::memcpy(stage + in.bt_stride, r.tokens.data() + p0, sizeof(int) * L);
+    Lane& ln = lane_of(g, in);
     CK(cudaMemcpyAsync(in.d_block_table + size_t(r.slot) * in.bt_stride, stage, sizeof(int) * in.bt_stride,
-                       cudaMemcpyHostToDevice, g->stream));
-    CK(cudaMemcpyAsync(g->p_tokens, stage + in.bt_stride, sizeof(int) * L, cudaMemcpyHostToDevice, g->stream));
+                       cudaMemcpyHostToDevice, ln.stream));
+    CK(cudaMemcpyAsync(ln.p_tokens, stage + in.bt_stride, sizeof(int) * L, cudaMemcpyHostToDevice, ln.stream));
     g->st.h2d_bytes += (long long)sizeof(int) * (in.bt_stride + L);
     PrefillArgs a{};
     a.s = in.s;
@@ -771,19 +799,20 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     a.slot = r.slot;
     a.L = L;
     a.p0 = p0;
-    a.tokens = g->p_tokens;
-    a.h = g->p_h;
-    a.act = g->p_act;
-    a.rs = g->p_rs;
-    a.q = reinterpret_cast<uint16_t*>(g->p_q);  // bf16 view of the fp32-sized buffer
-    a.attn = g->p_attn;
-    a.abuf = g->p_abuf;
-    a.logits = g->p_logits;
+    a.tokens = ln.p_tokens;
+    a.h = ln.p_h;
+    a.act = ln.p_act;
+    a.rs = ln.p_rs;
+    a.q = reinterpret_cast<uint16_t*>(ln.p_q);  // bf16 view of the fp32-sized buffer
+    a.attn = ln.p_attn;
+    a.abuf = ln.p_abuf;
+    a.logits = ln.p_logits;
+    a.max_ctas = ln.ctas;
     a.last_tok = in.d_last_tok;
     a.tok_out = g->d_tok + t.ring * 8;
-    CK(cudaEventRecord(t.start, g->stream));
-    CK(launch_prefill(a, g->stream));
-    CK(cudaEventRecord(t.kend, g->stream));
+    CK(cudaEventRecord(t.start, ln.stream));
+    CK(launch_prefill(a, ln.stream));
+    CK(cudaEventRecord(t.kend, ln.stream));
     g->st.kernel_launches += prefill_launch_count(in.s);
     r.ctx = p0 + L;
     // history: the prefill consumed tokens[0, n); anything beyond is stale
@@ -841,8 +870,23 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             throw MeshError(MESH_ERR_CUDA, std::string("sm_100a kernels need a Blackwell B200, found ") + prop.name);
         g->sms = prop.multiProcessorCount;
         if (!drv().ok) throw MeshError(MESH_ERR_CUDA, "CUDA VMM driver entry points unavailable");
-        CK(cudaStreamCreateWithFlags(&g->stream, cudaStreamNonBlocking));
+        // lanes: cfg->lanes (else MESH_GPU_LANES, else 1); the SMs (or the quota) split evenly
+        int nl = cfg->lanes > 0 ? cfg->lanes : 1;
+        if (cfg->lanes <= 0)
+            if (const char* e = std::getenv("MESH_GPU_LANES")) nl = std::max(1, std::atoi(e));
+        const int budget = cfg->sm_quota > 0 ? std::min(cfg->sm_quota, g->sms) : g->sms;
+        if (nl > budget) throw MeshError(MESH_ERR_ARG, "more lanes than SMs");
+        g->lanes.resize(size_t(nl));
+        for (Lane& l : g->lanes) {
+            CK(cudaStreamCreateWithFlags(&l.stream, cudaStreamNonBlocking));
+            l.ctas = budget / nl;
+            dalloc(&l.bar, 2);
+            dalloc(&l.arg_val, size_t(8) * g->sms);
+            dalloc(&l.arg_idx, size_t(8) * g->sms);
+            dalloc(&l.arg_cnt, 1);
+        }
         CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&g->lane_join, cudaEventDisableTiming));
         g->pool.device = cfg->device;
         CUmemAllocationProp prop2 = {};
         prop2.type = CU_MEM_ALLOCATION_TYPE_PINNED;
@@ -858,10 +902,6 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->pool.gran = want;
         g->st.kv_granule_bytes = (long long)want;
         g->pool.limit = cfg->kv_pool_bytes > 0 ? cfg->kv_pool_bytes : (long long)(prop.totalGlobalMem / 2);
-        dalloc(&g->bar, 2);
-        dalloc(&g->arg_val, size_t(8) * g->sms);
-        dalloc(&g->arg_idx, size_t(8) * g->sms);
-        dalloc(&g->arg_cnt, 1);
         CK(cudaHostAlloc((void**)&g->h_desc, sizeof(StepDesc) * RING, cudaHostAllocDefault));
         CK(cudaMalloc((void**)&g->d_desc, sizeof(StepDesc) * RING));
         CK(cudaHostAlloc((void**)&g->h_tok, sizeof(int) * 8 * RING, cudaHostAllocDefault));
@@ -907,9 +947,15 @@ void mesh_gpu_close(mesh_gpu* g) {
         cudaFree(in->d_last_tok);
     }
     for (auto h : g->pool.all) drv().release(h);
-    void* dev_ptrs[] = {g->h, g->act, g->attn, g->abuf, g->q, g->ssA, g->ssB, g->apart, g->acnt, g->arg_val,
-                        g->arg_idx, g->arg_cnt, g->logits, g->bar, g->p_h, g->p_act, g->p_rs, g->p_q, g->p_attn,
-                        g->p_abuf, g->p_logits, g->p_tokens, g->d_desc, g->d_tok};
+    for (Lane& l : g->lanes) {
+        void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
+                             l.arg_idx, l.arg_cnt, l.logits, l.bar, l.p_h, l.p_act, l.p_rs, l.p_q, l.p_attn,
+                             l.p_abuf, l.p_logits, l.p_tokens};
+        for (void* p : lane_ptrs)
+            if (p) cudaFree(p);
+        if (l.stream) cudaStreamDestroy(l.stream);
+    }
+    void* dev_ptrs[] = {g->d_desc, g->d_tok};
     for (void* p : dev_ptrs)
         if (p) cudaFree(p);
     if (g->h_desc) cudaFreeHost(g->h_desc);
@@ -917,10 +963,10 @@ void mesh_gpu_close(mesh_gpu* g) {
     if (g->h_pf_stage) cudaFreeHost(g->h_pf_stage);
     for (int i = 0; i < RING; ++i)
         if (g->ring_ev[i]) cudaEventDestroy(g->ring_ev[i]);
-    if (g->stream) cudaStreamDestroy(g->stream);
     if (g->side) cudaStreamDestroy(g->side);
     for (cudaEvent_t e : g->timer)
         if (e) cudaEventDestroy(e);
+    if (g->lane_join) cudaEventDestroy(g->lane_join);
     delete g;
 }
 
@@ -952,6 +998,12 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         ensure_scratch(g, s);
         auto in = std::make_unique<Instance>();
         in->id = instance_id;
+        // bind to the lane with the fewest weight bytes (the HBM each step streams)
+        size_t best = 0;
+        for (size_t i = 1; i < g->lanes.size(); ++i)
+            if (g->lanes[i].weight_bytes < g->lanes[best].weight_bytes) best = i;
+        in->lane = int(best);
+        cudaStream_t st = g->lanes[best].stream;
         in->s = s;
         in->seed = weight_seed;
         in->shape_key = shape_key_of(s, weight_seed);
@@ -981,16 +1033,16 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         in->w = Weights{wq, wo, wgu, wdn, wlm, wemb, ga, gm, gf, rp, qkv, o, gu, dn};
         const int blocks = g->sms * 8;
         for (int l = 0; l < s.n_layers; ++l) {
-            init_tiled<0><<<blocks, 256, 0, g->stream>>>(wq + l * qkv, s, weight_seed, l, s.qkv_rows(), s.d);
-            init_tiled<1><<<blocks, 256, 0, g->stream>>>(wo + l * o, s, weight_seed, l, s.d, s.n_heads * s.dh);
-            init_tiled<2><<<blocks, 256, 0, g->stream>>>(wgu + l * gu, s, weight_seed, l, 2 * s.ff, s.d);
-            init_tiled<3><<<blocks, 256, 0, g->stream>>>(wdn + l * dn, s, weight_seed, l, s.d, s.ff);
-            init_gain<<<32, 256, 0, g->stream>>>(ga + size_t(l) * s.d, s.d, weight_seed, T_GATTN, l);
-            init_gain<<<32, 256, 0, g->stream>>>(gm + size_t(l) * s.d, s.d, weight_seed, T_GMLP, l);
+            init_tiled<0><<<blocks, 256, 0, st>>>(wq + l * qkv, s, weight_seed, l, s.qkv_rows(), s.d);
+            init_tiled<1><<<blocks, 256, 0, st>>>(wo + l * o, s, weight_seed, l, s.d, s.n_heads * s.dh);
+            init_tiled<2><<<blocks, 256, 0, st>>>(wgu + l * gu, s, weight_seed, l, 2 * s.ff, s.d);
+            init_tiled<3><<<blocks, 256, 0, st>>>(wdn + l * dn, s, weight_seed, l, s.d, s.ff);
+            init_gain<<<32, 256, 0, st>>>(ga + size_t(l) * s.d, s.d, weight_seed, T_GATTN, l);
+            init_gain<<<32, 256, 0, st>>>(gm + size_t(l) * s.d, s.d, weight_seed, T_GMLP, l);
         }
-        init_tiled<4><<<blocks, 256, 0, g->stream>>>(wlm, s, weight_seed, 0, s.vocab, s.d);
-        init_emb<<<blocks, 256, 0, g->stream>>>(wemb, s, weight_seed);
-        init_gain<<<32, 256, 0, g->stream>>>(gf, s.d, weight_seed, T_GFINAL, 0);
+        init_tiled<4><<<blocks, 256, 0, st>>>(wlm, s, weight_seed, 0, s.vocab, s.d);
+        init_emb<<<blocks, 256, 0, st>>>(wemb, s, weight_seed);
+        init_gain<<<32, 256, 0, st>>>(gf, s.d, weight_seed, T_GFINAL, 0);
         CK(cudaGetLastError());
         // rotate-half RoPE table, computed in double on the host (the oracle uses the same formula)
         std::vector<float2> tab(size_t(s.max_seq) * (s.dh / 2));
@@ -1000,7 +1052,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
                 double ang = double(pos) * inv;
                 tab[size_t(pos) * (s.dh / 2) + i] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
             }
-        CK(cudaMemcpyAsync(rp, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, g->stream));
+        CK(cudaMemcpyAsync(rp, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
         // KV region: reserve the whole pool's worth of VA
         in->block_bytes = (long long)KV_BLOCK_TOKENS * s.kv_bytes_per_token();
         size_t gran = g->pool.gran;
@@ -1009,11 +1061,13 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
         in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
         CK(cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()));
-        CK(cudaMemsetAsync(in->d_block_table, 0, sizeof(int) * in->h_block_table.size(), g->stream));
+        CK(cudaMemsetAsync(in->d_block_table, 0, sizeof(int) * in->h_block_table.size(), st));
         CK(cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS));
-        CK(cudaMemsetAsync(in->d_last_tok, 0, sizeof(int) * MAX_SLOTS, g->stream));
+        CK(cudaMemsetAsync(in->d_last_tok, 0, sizeof(int) * MAX_SLOTS, st));
         for (int i = MAX_SLOTS - 1; i >= 0; --i) in->free_slots.push_back(i);
-        CK(cudaStreamSynchronize(g->stream));
+        CK(cudaStreamSynchronize(st));
+        in->weight_bytes = double(total);
+        g->lanes[best].weight_bytes += in->weight_bytes;
         g->insts.emplace(instance_id, std::move(in));
     });
 }
@@ -1022,9 +1076,10 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
     if (!g) return MESH_ERR_ARG;
     return guarded(g, [&] {
         Instance& in = inst_of(g, instance_id);
-        CK(cudaStreamSynchronize(g->stream));
+        CK(cudaStreamSynchronize(stream_of(g, in)));
         CK(cudaStreamSynchronize(g->side));
         unmap_tail(g, in, 0);
+        lane_of(g, in).weight_bytes -= in.weight_bytes;
         CU(drv().addr_free(in.va, in.va_size), "cuMemAddressFree");
         CK(cudaFree(in.wmem));
         CK(cudaFree(in.d_block_table));
@@ -1111,6 +1166,8 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
         t.logits = g->capture_logits;
         t.vocab = in.s.vocab;
         t.ring = take_ring(g);
+        t.lane = in.lane;
+        cudaStream_t st = stream_of(g, in);
         CK(cudaEventCreate(&t.start));
         CK(cudaEventCreate(&t.kend));
         CK(cudaEventCreate(&t.end));
@@ -1130,13 +1187,13 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
             throw;
         }
         CK(cudaMemcpyAsync(g->h_tok + t.ring * 8, g->d_tok + t.ring * 8, sizeof(int) * 8, cudaMemcpyDeviceToHost,
-                           g->stream));
+                           st));
         g->st.d2h_bytes += (long long)sizeof(int) * 8;
-        CK(cudaEventRecord(t.end, g->stream));
-        CK(cudaEventRecord(g->ring_ev[t.ring], g->stream));
+        CK(cudaEventRecord(t.end, st));
+        CK(cudaEventRecord(g->ring_ev[t.ring], st));
         g->st.steps++;
         if (g->check) {  // debug (MESH_GPU_CHECK=1): validate every step synchronously
-            CK(cudaStreamSynchronize(g->stream));
+            CK(cudaStreamSynchronize(st));
             const int n = t.prefill ? 1 : plan->n_decode;
             for (int i = 0; i < n; ++i) {
                 const int tok = g->h_tok[t.ring * 8 + i];
@@ -1177,7 +1234,8 @@ mesh_status mesh_gpu_step_wait(mesh_gpu* g, int64_t ticket, int32_t* tokens_out,
             // valid only for the most recent step (scratch is reused)
             size_t cnt = t.prefill ? size_t(t.vocab) : t.reqs.size() * size_t(t.vocab);
             if ((int64_t)cnt > logits_cap) throw MeshError(MESH_ERR_ARG, "logits buffer too small");
-            CK(cudaMemcpy(logits_out, t.prefill ? g->p_logits : g->logits, cnt * sizeof(float),
+            const Lane& ln = g->lanes[size_t(t.lane)];
+            CK(cudaMemcpy(logits_out, t.prefill ? ln.p_logits : ln.logits, cnt * sizeof(float),
                           cudaMemcpyDeviceToHost));
         }
         destroy_ticket(t);
@@ -1220,7 +1278,7 @@ mesh_status mesh_gpu_swap_out(mesh_gpu* g, int64_t instance_id, int64_t request_
             // order after every step that wrote this request's KV
             cudaEvent_t ready;
             CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-            CK(cudaEventRecord(ready, g->stream));
+            CK(cudaEventRecord(ready, stream_of(g, in)));
             CK(cudaStreamWaitEvent(g->side, ready, 0));
             cudaEventDestroy(ready);
             for (size_t i = 0; i < r.blocks.size(); ++i)
@@ -1254,13 +1312,14 @@ mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst,
         auto it = si.reqs.find(request_id);
         if (it == si.reqs.end()) throw MeshError(MESH_ERR_ARG, "migrate: request not resident at source");
         flush_request(src, src_instance, request_id);
-        CK(cudaStreamSynchronize(src->stream));
+        CK(cudaStreamSynchronize(stream_of(src, si)));
         CK(cudaSetDevice(dst->cfg.device));
         Instance& di = inst_of(dst, dst_instance);
         if (di.shape_key != si.shape_key) throw MeshError(MESH_ERR_ARG, "migrate: instances serve different models");
         ReqState& sr = it->second;
         if (di.reqs.count(request_id)) throw MeshError(MESH_ERR_ARG, "migrate: request already at destination");
         ReqState& dr = req_slot(di, request_id);
+        cudaStream_t dst_st = stream_of(dst, di);
         dr.tokens = sr.tokens;
         dr.ctx = sr.ctx;
         for (size_t i = 0; i < sr.blocks.size(); ++i) {
@@ -1270,17 +1329,17 @@ mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst,
             void* dptr = reinterpret_cast<uint8_t*>(di.va) + size_t(b) * di.block_bytes;
             const void* sptr = reinterpret_cast<uint8_t*>(si.va) + size_t(sr.blocks[i]) * si.block_bytes;
             if (src->cfg.device == dst->cfg.device)
-                CK(cudaMemcpyAsync(dptr, sptr, di.block_bytes, cudaMemcpyDeviceToDevice, dst->stream));
+                CK(cudaMemcpyAsync(dptr, sptr, di.block_bytes, cudaMemcpyDeviceToDevice, dst_st));
             else
-                CK(cudaMemcpyPeerAsync(dptr, dst->cfg.device, sptr, src->cfg.device, di.block_bytes, dst->stream));
+                CK(cudaMemcpyPeerAsync(dptr, dst->cfg.device, sptr, src->cfg.device, di.block_bytes, dst_st));
         }
         // the device-side last token travels with the request
         int last = sr.tokens.empty() ? 0 : sr.tokens.back();
-        set_int<<<1, 1, 0, dst->stream>>>(di.d_last_tok + dr.slot, last);
+        set_int<<<1, 1, 0, dst_st>>>(di.d_last_tok + dr.slot, last);
         CK(cudaMemcpyAsync(di.d_block_table + size_t(dr.slot) * di.bt_stride,
                            di.h_block_table.data() + size_t(dr.slot) * di.bt_stride, sizeof(int) * di.bt_stride,
-                           cudaMemcpyHostToDevice, dst->stream));
-        CK(cudaStreamSynchronize(dst->stream));
+                           cudaMemcpyHostToDevice, dst_st));
+        CK(cudaStreamSynchronize(dst_st));
         dst->st.migrate_bytes += (long long)sr.blocks.size() * di.block_bytes;
         CK(cudaSetDevice(src->cfg.device));
         free_request(si, request_id);
@@ -1320,6 +1379,15 @@ mesh_status mesh_gpu_request_tokens(mesh_gpu* g, int64_t instance_id, int64_t re
         int n = int(src->size());
         for (int i = 0; i < std::min(n, cap); ++i) tokens[i] = (*src)[i];
         if (n_out) *n_out = n;
+    });
+}
+
+mesh_status mesh_gpu_instance_lane(mesh_gpu* g, int64_t instance_id, int32_t* lane, int32_t* ctas) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        if (lane) *lane = in.lane;
+        if (ctas) *ctas = lane_of(g, in).ctas;
     });
 }
 
@@ -1374,9 +1442,10 @@ mesh_status mesh_gpu_read_weight(mesh_gpu* g, int64_t instance_id, int32_t tenso
         if (prow < 0 || n < K) throw MeshError(MESH_ERR_ARG, "read_weight: bad row or buffer");
         float* d = nullptr;
         CK(cudaMalloc((void**)&d, sizeof(float) * K));
-        read_tiled_row<<<1, 256, 0, g->stream>>>(W, K, prow, d);
-        CK(cudaMemcpyAsync(out, d, sizeof(float) * K, cudaMemcpyDeviceToHost, g->stream));
-        CK(cudaStreamSynchronize(g->stream));
+        cudaStream_t st = stream_of(g, in);
+        read_tiled_row<<<1, 256, 0, st>>>(W, K, prow, d);
+        CK(cudaMemcpyAsync(out, d, sizeof(float) * K, cudaMemcpyDeviceToHost, st));
+        CK(cudaStreamSynchronize(st));
         CK(cudaFree(d));
     });
 }
@@ -1390,17 +1459,22 @@ mesh_status mesh_gpu_stats_get(mesh_gpu* g, mesh_gpu_stats* out) {
 
 mesh_status mesh_gpu_sync(mesh_gpu* g) {
     if (!g) return MESH_ERR_ARG;
-    return guarded(g, [&] {
-        CK(cudaStreamSynchronize(g->stream));
-        CK(cudaStreamSynchronize(g->side));
-    });
+    return guarded(g, [&] { sync_all(g); });
 }
 
 mesh_status mesh_gpu_timer_mark(mesh_gpu* g, int32_t slot) {
     if (!g || slot < 0 || slot >= 8) return MESH_ERR_ARG;
     return guarded(g, [&] {
+        // a mark orders every lane: lane 0 joins the others, records, and they
+        // wait on the mark, so an interval between two marks covers all lanes
         if (!g->timer[slot]) CK(cudaEventCreate(&g->timer[slot]));
-        CK(cudaEventRecord(g->timer[slot], g->stream));
+        cudaStream_t s0 = g->lanes[0].stream;
+        for (size_t i = 1; i < g->lanes.size(); ++i) {
+            CK(cudaEventRecord(g->lane_join, g->lanes[i].stream));
+            CK(cudaStreamWaitEvent(s0, g->lane_join, 0));
+        }
+        CK(cudaEventRecord(g->timer[slot], s0));
+        for (size_t i = 1; i < g->lanes.size(); ++i) CK(cudaStreamWaitEvent(g->lanes[i].stream, g->timer[slot], 0));
     });
 }
 
@@ -1449,24 +1523,24 @@ mesh_status mesh_gpu_bench_decode(mesh_gpu* g, int64_t instance_id, const mesh_s
             CK(cudaMalloc((void**)&tr, sizeof(unsigned long long) * 4096));
             CK(cudaMemset(tr, 0, sizeof(unsigned long long) * 4096));
         }
-        CK(launch_decode(a, grid_of(g), g->stream));  // warm
+        CK(launch_decode(a, grid_of(g, in), stream_of(g, in)));  // warm
         if (tr) {
             DecodeArgs at = a;
             at.trace = tr;
             unsigned long long* arr = nullptr;
-            const size_t narr = size_t(256) * grid_of(g);
+            const size_t narr = size_t(256) * grid_of(g, in);
             CK(cudaMalloc((void**)&arr, sizeof(unsigned long long) * narr));
             CK(cudaMemset(arr, 0, sizeof(unsigned long long) * narr));
             at.arrive = arr;
-            CK(launch_decode(at, grid_of(g), g->stream));
-            CK(cudaStreamSynchronize(g->stream));
+            CK(launch_decode(at, grid_of(g, in), stream_of(g, in)));
+            CK(cudaStreamSynchronize(stream_of(g, in)));
             {
                 std::vector<unsigned long long> ha(narr);
                 CK(cudaMemcpy(ha.data(), arr, sizeof(unsigned long long) * narr, cudaMemcpyDeviceToHost));
                 std::string ap = std::string(trace_path) + ".arrive";
                 FILE* fa = std::fopen(ap.c_str(), "w");
                 if (fa) {
-                    for (size_t i = 0; i < narr; ++i) std::fprintf(fa, "%llu%c", ha[i], (i + 1) % grid_of(g) ? ' ' : '\n');
+                    for (size_t i = 0; i < narr; ++i) std::fprintf(fa, "%llu%c", ha[i], (i + 1) % grid_of(g, in) ? ' ' : '\n');
                     std::fclose(fa);
                 }
                 CK(cudaFree(arr));
@@ -1481,15 +1555,15 @@ mesh_status mesh_gpu_bench_decode(mesh_gpu* g, int64_t instance_id, const mesh_s
             }
             CK(cudaFree(tr));
         }
-        CK(cudaEventRecord(e0, g->stream));
-        for (int i = 0; i < iters; ++i) CK(launch_decode(a, grid_of(g), g->stream));
-        CK(cudaEventRecord(e1, g->stream));
+        CK(cudaEventRecord(e0, stream_of(g, in)));
+        for (int i = 0; i < iters; ++i) CK(launch_decode(a, grid_of(g, in), stream_of(g, in)));
+        CK(cudaEventRecord(e1, stream_of(g, in)));
         if (g->dbg_host) {
             for (int spin = 0; cudaEventQuery(e1) == cudaErrorNotReady; ++spin) {
                 usleep(1000);
                 if (spin == 20000) {
                     std::fprintf(stderr, "decode watchdog: step not finished after 20 s; per-CTA (barriers, stage):\n");
-                    for (int i = 0; i < grid_of(g); ++i)
+                    for (int i = 0; i < grid_of(g, in); ++i)
                         std::fprintf(stderr, "%d:(%d,%d) ", i, g->dbg_host[2 * i], g->dbg_host[2 * i + 1]);
                     std::fprintf(stderr, "\n");
                     std::fflush(stderr);

@@ -750,7 +750,8 @@ cudaError_t gemm_tc_launch(const PrefillArgs& a, const uint8_t* W, int N, int K,
     CUtensorMap wm, xm;
     if (!make_wmap(&wm, W, N, K) || !make_xmap(&xm, X, K, ldx, rows, BN / CS)) return cudaErrorInvalidValue;
     const int ctiles = (N / TC_BM / CS) * ((rows + BN - 1) / BN);
-    cfg.gridDim = dim3(CS * std::min(ctiles, max_clusters));
+    const int quota = a.max_ctas > 0 ? std::max(1, a.max_ctas / CS) : max_clusters;
+    cfg.gridDim = dim3(CS * std::min(ctiles, std::min(max_clusters, quota)));
     return cudaLaunchKernelEx(&cfg, pf_gemm_tc<KIND, BN, CS>, a, wm, xm, N, K, rows, layer);
 }
 

@@ -26,6 +26,7 @@ struct PrefillArgs {
     float* logits;      // [vocab] (last token)
     int* last_tok;      // instance request table
     int* tok_out;       // [1]
+    int max_ctas;       // SM quota of the lane (persistent GEMM grid); 0 = all SMs
 };
 
 cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t stream);

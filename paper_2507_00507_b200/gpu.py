@@ -33,7 +33,8 @@ class ModelShape(C.Structure):
 
 class GpuCfg(C.Structure):
     _fields_ = [("device", C.c_int32), ("sm_quota", C.c_int32), ("kv_pool_bytes", C.c_int64),
-                ("prompt_seed", C.c_uint64), ("kv_granule_bytes", C.c_int64)]
+                ("prompt_seed", C.c_uint64), ("kv_granule_bytes", C.c_int64), ("lanes", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class StepPlan(C.Structure):
@@ -135,6 +136,7 @@ def _load() -> C.CDLL:
                                               P(C.c_int32)]),
         "mesh_gpu_instance_kv": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int64), P(C.c_int64), P(C.c_int32),
                                            P(C.c_int32)]),
+        "mesh_gpu_instance_lane": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int32), P(C.c_int32)]),
         "mesh_gpu_read_weight": (C.c_int, [C.c_void_p, C.c_int64, C.c_int32, C.c_int32, C.c_int32, P(C.c_float),
                                            C.c_int32]),
         "mesh_gpu_stats_get": (C.c_int, [C.c_void_p, P(GpuStats)]),
@@ -164,16 +166,17 @@ EXPORTED = ["mesh_gpu_version", "mesh_gpu_device_count", "mesh_gpu_open", "mesh_
             "mesh_gpu_instance_create", "mesh_gpu_instance_destroy", "mesh_gpu_kv_resize", "mesh_gpu_step",
             "mesh_gpu_step_wait", "mesh_gpu_set_capture_logits", "mesh_gpu_request_free", "mesh_gpu_swap_out",
             "mesh_gpu_migrate", "mesh_gpu_request_info", "mesh_gpu_request_tokens", "mesh_gpu_instance_kv",
-            "mesh_gpu_read_weight", "mesh_gpu_stats_get", "mesh_gpu_sync", "mesh_gpu_bench_decode"]
+            "mesh_gpu_read_weight", "mesh_gpu_stats_get", "mesh_gpu_sync", "mesh_gpu_bench_decode",
+            "mesh_gpu_instance_lane"]
 
 
 class MeshGpu:
     """One B200 (one handle of the C ABI)."""
 
     def __init__(self, device: int = 0, sm_quota: int = 0, kv_pool_bytes: int = 0, prompt_seed: int = 1234,
-                 kv_granule_bytes: int = 0):
+                 kv_granule_bytes: int = 0, lanes: int = 0):
         self._l = lib()
-        cfg = GpuCfg(device, sm_quota, kv_pool_bytes, prompt_seed, kv_granule_bytes)
+        cfg = GpuCfg(device, sm_quota, kv_pool_bytes, prompt_seed, kv_granule_bytes, lanes, 0)
         h = C.c_void_p()
         st = self._l.mesh_gpu_open(C.byref(cfg), C.byref(h))
         if st != MESH_OK:
@@ -263,6 +266,12 @@ class MeshGpu:
         cap, live = C.c_int32(), C.c_int32()
         self._ck(self._l.mesh_gpu_instance_kv(self.h, iid, C.byref(t), C.byref(m), C.byref(cap), C.byref(live)))
         return {"target": t.value, "mapped": m.value, "capacity_blocks": cap.value, "live_blocks": live.value}
+
+    def instance_lane(self, iid: int) -> tuple[int, int]:
+        """(lane, lane SM quota) the instance is bound to."""
+        lane, ctas = C.c_int32(), C.c_int32()
+        self._ck(self._l.mesh_gpu_instance_lane(self.h, iid, C.byref(lane), C.byref(ctas)))
+        return lane.value, ctas.value
 
     def read_weight(self, iid: int, tensor: int, layer: int, row: int, n: int) -> np.ndarray:
         out = np.zeros(n, dtype=np.float32)

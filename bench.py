@@ -51,6 +51,7 @@ METRIC = "co-located tokens/s at TTFT/TPOT SLO per B200"
 UNIT = "tokens/s"
 MODELS = ["1b", "3b", "1b", "3b"]
 BATCH = 8
+LANES = int(os.environ.get("MESH_BENCH_LANES", "4"))  # one execution lane per co-located instance
 E2E_WINDOW_S = 20.0
 E2E_SCEN = os.path.join(ROOT, "scenarios", "c2_saturated", "config.json")
 CPU_MAX_SEQ = 64        # CPU sample contexts (short: generous to the CPU)
@@ -167,7 +168,7 @@ class Colocated:
         import random
 
         from paper_2507_00507_b200.gpu import SHAPES, MeshGpu
-        self.g = MeshGpu(device, kv_pool_bytes=48 << 30, prompt_seed=seed)
+        self.g = MeshGpu(device, kv_pool_bytes=48 << 30, prompt_seed=seed, lanes=LANES)
         self.shapes = [SHAPES[m] for m in MODELS]
         self.rng = random.Random(seed)
         self.lengths = load_lengths()
@@ -179,6 +180,7 @@ class Colocated:
             self.g.kv_resize(iid, 0, kv)
             self.insts.append({"id": iid, "shape": shape, "reqs": [], "pending": []})
         self.clock = 0.0  # device-time clock (s) for SLO accounting
+        self.mark0 = None  # clock value at timer mark 0: emissions are then read off the device timeline
         self.tokens_ok = 0
         self.tokens_all = 0
         self.violations = 0
@@ -251,7 +253,11 @@ class Colocated:
         t, inst, kind, reqs = item
         self.g.wait(t)
         st = self.g.stats()
-        self.clock += st["last_step_ms"] / 1e3
+        if self.mark0 is not None and st["last_step_end_ms"] >= 0:
+            emit = self.mark0 + st["last_step_end_ms"] / 1e3  # the step's end on the device timeline
+        else:
+            emit = self.clock + st["last_step_ms"] / 1e3      # untimed warm-up: steps back to back
+        self.clock = max(self.clock, emit)
         if kind == "decode":
             s = inst["shape"]
             ctx = sum(r["I"] + r["gen"] for r in reqs)
@@ -261,7 +267,7 @@ class Colocated:
             self.decode_steps += 1
         for r in reqs:
             deadline = r["arrival"] + max(2.0, r["I"] / 512.0) + 0.25 * r["gen"]
-            if self.clock > deadline + 1e-9:
+            if emit > deadline + 1e-9:
                 r["ok"] = False
             r["gen"] += 1
             self.tokens_all += 1
@@ -373,6 +379,7 @@ def run_e2e(device: int, d: Dist):
     import tempfile
 
     from paper_2507_00507_b200 import control, gpu
+    os.environ["MESH_GPU_LANES"] = str(LANES)  # the data plane under the control plane: one lane per instance
     with control.Experiment(E2E_SCEN) as exp:
         exp.out_dir(tempfile.mkdtemp(prefix="mesh_e2e_"))
         exp.attach_gpu([device], 48 << 30, gpu.LIB_PATH)
@@ -412,6 +419,7 @@ def run_ours(args, d: Dist):
     with Clocks(device) as clk:
         node.g.sync()
         node.g.timer_mark(0)
+        node.mark0 = node.clock
         launches = node.run(args.steps)
         node.g.timer_mark(1)
         node.g.sync()
@@ -419,7 +427,13 @@ def run_ours(args, d: Dist):
     wall_max = d.reduce(dev_s, "max")
     tok_ok = d.reduce(float(node.tokens_ok), "sum")
     value = tok_ok / wall_max
-    achieved = node.decode_bytes / (node.decode_kernel_ms / 1e3) / 1e9 if node.decode_kernel_ms else 0.0
+    # Decode launches of the four lanes overlap, so a launch's own duration is not the
+    # time the node spends per launch: achieved = algorithmic decode bytes of every
+    # launch over the timed device span (prefill steps inside the span make it a lower
+    # bound); the single-launch figure (bytes / the launch's own CUDA-event time, on
+    # its lane's SM quota) is kept beside it.
+    per_launch = node.decode_bytes / (node.decode_kernel_ms / 1e3) / 1e9 if node.decode_kernel_ms else 0.0
+    achieved = node.decode_bytes / dev_s / 1e9 if dev_s else 0.0
     e2e = run_e2e(device, d) if not args.no_e2e else None
     if d.rank != 0:
         return
@@ -437,15 +451,24 @@ def run_ours(args, d: Dist):
         "config": {"workload": "C2: 4 co-located Llama-shaped instances [1.1B, 3B, 1.1B, 3B] on one B200, "
                                "batch 8 each, shared VMM KV pool",
                    "models": MODELS, "batch_per_instance": BATCH, "step": "one instance step (decode of its batch "
-                   "or prefill of a newly admitted request), instances in turn",
+                   "or prefill of a newly admitted request), issued in turn; each instance on its own "
+                   f"execution lane ({LANES} lanes, SM quotas in proportion to streamed weight bytes), so "
+                   "co-located instances step concurrently",
+                   "lane_sm_quotas": [node.g.instance_lane(i["id"])[1] for i in node.insts],
                    "l2": "weights 17 GB + KV streamed per 4-step round >> 126 MB L2",
                    "slo_compliant_tokens": int(node.tokens_ok), "tokens": int(node.tokens_all),
                    "completed_requests": node.completed, "slo_violations": node.violations,
                    "decode_steps": node.decode_steps, "parallelism": f"{d.ws} independent co-located nodes"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,
-                     "kernel": "decode_kernel (persistent, TMA-ring)", "peak_source": peak_kind,
-                     "algorithmic_bytes_per_launch": node.decode_bytes / max(1, node.decode_steps)},
+                     "kernel": "decode_kernel (persistent, TMA-ring), one launch per lane step",
+                     "peak_source": peak_kind,
+                     "algorithmic_bytes_per_launch": node.decode_bytes / max(1, node.decode_steps),
+                     "launches": node.decode_steps,
+                     "achieved_basis": "sum of decode launches' algorithmic bytes / timed device span "
+                                       "(lanes overlap; prefill steps in the span make this a lower bound)",
+                     "per_launch_gbs": per_launch,
+                     "per_launch_note": "bytes / the launch's own CUDA-event time on its lane's SM quota"},
         "cpu_baseline": cpu,
         "reference_simulator": sim,
         "e2e": e2e,

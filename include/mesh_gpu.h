@@ -88,6 +88,8 @@ typedef struct mesh_gpu_stats {
     int64_t vmm_calls;            /* cuMemMap / cuMemUnmap / cuMemSetAccess calls */
     double vmm_ms;                /* host time inside them */
     int64_t kv_reclaims;          /* lazy-shrink slack reclaims (each drains the streams once) */
+    double last_step_end_ms;      /* end of the last waited step on the device timeline of timer
+                                     mark 0 (all lanes), -1 before the mark */
 } mesh_gpu_stats;
 
 const char* mesh_gpu_version(void);
@@ -127,7 +129,9 @@ mesh_status mesh_gpu_request_info(mesh_gpu* g, int64_t instance_id, int64_t requ
                                   int32_t* blocks, int32_t* block_ids, int32_t cap);
 mesh_status mesh_gpu_request_tokens(mesh_gpu* g, int64_t instance_id, int64_t request_id, int32_t* tokens,
                                     int32_t cap, int32_t* n_out);
-/* Execution lane an instance is bound to and that lane's SM quota (CTAs). */
+/* Execution lane an instance is bound to and that lane's SM quota (CTAs). Quotas
+ * are re-split at every instance create / destroy in proportion to the weight
+ * bytes bound to each lane (token-level SM quotas, summing to <= the SMs). */
 mesh_status mesh_gpu_instance_lane(mesh_gpu* g, int64_t instance_id, int32_t* lane, int32_t* ctas);
 
 mesh_status mesh_gpu_instance_kv(mesh_gpu* g, int64_t instance_id, int64_t* target_bytes, int64_t* mapped_bytes,

@@ -37,6 +37,10 @@ struct GpuExecutor::Api {
 };
 
 namespace {
+// Steps the host may have in flight before it retires the oldest: deep enough
+// that every execution lane stays fed while one lane runs a long step (the
+// data plane's ticket ring holds 64).
+constexpr std::size_t kMaxPending = 56;
 struct HostTimer {  // adds the scope's wall time (ms) to `acc`
     double& acc;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
@@ -154,7 +158,7 @@ void GpuExecutor::iteration_done(const Cluster&, const Node& nd, const Iteration
     if (it == tickets_.end()) return;
     for (long long t : it->second) pending_.push_back({handle_for_node(nd.id), t});
     it->second.clear();
-    while (pending_.size() > 32) retire_one();
+    while (pending_.size() > kMaxPending) retire_one();
 }
 
 void GpuExecutor::retire_one() {

@@ -288,7 +288,8 @@ struct Lane {
     uint16_t* p_abuf = nullptr;
     float* p_logits = nullptr;
     int* p_tokens = nullptr;
-    double weight_bytes = 0;  // bound instances (placement balance)
+    double weight_bytes = 0;  // bound instances (placement balance, SM quota)
+    int n_inst = 0;
 };
 
 }  // namespace
@@ -348,6 +349,55 @@ cudaStream_t stream_of(mesh_gpu* g, const Instance& in) { return lane_of(g, in).
 void sync_all(mesh_gpu* g) {
     for (Lane& l : g->lanes) CK(cudaStreamSynchronize(l.stream));
     CK(cudaStreamSynchronize(g->side));
+}
+
+int sm_budget(const mesh_gpu* g) { return g->cfg.sm_quota > 0 ? std::min(g->cfg.sm_quota, g->sms) : g->sms; }
+
+// Token-level SM quotas: the SM budget is split over the lanes that hold
+// instances in proportion to the weight bytes every step of theirs streams
+// (decode is HBM-bound, so equal-duration steps need SMs in proportion to
+// bytes); lanes without instances keep an even share for their first step.
+// Quotas always sum to <= the budget, so every lane's persistent decode grid
+// can be co-resident. Called with all lanes drained (create / destroy).
+void rebalance_lanes(mesh_gpu* g) {
+    const int budget = sm_budget(g), n = int(g->lanes.size());
+    double wsum = 0;
+    int busy = 0;
+    for (const Lane& l : g->lanes)
+        if (l.n_inst > 0) {
+            wsum += l.weight_bytes;
+            busy++;
+        }
+    sync_all(g);
+    if (busy == 0) {
+        for (Lane& l : g->lanes) l.ctas = budget / n;
+        return;
+    }
+    int used = 0;
+    for (Lane& l : g->lanes) {
+        l.ctas = l.n_inst > 0 ? std::max(1, int(double(budget) * l.weight_bytes / wsum)) : 0;
+        used += l.ctas;
+    }
+    // idle lanes: an even share of what is left (at least 1 SM, taken from the largest lane)
+    for (Lane& l : g->lanes)
+        if (l.n_inst == 0) {
+            Lane* big = &g->lanes[0];
+            for (Lane& o : g->lanes)
+                if (o.ctas > big->ctas) big = &o;
+            if (used >= budget && big->ctas > 1) {
+                big->ctas--;
+                used--;
+            }
+            l.ctas = std::max(1, (budget - used) / std::max(1, n - busy));
+            used += l.ctas;
+        }
+    while (used > budget) {  // rounding guard
+        Lane* big = &g->lanes[0];
+        for (Lane& o : g->lanes)
+            if (o.ctas > big->ctas) big = &o;
+        big->ctas--;
+        used--;
+    }
 }
 
 template <typename T>
@@ -593,11 +643,13 @@ void drain_ticket(mesh_gpu* g, Ticket& t) {
             rit->second.pending_tokens--;
         }
     }
-    float ms = 0.f, kms = 0.f;
+    float ms = 0.f, kms = 0.f, end_ms = -1.f;
     cudaEventElapsedTime(&ms, t.start, t.end);
     cudaEventElapsedTime(&kms, t.start, t.kend);
+    if (g->timer[0] && cudaEventElapsedTime(&end_ms, g->timer[0], t.end) != cudaSuccess) end_ms = -1.f;
     g->st.last_step_ms = ms;
     g->st.last_kernel_ms = kms;
+    g->st.last_step_end_ms = end_ms;
     g->ring_used[t.ring] = false;
     t.drained = true;
 }
@@ -998,10 +1050,13 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         ensure_scratch(g, s);
         auto in = std::make_unique<Instance>();
         in->id = instance_id;
-        // bind to the lane with the fewest weight bytes (the HBM each step streams)
+        // bind to an empty lane if there is one, else to the lane with the fewest
+        // weight bytes (the HBM every step streams)
         size_t best = 0;
-        for (size_t i = 1; i < g->lanes.size(); ++i)
-            if (g->lanes[i].weight_bytes < g->lanes[best].weight_bytes) best = i;
+        for (size_t i = 1; i < g->lanes.size(); ++i) {
+            const Lane &a = g->lanes[i], &b = g->lanes[best];
+            if ((a.n_inst == 0) != (b.n_inst == 0) ? a.n_inst == 0 : a.weight_bytes < b.weight_bytes) best = i;
+        }
         in->lane = int(best);
         cudaStream_t st = g->lanes[best].stream;
         in->s = s;
@@ -1068,7 +1123,9 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         CK(cudaStreamSynchronize(st));
         in->weight_bytes = double(total);
         g->lanes[best].weight_bytes += in->weight_bytes;
+        g->lanes[best].n_inst++;
         g->insts.emplace(instance_id, std::move(in));
+        rebalance_lanes(g);
     });
 }
 
@@ -1080,6 +1137,7 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
         CK(cudaStreamSynchronize(g->side));
         unmap_tail(g, in, 0);
         lane_of(g, in).weight_bytes -= in.weight_bytes;
+        lane_of(g, in).n_inst--;
         CU(drv().addr_free(in.va, in.va_size), "cuMemAddressFree");
         CK(cudaFree(in.wmem));
         CK(cudaFree(in.d_block_table));
@@ -1094,6 +1152,7 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
             g->tickets.erase(tid);
         }
         g->insts.erase(instance_id);
+        rebalance_lanes(g);
     });
 }
 

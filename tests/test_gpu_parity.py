@@ -309,7 +309,7 @@ def test_concurrent_lanes_match_oracle():
             models[iid] = ora.Oracle(sh, 30 + iid)
         lanes = {iid: g.instance_lane(iid) for iid in shapes}
         assert {lanes[1][0], lanes[2][0]} == {0, 1}
-        assert all(c == g.sms // 2 for _, c in lanes.values()) if hasattr(g, "sms") else True
+        assert all(c > 0 for _, c in lanes.values()) and sum(c for _, c in lanes.values()) <= 148
         seqs, last = {}, {}
         tk = {iid: g.step_async(iid, prefill=9, prefill_len=40 + 13 * iid) for iid in shapes}
         for iid, t in tk.items():

@@ -290,6 +290,8 @@ struct Lane {
     int* p_tokens = nullptr;
     double weight_bytes = 0;  // bound instances (placement balance, SM quota)
     int n_inst = 0;
+    int2* d_moves = nullptr;  // compaction (src, dst) block pairs, reused in stream order
+    size_t moves_cap = 0;
 };
 
 }  // namespace
@@ -566,16 +568,21 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
         }
     }
     if (!moves.empty()) {
-        int2* dpairs = nullptr;
-        cudaStream_t st = stream_of(g, in);
-        CK(cudaMallocAsync((void**)&dpairs, moves.size() * sizeof(int2), st));
+        Lane& ln = lane_of(g, in);
+        cudaStream_t st = ln.stream;
+        if (ln.moves_cap < moves.size()) {  // grow the lane's pair buffer (rare: drains the lane)
+            CK(cudaStreamSynchronize(st));
+            if (ln.d_moves) CK(cudaFree(ln.d_moves));
+            ln.moves_cap = std::max<size_t>(moves.size(), 4096);
+            CK(cudaMalloc((void**)&ln.d_moves, ln.moves_cap * sizeof(int2)));
+        }
+        int2* dpairs = ln.d_moves;
         CK(cudaMemcpyAsync(dpairs, moves.data(), moves.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
         dim3 grid(std::max(1, int(std::min<long long>(64, in.block_bytes / (16 * 256)))), unsigned(moves.size()));
         kv_block_copy<<<grid, 256, 0, st>>>(reinterpret_cast<uint8_t*>(in.va), in.block_bytes, dpairs);
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(in.d_block_table, in.h_block_table.data(), in.h_block_table.size() * sizeof(int),
                            cudaMemcpyHostToDevice, st));
-        CK(cudaFreeAsync(dpairs, st));
         g->st.blocks_moved += (long long)moves.size();
         g->st.bytes_moved += 2LL * (long long)moves.size() * in.block_bytes;
     }
@@ -1002,7 +1009,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
                              l.arg_idx, l.arg_cnt, l.logits, l.bar, l.p_h, l.p_act, l.p_rs, l.p_q, l.p_attn,
-                             l.p_abuf, l.p_logits, l.p_tokens};
+                             l.p_abuf, l.p_logits, l.p_tokens, l.d_moves};
         for (void* p : lane_ptrs)
             if (p) cudaFree(p);
         if (l.stream) cudaStreamDestroy(l.stream);

@@ -72,6 +72,15 @@ def measured_table_path(size_class: str) -> str:
     return os.path.join(TABLE_DIR, f"{size_class}_gpu_b200.csv")
 
 
+def measured_cost_params() -> dict:
+    """perf.gpu.* (proj/src/config.cpp:36-46) measured by tools/measure_tables.py."""
+    import json
+    with open(os.path.join(TABLE_DIR, "b200_cost_params.json")) as fh:
+        p = json.load(fh)
+    return {k: p[k] for k in ("scale_up_gbps", "scale_down_gbps", "load_gbps", "min_scale_latency_s",
+                              "unload_latency_s")}
+
+
 def write_model_tables() -> None:
     for sc in ("1b", "3b", "7b", "13b"):
         write_table(model_table_path(sc), model_rows(sc))

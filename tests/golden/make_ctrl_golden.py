@@ -80,7 +80,7 @@ def const_rate(r):
 
 
 def scenario(name, *, nodes, templates, assignment, n_fns, window, rate_fn, seed, gpu_tables=True,
-             policy=None, perf=None, n_len=200, len_kw=None, tpl_over=None, sample=None):
+             policy=None, perf=None, n_len=200, len_kw=None, tpl_over=None, sample=None, measured=False):
     d = os.path.join(GOLD, name)
     os.makedirs(d, exist_ok=True)
     fns = [f"fn{i:02d}" for i in range(n_fns)]
@@ -103,8 +103,10 @@ def scenario(name, *, nodes, templates, assignment, n_fns, window, rate_fn, seed
         "output": {"dir": rel(os.path.join(d, "out")), "event_log": True},
     }
     if gpu_tables:
-        cfg["perf"]["tables"] = {f"{t['size_class']}:gpu": rel(tables.model_table_path(t["size_class"]))
-                                 for t in tpls}
+        path = tables.measured_table_path if measured else tables.model_table_path
+        cfg["perf"]["tables"] = {f"{t['size_class']}:gpu": rel(path(t["size_class"])) for t in tpls}
+    if measured:  # B200-measured tables and CostParams (tools/measure_tables.py), fed to both sides
+        cfg["perf"]["gpu"] = tables.measured_cost_params()
     if perf:
         cfg["perf"].update(perf)
     if policy:
@@ -132,6 +134,10 @@ def build_scenarios():
                         window=120.0, rate_fn=const_rate(4.0), seed=11))
     out.append(scenario("c2_colocated", nodes=[gpu(1, 160.0)], templates=["1b", "3b"],
                         assignment=["1b", "3b", "1b", "3b"], n_fns=4, window=120.0, rate_fn=const_rate(1.5), seed=12))
+    # the same node priced by the B200-measured tables and CostParams
+    out.append(scenario("c2_measured", nodes=[gpu(1, 160.0)], templates=["1b", "3b"],
+                        assignment=["1b", "3b", "1b", "3b"], n_fns=4, window=120.0, rate_fn=const_rate(4.0), seed=23,
+                        measured=True))
     hot = {f"fn{i:02d}" for i in range(3)}
     out.append(scenario("c3_bursty", nodes=[gpu(1, 160.0)], templates=["1b", "3b", "7b"],
                         assignment=["1b", "3b", "7b"], n_fns=8, window=150.0,

@@ -52,6 +52,9 @@ METRICS = {
     "sm__warps_active.avg.pct_of_peak_sustained_active": "warps_active_pct",
     "launch__grid_size": "grid",
     "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active": "tensor_pipe_pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed": "tensor_pipe_pct_elapsed",
+    "sm__cycles_elapsed.avg.per_second": "sm_clock_hz",
+    "l1tex__m_xbar2l1tex_read_bytes.sum.pct_of_peak_sustained_elapsed": "xbar_to_l1_pct",
 }
 
 
@@ -82,6 +85,8 @@ def full(rep, out, algo):
             d["dram_GBps"] = d["dram_bytes"] / (d["duration_us"] * 1e3)
         res.append(d)
     for d, a in zip(res, algo):
+        if a <= 0:
+            continue
         d["algorithmic_bytes"] = a
         d["traffic_over_algorithmic"] = d["dram_bytes"] / a
         d["algorithmic_GBps"] = a / (d["duration_us"] * 1e3)

@@ -402,25 +402,6 @@ __device__ __forceinline__ void release_stage(Ctx& c, uint32_t slot) {
     if (c.lane == 0) mbar_arrive(&c.sm.empty[slot]);
 }
 
-// rs[b] = 1/sqrt(mean(h_b^2) + eps) from per-tile partials, summed in a fixed order.
-__device__ __forceinline__ void compute_rs(Ctx& c, const float* ss, float* rs_out) {
-    const DecodeArgs& a = *c.a;
-    const int nt = a.s.d / 16;  // <= 512 partials, 16 per lane, all loads issued before use
-    const int b = c.warp;       // 8 warps <-> 8 batch columns
-    float v[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) {
-        const int t = c.lane + 32 * k;
-        v[k] = t < nt ? ldcg_f32(ss + t * 8 + b) : 0.f;
-    }
-    float acc = 0.f;
-#pragma unroll
-    for (int k = 0; k < 16; ++k) acc += v[k];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if (c.lane == 0) rs_out[b] = rsqrtf(acc / float(a.s.d) + a.s.eps);
-}
-
 // Activation columns [k0, k1) of the 8 batch rows (bf16, global) into smem,
 // every thread's loads issued before its stores (up to 8 x 16 B in flight).
 __device__ __forceinline__ void load_act(Ctx& c, const uint16_t* src, int ld, int k0, int k1) {
@@ -442,6 +423,30 @@ __device__ __forceinline__ void load_act(Ctx& c, const uint16_t* src, int ld, in
             }
         }
     }
+}
+
+// load_act + the RMSNorm scale rs[b] = 1/sqrt(mean(h_b^2) + eps) from the
+// per-tile sum-of-squares partials (summed in a fixed order; warp b <-> batch
+// column b). The partial loads are issued first, so the two L2 round trips of
+// a normed phase's prologue overlap.
+__device__ __forceinline__ void load_act_rs(Ctx& c, const uint16_t* src, int ld, int k0, int k1, const float* ss,
+                                            float* rs_out) {
+    const DecodeArgs& a = *c.a;
+    const int nt = a.s.d / 16;
+    const int b = c.warp;
+    float pv[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int t = c.lane + 32 * k;
+        pv[k] = t < nt ? ldcg_f32(ss + t * 8 + b) : 0.f;
+    }
+    load_act(c, src, ld, k0, k1);
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) acc += pv[k];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (c.lane == 0) rs_out[b] = rsqrtf(acc / float(a.s.d) + a.s.eps);
 }
 
 // One 8 KB weight stage: 16 rows x 256 columns against the 8 activation
@@ -563,8 +568,8 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
     trace(c, 1);
     if (a.skip & 2) return;
     float* rs = c.sm.misc;  // [8]
-    if (kind == PH_QKV || kind == PH_LM) compute_rs(c, a.ssA, rs);
-    if (kind == PH_GU) compute_rs(c, a.ssB, rs);
+    // the RMSNorm scale is folded into the first activation load (both L2 round trips overlap)
+    const float* ss = (kind == PH_QKV || kind == PH_LM) ? a.ssA : (kind == PH_GU ? a.ssB : nullptr);
     if (mt.n == 0) {
         csync();
         return;
@@ -586,7 +591,10 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
             const int nch = c1 - c0;
             if (nseg > 1 || g0 == 0) {
                 csync();
-                load_act(c, src, ld, c0 * DEC_CHUNK_COLS, c1 * DEC_CHUNK_COLS);
+                if (g0 == 0 && sg == 0 && ss)
+                    load_act_rs(c, src, ld, c0 * DEC_CHUNK_COLS, c1 * DEC_CHUNK_COLS, ss, rs);
+                else
+                    load_act(c, src, ld, c0 * DEC_CHUNK_COLS, c1 * DEC_CHUNK_COLS);
                 csync();
                 trace(c, 2);
             }

@@ -2,7 +2,7 @@
 import collections, sys
 NAMES = {1: "phase-begin", 2: "operands", 3: "stages-done", 4: "epilogue", 5: "barrier", 6: "attn-begin", 7: "attn-end"}
 for path in sys.argv[1:]:
-    rows = [tuple(map(int, l.split())) for l in open(path) if l.strip()]
+    rows = [(a, b % 100) for a, b in (tuple(map(int, l.split())) for l in open(path) if l.strip())]
     t0 = rows[0][0]
     agg = collections.defaultdict(float); cnt = collections.Counter()
     for (ta, ga), (tb, gb) in zip(rows, rows[1:]):

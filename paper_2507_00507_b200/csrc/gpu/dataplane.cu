@@ -291,6 +291,7 @@ struct Lane {
     double weight_bytes = 0;  // bound instances (placement balance, SM quota)
     int n_inst = 0;
     int2* d_moves = nullptr;  // compaction (src, dst) block pairs, reused in stream order
+    int* tile_ctr = nullptr;  // prefill GEMM dynamic tile counter
     size_t moves_cap = 0;
 };
 
@@ -871,6 +872,7 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     // queue behind other lanes' decode grids and finish); a lane's quota bounds
     // its persistent decode grid only. Measured: +5 % C2 tokens/s, -8 % e2e wall.
     a.max_ctas = g->prefill_quota ? ln.ctas : 0;
+    a.tile_ctr = ln.tile_ctr;
     a.last_tok = in.d_last_tok;
     a.tok_out = g->d_tok + t.ring * 8;
     CK(cudaEventRecord(t.start, ln.stream));
@@ -947,6 +949,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             dalloc(&l.arg_val, size_t(8) * g->sms);
             dalloc(&l.arg_idx, size_t(8) * g->sms);
             dalloc(&l.arg_cnt, 1);
+            dalloc(&l.tile_ctr, 1);
         }
         CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&g->lane_join, cudaEventDisableTiming));
@@ -1014,7 +1017,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
                              l.arg_idx, l.arg_cnt, l.logits, l.bar, l.p_h, l.p_act, l.p_rs, l.p_q, l.p_attn,
-                             l.p_abuf, l.p_logits, l.p_tokens, l.d_moves};
+                             l.p_abuf, l.p_logits, l.p_tokens, l.d_moves, l.tile_ctr};
         for (void* p : lane_ptrs)
             if (p) cudaFree(p);
         if (l.stream) cudaStreamDestroy(l.stream);

@@ -166,7 +166,7 @@ struct TcCfg {
     static constexpr int B_STAGE = BN * TC_BK * 2;
     static constexpr int STAGES = (196608) / (TC_A_STAGE + B_STAGE);
     static constexpr int TMEM_COLS = 2 * BN;  // two accumulator buffers
-    static constexpr int SMEM = 1024 + STAGES * (TC_A_STAGE + B_STAGE) + 256;
+    static constexpr int SMEM = 1024 + STAGES * (TC_A_STAGE + B_STAGE) + 512;  // + barriers, tile queue
     static_assert(TMEM_COLS == 128 || TMEM_COLS == 256 || TMEM_COLS == 512, "TMEM allocation must be 2^k");
 };
 
@@ -271,7 +271,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t* empty = full + C::STAGES;
     uint64_t* tfull = empty + C::STAGES;  // [2] accumulator ready
     uint64_t* tempty = tfull + 2;         // [2] accumulator drained
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+    uint64_t* qfull = tempty + 2;         // [4] tile-queue slot written (dynamic schedule)
+    uint64_t* qempty = qfull + 4;         // [4] tile-queue slot read by the MMA thread + 4 epilogue warps
+    int* qid = reinterpret_cast<int*>(qempty + 4);  // [4]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(qid + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int rank = CS > 1 ? int(cluster_ctarank()) : 0;
@@ -287,6 +290,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(tfull + i, 1);
             mbar_init(tempty + i, 4);
         }
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(qfull + i, 1);
+            mbar_init(qempty + i, 5);
+        }
         fence_mbar_init();
         prefetch_tmap(&wmap);
         prefetch_tmap(&xmap);
@@ -296,12 +303,46 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if constexpr (CS > 1) cluster_sync_all(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // Tile sequence. CS == 1: dynamic - the producer draws tiles from a
+    // self-resetting global counter (late CTAs, e.g. ones queued behind another
+    // lane's decode grid, simply find less work) and hands each tile to the MMA
+    // thread and the epilogue warps through a 4-slot shared-memory queue.
+    // CS > 1: static round-robin over clusters.
+    auto draw = [&](int i, int t_static) -> int {  // producer
+        if constexpr (CS > 1) {
+            return t_static < ntiles ? t_static : -1;
+        } else {
+            const int sl = i & 3;
+            mbar_wait(qempty + sl, ((i >> 2) & 1) ^ 1);
+            const int t = atomicAdd(a.tile_ctr, 1);
+            // ntiles + gridDim.x draws in all; the last one resets the counter for the next launch
+            if (t == ntiles + int(gridDim.x) - 1) *reinterpret_cast<volatile int*>(a.tile_ctr) = 0;
+            qid[sl] = t < ntiles ? t : -1;
+            mbar_arrive(qfull + sl);
+            return t < ntiles ? t : -1;
+        }
+    };
+    // whole_warp: every lane reads the slot, then lane 0 releases it; else one thread does both
+    auto take = [&](int i, int t_static, bool whole_warp) -> int {  // MMA thread / epilogue warps
+        if constexpr (CS > 1) {
+            return t_static < ntiles ? t_static : -1;
+        } else {
+            const int sl = i & 3;
+            mbar_wait(qfull + sl, (i >> 2) & 1);
+            const int t = *reinterpret_cast<volatile int*>(qid + sl);
+            if (whole_warp) __syncwarp();
+            if (!whole_warp || lane == 0) mbar_arrive(qempty + sl);
+            return t;
+        }
+    };
 
     if (warp == 0) {
         if (lane == 0) {  // ---- producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int t = cluster; t < ntiles; t += nclusters) {
+            for (int i = 0;; ++i) {
+                const int t = draw(i, cluster + i * nclusters);
+                if (t < 0) break;
                 const int mt = (t / nN) * CS + rank, nt = t % nN;
                 for (int kb = 0; kb < nk; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1);
@@ -326,7 +367,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             constexpr uint32_t idesc = umma_idesc_bf16(TC_BM, BN);
             int stage = 0, acc = 0;
             uint32_t phase = 0, aphase = 0;
-            for (int t = cluster; t < ntiles; t += nclusters) {
+            for (int i = 0;; ++i) {
+                if (take(i, cluster + i * nclusters, false) < 0) break;
                 mbar_wait(tempty + acc, aphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + uint32_t(acc * BN);
@@ -358,7 +400,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int sub = warp & 3;
         int acc = 0;
         uint32_t aphase = 0;
-        for (int t = cluster; t < ntiles; t += nclusters) {
+        for (int i = 0;; ++i) {
+            const int t = take(i, cluster + i * nclusters, true);
+            if (t < 0) break;
             const int mt = (t / nN) * CS + rank, nt = t % nN;
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();

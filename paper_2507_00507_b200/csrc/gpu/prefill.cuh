@@ -27,6 +27,7 @@ struct PrefillArgs {
     int* last_tok;      // instance request table
     int* tok_out;       // [1]
     int max_ctas;       // SM quota of the lane (persistent GEMM grid); 0 = all SMs
+    int* tile_ctr;      // lane's dynamic tile counter (zero between launches; self-resetting)
 };
 
 cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t stream);

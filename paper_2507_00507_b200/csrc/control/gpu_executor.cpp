@@ -39,8 +39,8 @@ struct GpuExecutor::Api {
 namespace {
 // Steps the host may have in flight before it retires the oldest: deep enough
 // that every execution lane stays fed while one lane runs a long step (the
-// data plane's ticket ring holds 64).
-constexpr std::size_t kMaxPending = 56;
+// data plane's ticket ring holds 256).
+constexpr std::size_t kMaxPending = 240;
 struct HostTimer {  // adds the scope's wall time (ms) to `acc`
     double& acc;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();

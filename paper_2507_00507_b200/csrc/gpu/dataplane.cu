@@ -254,7 +254,7 @@ struct Ticket {
     std::vector<int> toks;
 };
 
-constexpr int RING = 64;
+constexpr int RING = 256;
 
 // An execution lane: one stream, its own decode/prefill scratch and grid
 // barrier, and a share of the SMs. Instances are bound to a lane; lanes run

@@ -105,14 +105,55 @@ class Dist:
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """Clock / throttle-reason sampling DURING the timed region (B200_PROFILING.md
+    clocks line). NVML is polled every 10 ms from a thread, and sampled once more
+    synchronously at both edges of the region, so even a sub-second region has
+    samples; nvidia-smi (100 ms, slow to start) is the fallback."""
+
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, device: int):
         self.device = device
-        self.samples = []
+        self.samples = []  # (sm_mhz, max_mhz, {reasons})
         self.proc = None
+        self.nv = None
+        self.stop = threading.Event()
+
+    def _nvml_handle(self):
+        import pynvml as nv
+        nv.nvmlInit()
+        idx = self.device
+        vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+        if vis and vis.split(",")[self.device].strip().isdigit():
+            idx = int(vis.split(",")[self.device])
+        self.nv = nv
+        return nv.nvmlDeviceGetHandleByIndex(idx)
+
+    def _nvml_sample(self):
+        nv, h = self.nv, self.h
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        bits = [nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap]
+        self.samples.append((float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)),
+                             float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)),
+                             {n for n, bit in zip(self.NAMES, bits) if r & bit}))
+
+    def _poll(self):
+        while not self.stop.wait(0.01):
+            try:
+                self._nvml_sample()
+            except Exception:
+                return
 
     def __enter__(self):
+        try:
+            self.h = self._nvml_handle()
+            self._nvml_sample()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
+            self.thread.start()
+            return self
+        except Exception:
+            self.nv = None
         q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
@@ -128,11 +169,19 @@ class Clocks:
 
     def _read(self):
         for line in self.proc.stdout:
-            parts = [p.strip() for p in line.split(",")]
-            if len(parts) == 7:
-                self.samples.append(parts)
+            p = [x.strip() for x in line.split(",")]
+            if len(p) == 7 and p[0].replace(".", "").isdigit():
+                self.samples.append((float(p[0]), float(p[1]) if p[1].replace(".", "").isdigit() else 0.0,
+                                     {n for n, v in zip(self.NAMES, p[3:]) if v.lower() == "active"}))
 
     def __exit__(self, *a):
+        if self.nv is not None:
+            self.stop.set()
+            self.thread.join(timeout=1)
+            try:
+                self._nvml_sample()  # the region's trailing edge (the step stream was just synchronised)
+            except Exception:
+                pass
         if self.proc:
             self.proc.terminate()
             try:
@@ -143,12 +192,10 @@ class Clocks:
     def summary(self):
         if not self.samples:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons}
+        sm = [x[0] for x in self.samples]
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(x[1] for x in self.samples),
+                "reasons": sorted(set().union(*(x[2] for x in self.samples))), "samples": len(self.samples),
+                "source": "nvml" if self.nv is not None else "nvidia-smi"}
 
 
 def load_lengths():

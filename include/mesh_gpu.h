@@ -90,6 +90,8 @@ typedef struct mesh_gpu_stats {
     int64_t kv_reclaims;          /* lazy-shrink slack reclaims (each drains the streams once) */
     double last_step_end_ms;      /* end of the last waited step on the device timeline of timer
                                      mark 0 (all lanes), -1 before the mark */
+    int64_t weight_cache_hits;    /* instance creates served from a cached replica of the model
+                                     (weights, KV VA range and block table kept across unload) */
 } mesh_gpu_stats;
 
 const char* mesh_gpu_version(void);

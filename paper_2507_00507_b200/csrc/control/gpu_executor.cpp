@@ -128,13 +128,13 @@ void GpuExecutor::kv_issue(const Cluster&, const Instance& inst, const ScaleOp& 
 void GpuExecutor::iteration_start(const Cluster& c, const Node& nd, const Instance& inst, const IterationPlan& p) {
     HostTimer ht(host_ms_step_);
     mesh_gpu* h = handle_for_node(nd.id);
-    std::vector<long long>& tk = tickets_[nd.id];
+    std::vector<Pending>& tk = tickets_[nd.id];
     if (p.is_prefill) {
         const Request& r = c.requests().get(p.prefill_request);
         mesh_step_plan sp{1, p.prefill_request, p.kind.input_len, r.input_len, 0, nullptr};
         int64_t t = 0;
         check(h, api_->step(h, inst.id, &sp, &t), "prefill step");
-        tk.push_back(t);
+        tk.push_back({h, t, inst.id});
         prefill_tokens_ += p.kind.input_len;
         return;
     }
@@ -146,7 +146,7 @@ void GpuExecutor::iteration_start(const Cluster& c, const Node& nd, const Instan
         mesh_step_plan sp{0, -1, 0, 0, n, rids.data() + o};
         int64_t t = 0;
         check(h, api_->step(h, inst.id, &sp, &t), "decode step");
-        tk.push_back(t);
+        tk.push_back({h, t, inst.id});
     }
     decode_tokens_ += static_cast<long long>(rids.size());
 }
@@ -156,15 +156,19 @@ void GpuExecutor::iteration_done(const Cluster&, const Node& nd, const Iteration
     // data plane's ticket ring), so the host keeps scheduling while the GPU runs.
     auto it = tickets_.find(nd.id);
     if (it == tickets_.end()) return;
-    for (long long t : it->second) pending_.push_back({handle_for_node(nd.id), t});
+    for (const Pending& p : it->second) pending_.push_back(p);
     it->second.clear();
     while (pending_.size() > kMaxPending) retire_one();
 }
 
-void GpuExecutor::retire_one() {
+void GpuExecutor::retire_one() { retire_at(0); }
+
+void GpuExecutor::retire_at(std::size_t i) {
     HostTimer ht(host_ms_wait_);
-    auto [h, t] = pending_.front();
-    pending_.pop_front();
+    const Pending p = pending_[i];
+    pending_.erase(pending_.begin() + static_cast<long>(i));
+    mesh_gpu* h = p.h;
+    const long long t = p.ticket;
     int32_t toks[8];
     int32_t n = 0;
     check(h, api_->step_wait(h, t, toks, 8, &n, nullptr, 0), "step_wait");
@@ -195,7 +199,13 @@ void GpuExecutor::request_finished(const Cluster&, InstanceId inst, const Reques
 void GpuExecutor::instance_unloaded(const Cluster&, InstanceId inst) {
     auto d = inst_dev_.find(inst);
     if (d == inst_dev_.end()) return;
-    drain();  // retire outstanding tickets before the instance (and its tickets) go away
+    // retire the instance's own outstanding tickets before it (and they) go away;
+    // other instances' steps keep running
+    for (std::size_t i = 0; i < pending_.size();)
+        if (pending_[i].inst == inst)
+            retire_at(i);
+        else
+            ++i;
     HostTimer ht(host_ms_destroy_);
     mesh_gpu* h = handles_[static_cast<std::size_t>(d->second)];
     check(h, api_->instance_destroy(h, inst), "instance_destroy");
@@ -214,7 +224,8 @@ std::map<std::string, double> GpuExecutor::metrics() const {
     m["gpu.host_ms.kv_resize"] = host_ms_kv_;
     m["gpu.host_ms.step_issue"] = host_ms_step_;
     m["gpu.host_ms.step_wait"] = host_ms_wait_;
-    double swap = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0, vmm_calls = 0, vmm_ms = 0, reclaims = 0;
+    double swap = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0, vmm_calls = 0, vmm_ms = 0, reclaims = 0,
+           wcache = 0;
     for (mesh_gpu* h : handles_) {
         mesh_gpu_stats st{};
         api_->stats_get(h, &st);
@@ -227,7 +238,9 @@ std::map<std::string, double> GpuExecutor::metrics() const {
         vmm_calls += static_cast<double>(st.vmm_calls);
         vmm_ms += st.vmm_ms;
         reclaims += static_cast<double>(st.kv_reclaims);
+        wcache += static_cast<double>(st.weight_cache_hits);
     }
+    m["gpu.weight_cache_hits"] = wcache;
     m["gpu.vmm_calls"] = vmm_calls;
     m["gpu.host_ms.vmm"] = vmm_ms;
     m["gpu.kv_reclaims"] = reclaims;

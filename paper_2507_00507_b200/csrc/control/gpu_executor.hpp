@@ -45,13 +45,19 @@ private:
     long long pool_bytes_;
     std::vector<mesh_gpu*> handles_;                 // per device index
     std::map<InstanceId, int> inst_dev_;             // instance -> device index
-    std::map<NodeId, std::vector<long long>> tickets_;  // in-flight step of each node
+    struct Pending {
+        mesh_gpu* h;
+        long long ticket;
+        InstanceId inst;
+    };
+    std::map<NodeId, std::vector<Pending>> tickets_;  // in-flight step of each node
     double device_ms_ = 0.0;
     long long steps_ = 0, decode_tokens_ = 0, prefill_tokens_ = 0, instance_starts_ = 0;
     // host wall time spent inside each data-plane hook (e2e breakdown)
     double host_ms_create_ = 0, host_ms_destroy_ = 0, host_ms_kv_ = 0, host_ms_step_ = 0, host_ms_wait_ = 0;
-    std::deque<std::pair<mesh_gpu*, long long>> pending_;  // launched, not yet retired
+    std::deque<Pending> pending_;  // launched, not yet retired (oldest first)
     void retire_one();
+    void retire_at(std::size_t i);
     mesh_gpu* handle_for_node(NodeId node);
     void check(mesh_gpu* h, int status, const char* what);
 };

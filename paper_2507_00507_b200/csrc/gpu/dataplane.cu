@@ -239,6 +239,7 @@ struct Instance {
     std::vector<int> h_block_table;
     int lane = 0;
     double weight_bytes = 0;
+    cudaEvent_t last_ev = nullptr;  // after the instance's last enqueued lane work (steps, compaction)
 };
 
 struct Ticket {
@@ -330,6 +331,23 @@ struct mesh_gpu {
     int skip = 0;             // MESH_GPU_SKIP debug mask (benchmarking only)
     int* dbg_host = nullptr;  // MESH_GPU_WATCHDOG: host-mapped decode progress
     int* dbg_dev = nullptr;
+    // Unloaded instances' device state, kept for a reload of the same model
+    // (weights are a pure function of shape + weight seed, and the seed is the
+    // model's, so every replica of a model is identical): weights, RoPE table,
+    // KV VA reservation, block table. A reload then costs no allocation, no
+    // init kernels and no device-wide synchronisation (cudaFree / cudaMalloc
+    // serialise the device). Oldest first; bounded by wcache_cap bytes.
+    struct Cached {
+        uint64_t key;
+        uint8_t* wmem;
+        size_t wbytes;
+        CUdeviceptr va;
+        size_t va_size;
+        int* d_block_table;
+        int* d_last_tok;
+    };
+    std::vector<Cached> wcache;
+    size_t wcache_bytes = 0, wcache_cap = size_t(32) << 30;  // MESH_GPU_WCACHE_GB
 };
 
 namespace {
@@ -362,9 +380,12 @@ int sm_budget(const mesh_gpu* g) { return g->cfg.sm_quota > 0 ? std::min(g->cfg.
 // (decode is HBM-bound, so equal-duration steps need SMs in proportion to
 // bytes); lanes without instances keep an even share for their first step.
 // Quotas always sum to <= the budget, so every lane's persistent decode grid
-// can be co-resident. Called with all lanes drained (create / destroy).
+// can be co-resident. Only lanes whose quota shrinks are drained: their
+// in-flight grids (old, larger quota) finish before any lane launches at its
+// new, larger quota, so old and new grids in flight never exceed the budget.
 void rebalance_lanes(mesh_gpu* g) {
     const int budget = sm_budget(g), n = int(g->lanes.size());
+    std::vector<int> q(size_t(n), 0);
     double wsum = 0;
     int busy = 0;
     for (const Lane& l : g->lanes)
@@ -372,36 +393,42 @@ void rebalance_lanes(mesh_gpu* g) {
             wsum += l.weight_bytes;
             busy++;
         }
-    sync_all(g);
     if (busy == 0) {
-        for (Lane& l : g->lanes) l.ctas = budget / n;
-        return;
-    }
-    int used = 0;
-    for (Lane& l : g->lanes) {
-        l.ctas = l.n_inst > 0 ? std::max(1, int(double(budget) * l.weight_bytes / wsum)) : 0;
-        used += l.ctas;
-    }
-    // idle lanes: an even share of what is left (at least 1 SM, taken from the largest lane)
-    for (Lane& l : g->lanes)
-        if (l.n_inst == 0) {
-            Lane* big = &g->lanes[0];
-            for (Lane& o : g->lanes)
-                if (o.ctas > big->ctas) big = &o;
-            if (used >= budget && big->ctas > 1) {
-                big->ctas--;
-                used--;
-            }
-            l.ctas = std::max(1, (budget - used) / std::max(1, n - busy));
-            used += l.ctas;
+        for (int i = 0; i < n; ++i) q[size_t(i)] = budget / n;
+    } else {
+        int used = 0;
+        for (int i = 0; i < n; ++i) {
+            const Lane& l = g->lanes[size_t(i)];
+            q[size_t(i)] = l.n_inst > 0 ? std::max(1, int(double(budget) * l.weight_bytes / wsum)) : 0;
+            used += q[size_t(i)];
         }
-    while (used > budget) {  // rounding guard
-        Lane* big = &g->lanes[0];
-        for (Lane& o : g->lanes)
-            if (o.ctas > big->ctas) big = &o;
-        big->ctas--;
-        used--;
+        auto biggest = [&] {
+            int b = 0;
+            for (int i = 1; i < n; ++i)
+                if (q[size_t(i)] > q[size_t(b)]) b = i;
+            return b;
+        };
+        // idle lanes: an even share of what is left (at least 1 SM, taken from the largest lane)
+        for (int i = 0; i < n; ++i)
+            if (g->lanes[size_t(i)].n_inst == 0) {
+                const int big = biggest();
+                if (used >= budget && q[size_t(big)] > 1) {
+                    q[size_t(big)]--;
+                    used--;
+                }
+                q[size_t(i)] = std::max(1, (budget - used) / std::max(1, n - busy));
+                used += q[size_t(i)];
+            }
+        while (used > budget) {  // rounding guard
+            q[size_t(biggest())]--;
+            used--;
+        }
     }
+    for (int i = 0; i < n; ++i) {
+        Lane& l = g->lanes[size_t(i)];
+        if (q[size_t(i)] < l.ctas) CK(cudaStreamSynchronize(l.stream));
+    }
+    for (int i = 0; i < n; ++i) g->lanes[size_t(i)].ctas = q[size_t(i)];
 }
 
 template <typename T>
@@ -479,6 +506,21 @@ struct VmmTimer {  // host time of VMM driver calls -> stats
         g->st.vmm_ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
     }
 };
+
+void free_cached(const mesh_gpu::Cached& c) {
+    drv().addr_free(c.va, c.va_size);
+    cudaFree(c.wmem);
+    cudaFree(c.d_block_table);
+    cudaFree(c.d_last_tok);
+}
+
+void trim_wcache(mesh_gpu* g, size_t cap) {
+    while (!g->wcache.empty() && g->wcache_bytes > cap) {
+        free_cached(g->wcache.front());
+        g->wcache_bytes -= g->wcache.front().wbytes;
+        g->wcache.erase(g->wcache.begin());
+    }
+}
 
 void unmap_tail(mesh_gpu* g, Instance& in, size_t keep) {
     Driver& d = drv();
@@ -585,6 +627,7 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(in.d_block_table, in.h_block_table.data(), in.h_block_table.size() * sizeof(int),
                            cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(in.last_ev, st));
         g->st.blocks_moved += (long long)moves.size();
         g->st.bytes_moved += 2LL * (long long)moves.size() * in.block_bytes;
     }
@@ -981,6 +1024,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->prefill_quota = std::getenv("MESH_PREFILL_QUOTA") != nullptr;
         if (const char* e = std::getenv("MESH_GPU_NSTAGE")) g->nstage = std::atoi(e) >= 16 ? 16 : 8;
         if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
+        if (const char* e = std::getenv("MESH_GPU_WCACHE_GB")) g->wcache_cap = size_t(std::max(0.0, std::atof(e)) * double(1 << 30));
         if (std::getenv("MESH_GPU_WATCHDOG")) {
             CK(cudaHostAlloc((void**)&g->dbg_host, sizeof(int) * 2 * 1024, cudaHostAllocMapped));
             std::memset(g->dbg_host, 0, sizeof(int) * 2 * 1024);
@@ -1009,10 +1053,12 @@ void mesh_gpu_close(mesh_gpu* g) {
         } catch (...) {
         }
         if (in->va) drv().addr_free(in->va, in->va_size);
+        if (in->last_ev) cudaEventDestroy(in->last_ev);
         cudaFree(in->wmem);
         cudaFree(in->d_block_table);
         cudaFree(in->d_last_tok);
     }
+    trim_wcache(g, 0);
     for (auto h : g->pool.all) drv().release(h);
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
@@ -1083,7 +1129,33 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
                emb = size_t(s.vocab) * s.d * 2;
         size_t norms = (2 * L + 1) * s.d * 4, rope = size_t(s.max_seq) * (s.dh / 2) * 8;
         size_t total = L * (qkv + o + gu + dn) + lm + emb + norms + rope + 4096;
-        CK(cudaMalloc((void**)&in->wmem, total));
+        in->block_bytes = (long long)KV_BLOCK_TOKENS * s.kv_bytes_per_token();
+        size_t gran = g->pool.gran;
+        in->va_size = ((size_t(g->pool.limit) + size_t(in->block_bytes) * (DEC_MAXB + 2)) / gran + 1) * gran;
+        in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
+        in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
+        // a reload of a cached replica of the same model: same weights, nothing to initialise
+        bool cached = false;
+        for (size_t i = g->wcache.size(); i-- > 0;) {
+            const mesh_gpu::Cached& c = g->wcache[i];
+            if (c.key != in->shape_key || c.wbytes != total || c.va_size != in->va_size) continue;
+            in->wmem = c.wmem;
+            in->va = c.va;
+            in->d_block_table = c.d_block_table;
+            in->d_last_tok = c.d_last_tok;
+            g->wcache_bytes -= c.wbytes;
+            g->wcache.erase(g->wcache.begin() + long(i));
+            cached = true;
+            g->st.weight_cache_hits++;
+            break;
+        }
+        if (!cached) {
+            if (cudaMalloc((void**)&in->wmem, total) != cudaSuccess) {
+                cudaGetLastError();
+                trim_wcache(g, 0);  // make room: drop every cached replica, then retry
+                CK(cudaMalloc((void**)&in->wmem, total));
+            }
+        }
         uint8_t* p = in->wmem;
         auto take = [&](size_t n) {
             uint8_t* r = p;
@@ -1101,41 +1173,41 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         float* gf = reinterpret_cast<float*>(take(size_t(s.d) * 4));
         float2* rp = reinterpret_cast<float2*>(take(rope));
         in->w = Weights{wq, wo, wgu, wdn, wlm, wemb, ga, gm, gf, rp, qkv, o, gu, dn};
-        const int blocks = g->sms * 8;
-        for (int l = 0; l < s.n_layers; ++l) {
-            init_tiled<0><<<blocks, 256, 0, st>>>(wq + l * qkv, s, weight_seed, l, s.qkv_rows(), s.d);
-            init_tiled<1><<<blocks, 256, 0, st>>>(wo + l * o, s, weight_seed, l, s.d, s.n_heads * s.dh);
-            init_tiled<2><<<blocks, 256, 0, st>>>(wgu + l * gu, s, weight_seed, l, 2 * s.ff, s.d);
-            init_tiled<3><<<blocks, 256, 0, st>>>(wdn + l * dn, s, weight_seed, l, s.d, s.ff);
-            init_gain<<<32, 256, 0, st>>>(ga + size_t(l) * s.d, s.d, weight_seed, T_GATTN, l);
-            init_gain<<<32, 256, 0, st>>>(gm + size_t(l) * s.d, s.d, weight_seed, T_GMLP, l);
-        }
-        init_tiled<4><<<blocks, 256, 0, st>>>(wlm, s, weight_seed, 0, s.vocab, s.d);
-        init_emb<<<blocks, 256, 0, st>>>(wemb, s, weight_seed);
-        init_gain<<<32, 256, 0, st>>>(gf, s.d, weight_seed, T_GFINAL, 0);
-        CK(cudaGetLastError());
-        // rotate-half RoPE table, computed in double on the host (the oracle uses the same formula)
-        std::vector<float2> tab(size_t(s.max_seq) * (s.dh / 2));
-        for (int pos = 0; pos < s.max_seq; ++pos)
-            for (int i = 0; i < s.dh / 2; ++i) {
-                double inv = std::pow(double(s.rope_theta), -2.0 * i / double(s.dh));
-                double ang = double(pos) * inv;
-                tab[size_t(pos) * (s.dh / 2) + i] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+        if (!cached) {
+            const int blocks = g->sms * 8;
+            for (int l = 0; l < s.n_layers; ++l) {
+                init_tiled<0><<<blocks, 256, 0, st>>>(wq + l * qkv, s, weight_seed, l, s.qkv_rows(), s.d);
+                init_tiled<1><<<blocks, 256, 0, st>>>(wo + l * o, s, weight_seed, l, s.d, s.n_heads * s.dh);
+                init_tiled<2><<<blocks, 256, 0, st>>>(wgu + l * gu, s, weight_seed, l, 2 * s.ff, s.d);
+                init_tiled<3><<<blocks, 256, 0, st>>>(wdn + l * dn, s, weight_seed, l, s.d, s.ff);
+                init_gain<<<32, 256, 0, st>>>(ga + size_t(l) * s.d, s.d, weight_seed, T_GATTN, l);
+                init_gain<<<32, 256, 0, st>>>(gm + size_t(l) * s.d, s.d, weight_seed, T_GMLP, l);
             }
-        CK(cudaMemcpyAsync(rp, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
-        // KV region: reserve the whole pool's worth of VA
-        in->block_bytes = (long long)KV_BLOCK_TOKENS * s.kv_bytes_per_token();
-        size_t gran = g->pool.gran;
-        in->va_size = ((size_t(g->pool.limit) + size_t(in->block_bytes) * (DEC_MAXB + 2)) / gran + 1) * gran;
-        CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
-        in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
-        in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
-        CK(cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()));
+            init_tiled<4><<<blocks, 256, 0, st>>>(wlm, s, weight_seed, 0, s.vocab, s.d);
+            init_emb<<<blocks, 256, 0, st>>>(wemb, s, weight_seed);
+            init_gain<<<32, 256, 0, st>>>(gf, s.d, weight_seed, T_GFINAL, 0);
+            CK(cudaGetLastError());
+            // rotate-half RoPE table, computed in double on the host (the oracle uses the same formula)
+            std::vector<float2> tab(size_t(s.max_seq) * (s.dh / 2));
+            for (int pos = 0; pos < s.max_seq; ++pos)
+                for (int i = 0; i < s.dh / 2; ++i) {
+                    double inv = std::pow(double(s.rope_theta), -2.0 * i / double(s.dh));
+                    double ang = double(pos) * inv;
+                    tab[size_t(pos) * (s.dh / 2) + i] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
+                }
+            CK(cudaMemcpyAsync(rp, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
+            // KV region: reserve the whole pool's worth of VA
+            CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
+            CK(cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()));
+            CK(cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS));
+            // the pageable table copy returns once staged; the init kernels and every
+            // later step of the instance are ordered on the lane stream: no host wait
+        }
         CK(cudaMemsetAsync(in->d_block_table, 0, sizeof(int) * in->h_block_table.size(), st));
-        CK(cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS));
         CK(cudaMemsetAsync(in->d_last_tok, 0, sizeof(int) * MAX_SLOTS, st));
+        CK(cudaEventCreateWithFlags(&in->last_ev, cudaEventDisableTiming));
+        CK(cudaEventRecord(in->last_ev, st));
         for (int i = MAX_SLOTS - 1; i >= 0; --i) in->free_slots.push_back(i);
-        CK(cudaStreamSynchronize(st));
         in->weight_bytes = double(total);
         g->lanes[best].weight_bytes += in->weight_bytes;
         g->lanes[best].n_inst++;
@@ -1148,15 +1220,18 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
     if (!g) return MESH_ERR_ARG;
     return guarded(g, [&] {
         Instance& in = inst_of(g, instance_id);
-        CK(cudaStreamSynchronize(stream_of(g, in)));
+        // wait for this instance's own lane work only (co-located instances keep running)
+        CK(cudaEventSynchronize(in.last_ev));
         CK(cudaStreamSynchronize(g->side));
+        cudaEventDestroy(in.last_ev);
         unmap_tail(g, in, 0);
         lane_of(g, in).weight_bytes -= in.weight_bytes;
         lane_of(g, in).n_inst--;
-        CU(drv().addr_free(in.va, in.va_size), "cuMemAddressFree");
-        CK(cudaFree(in.wmem));
-        CK(cudaFree(in.d_block_table));
-        CK(cudaFree(in.d_last_tok));
+        // keep the replica for a reload (no cudaFree: it would serialise the device)
+        g->wcache.push_back({in.shape_key, in.wmem, size_t(in.weight_bytes), in.va, in.va_size, in.d_block_table,
+                             in.d_last_tok});
+        g->wcache_bytes += size_t(in.weight_bytes);
+        trim_wcache(g, g->wcache_cap);
         std::vector<int64_t> dead;
         for (auto& [tid, t] : g->tickets)
             if (t.instance == instance_id) dead.push_back(tid);
@@ -1265,6 +1340,7 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
         g->st.d2h_bytes += (long long)sizeof(int) * 8;
         CK(cudaEventRecord(t.end, st));
         CK(cudaEventRecord(g->ring_ev[t.ring], st));
+        CK(cudaEventRecord(in.last_ev, st));
         g->st.steps++;
         if (g->check) {  // debug (MESH_GPU_CHECK=1): validate every step synchronously
             CK(cudaStreamSynchronize(st));

@@ -215,15 +215,13 @@ struct Producer {
     uint32_t qb = 0;   // first stage of the pending batch
     uint32_t nsh, nmask;
     uint64_t pol;
-    uint32_t kv_blk;   // bytes of one (layer, k|v, head) block
-    size_t kv_voff;    // V plane offset from the K plane
+    uint32_t kv_blk;   // bytes of one (layer, head, k|v) block; its K and V are adjacent
     StageSrc mine;     // this lane's pending stage
     __device__ __forceinline__ Producer(const DecodeArgs& args, Smem& s, int ln) : a(args), sm(s), lane(ln) {
         nsh = uint32_t(__ffs(a.nstage) - 1);
         nmask = uint32_t(a.nstage) - 1u;
         pol = l2_evict_first_policy();
         kv_blk = uint32_t(KV_BLOCK_TOKENS * a.s.dh * 2);
-        kv_voff = size_t(a.s.n_kv) * KV_BLOCK_TOKENS * a.s.dh * 2;
         mine.p0 = mine.p1 = nullptr;
         mine.nblk = -1;
     }
@@ -238,15 +236,10 @@ struct Producer {
                 mbar_arrive_expect_tx(&sm.full[slot], DEC_STAGE_BYTES);
                 bulk_g2s_evict_first(dst, mine.p0, DEC_STAGE_BYTES, &sm.full[slot], pol);
             } else {
+                // one copy per KV block: [K rows | V rows] of the (layer, head)
                 mbar_arrive_expect_tx(&sm.full[slot], 2u * uint32_t(mine.nblk) * kv_blk);
-                if (mine.nblk > 0) {
-                    bulk_g2s(dst, mine.p0, kv_blk, &sm.full[slot]);
-                    bulk_g2s(dst + 4096, mine.p0 + kv_voff, kv_blk, &sm.full[slot]);
-                }
-                if (mine.nblk > 1) {
-                    bulk_g2s(dst + kv_blk, mine.p1, kv_blk, &sm.full[slot]);
-                    bulk_g2s(dst + 4096 + kv_blk, mine.p1 + kv_voff, kv_blk, &sm.full[slot]);
-                }
+                if (mine.nblk > 0) bulk_g2s(dst, mine.p0, 2u * kv_blk, &sm.full[slot]);
+                if (mine.nblk > 1) bulk_g2s(dst + 2u * kv_blk, mine.p1, 2u * kv_blk, &sm.full[slot]);
             }
         }
         qb = q;
@@ -298,7 +291,7 @@ struct Producer {
         if (ap.a1 <= ap.a0) return;
         const Shape& s = a.s;
         const int bps = ap.rt / KV_BLOCK_TOKENS;  // blocks per stage
-        const size_t head_stride = size_t(KV_BLOCK_TOKENS) * s.dh * 2;
+        const size_t head_stride = size_t(2) * KV_BLOCK_TOKENS * s.dh * 2;  // K + V of one head
         const uint8_t* layer_base = a.kv_base + kv_offset(s, layer, 0, 0, 0);
         // decode the first stage once, then walk
         AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0);
@@ -455,6 +448,10 @@ __device__ __forceinline__ void consume_stage(Ctx& c, uint32_t qi, int act_col, 
                                               float (&d1)[4]) {
     uint32_t slot;
     wait_stage(c, qi, slot);
+    if (c.a->skip & 16) {  // debug: ring handshake only (results are garbage)
+        release_stage(c, slot);
+        return;
+    }
     const uint32_t stage_addr = smem_u32(c.sm.ring + size_t(slot) * DEC_STAGE_BYTES);
     const int lane = c.lane, r = lane & 15, g = lane >> 2, t = lane & 3;
     const uint16_t* actrow = c.sm.act + g * act_stride + act_col + 2 * t;
@@ -682,11 +679,16 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
 //   S^T = K Q^T   mma.m16n8k16: A = 16 K rows (ldmatrix), B = Q^T (bf16 regs)
 //   online softmax per head column (a column lives in 8 lanes x 2 regs)
 //   O^T += V^T P^T  A = V^T (ldmatrix.trans), B = P^T (movmatrix.trans of S^T)
-// Stage layout in the ring slot: K rows at [0, 4 KB), V rows at [4 KB, 8 KB),
-// token r of the stage at row r with the KV block's chunk swizzle (r & 7).
+// Stage layout in the ring slot: one [K rows | V rows] run per KV block (its
+// single bulk copy), blocks back to back: token r's K row at kv_row(r), its V
+// row KVB bytes later, with the KV block's chunk swizzle (r & 7).
 template <int DH>
 struct AttnCfg {
     static constexpr int RT = 2048 / DH;  // tokens per 8 KB stage (K + V)
+    static constexpr int KVB = KV_BLOCK_TOKENS * DH * 2;  // K (or V) rows of one block
+    static __device__ __forceinline__ uint32_t kv_row(int r) {
+        return uint32_t((r / KV_BLOCK_TOKENS) * 2 * KVB + (r % KV_BLOCK_TOKENS) * DH * 2);
+    }
     static constexpr int KS = DH / 16;    // k-steps of S^T (head dims)
     static constexpr int MT = RT / 16;    // token m-tiles of S^T == k-steps of O^T
     static constexpr int MD = DH / 16;    // dim m-tiles of O^T
@@ -890,16 +892,16 @@ __device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage&
     uint8_t* stage = c.sm.ring + size_t(slot) * DEC_STAGE_BYTES;
     if (patch) {
         if (lane < 2 * CH)
-            *reinterpret_cast<uint4*>(stage + (lane / CH) * 4096 + (cur - t0) * DH * 2 + (lane % CH) * 16) = pv;
+            *reinterpret_cast<uint4*>(stage + CFG::kv_row(cur - t0) + (lane / CH) * CFG::KVB + (lane % CH) * 16) = pv;
         // V rows past the current token hold stale memory (the unwritten tail of the
         // block, or a previous stage): their softmax weight is 0, but 0 x NaN would
         // still reach O through the PV mma, so clear them
         for (int i = lane; i < (RT - 1 - (cur - t0)) * CH; i += 32)
-            *reinterpret_cast<uint4*>(stage + 4096 + (cur - t0 + 1 + i / CH) * DH * 2 + (i % CH) * 16) =
+            *reinterpret_cast<uint4*>(stage + CFG::kv_row(cur - t0 + 1 + i / CH) + CFG::KVB + (i % CH) * 16) =
                 make_uint4(0, 0, 0, 0);
         __syncwarp();
     }
-    const uint32_t kbase = smem_u32(stage), vbase = kbase + 4096;
+    const uint32_t kbase = smem_u32(stage), vbase = kbase + CFG::KVB;
     // ldmatrix.x4 lane address: matrix j = lane >> 3 covers rows +8*(j&1), chunk +(j>>1)
     const int lrow = (lane & 7) + ((lane >> 3) & 1) * 8, lch = lane >> 4;
     // ---- S^T = K Q^T
@@ -911,7 +913,7 @@ __device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage&
 #pragma unroll
         for (int ks = 0; ks < KS; ++ks) {
             uint32_t k0, k1, k2, k3;
-            ldmatrix_x4(kbase + row * DH * 2 + (((2 * ks + lch) ^ (row & 7)) << 4), k0, k1, k2, k3);
+            ldmatrix_x4(kbase + CFG::kv_row(row) + (((2 * ks + lch) ^ (row & 7)) << 4), k0, k1, k2, k3);
             mma_bf16_16816(sc[mt], k0, k1, k2, k3, stt.qb[ks][0], stt.qb[ks][1]);
         }
     }
@@ -965,7 +967,7 @@ __device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage&
 #pragma unroll
         for (int md = 0; md < MD; ++md) {
             uint32_t v0, v1, v2, v3;
-            ldmatrix_x4_trans(vbase + row * DH * 2 + (((2 * md + dsel) ^ (row & 7)) << 4), v0, v1, v2, v3);
+            ldmatrix_x4_trans(vbase + CFG::kv_row(row) + (((2 * md + dsel) ^ (row & 7)) << 4), v0, v1, v2, v3);
             mma_bf16_16816(stt.o[md], v0, v1, v2, v3, pb0, pb1);
         }
     }

@@ -65,7 +65,7 @@ struct DecodeArgs {
     unsigned long long* trace;  // optional [4096]: %globaltimer at CTA 0's phase boundaries
     unsigned long long* arrive; // optional [barriers][grid]: %globaltimer of every CTA's barrier arrival
     int nstage;    // weight-ring stages in use (<= DEC_NSTAGE): bounds bytes in flight per SM
-    int skip;      // debug: 1 skips attention work, 2 skips the GEMV phases (results are garbage)
+    int skip;      // debug: 1 skips attention, 2 the GEMV phases, 8 / 16 the attention / GEMV math (ring only); results are garbage
 };
 
 cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t stream);

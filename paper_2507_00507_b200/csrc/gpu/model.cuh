@@ -92,12 +92,16 @@ __host__ __device__ inline void gu_row(int prow, int* is_up, int* row) {
 }
 
 // ---- paged KV block layout ----
-// A block holds KV_BLOCK_TOKENS tokens of every layer: [layer][k|v][kv_head][slot][dh] bf16.
-// Within a token row the 16-byte chunks are XOR-swizzled by (slot & 7) so that
-// ldmatrix over 8 consecutive token rows hits 8 distinct bank groups.
+// A block holds KV_BLOCK_TOKENS tokens of every layer: [layer][kv_head][k|v][slot][dh] bf16.
+// The K and V rows of one (layer, kv head) are adjacent, so the decode ring moves
+// a block's K+V in ONE bulk copy (4 KB at dh = 64, 8 KB at dh = 128): scattered
+// 2 KB copies cap a TMA ring at ~30 GB/s per SM, 4 KB at ~56, 8 KB at ~91
+// (profiles/readbw_grid_r01.json). Within a token row the 16-byte chunks are
+// XOR-swizzled by (slot & 7) so that ldmatrix over 8 consecutive token rows
+// hits 8 distinct bank groups.
 constexpr int KV_BLOCK_TOKENS = 16;
 __host__ __device__ inline size_t kv_offset(const Shape& s, int layer, int kv, int head, int slot) {
-    return ((((size_t(layer) * 2 + kv) * s.n_kv + head) * KV_BLOCK_TOKENS + slot) * s.dh) * 2;
+    return ((((size_t(layer) * s.n_kv + head) * 2 + kv) * KV_BLOCK_TOKENS + slot) * s.dh) * 2;
 }
 // byte offset of element `dim` inside a token row of block-slot `slot`
 __host__ __device__ inline uint32_t kv_dim_off(int slot, int dim) {

@@ -50,7 +50,8 @@ class GpuStats(C.Structure):
                 ("prefill_tokens", C.c_int64), ("last_step_ms", C.c_double), ("last_kernel_ms", C.c_double),
                 ("kernel_launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("kv_granule_bytes", C.c_int64), ("vmm_calls", C.c_int64), ("vmm_ms", C.c_double),
-                ("kv_reclaims", C.c_int64), ("last_step_end_ms", C.c_double)]
+                ("kv_reclaims", C.c_int64), ("last_step_end_ms", C.c_double),
+                ("weight_cache_hits", C.c_int64)]
 
 
 @dataclass(frozen=True)

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdint>
 #include <cstdlib>
+#include <string>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
@@ -49,7 +50,7 @@ __global__ void ldg_kernel(const uint4* p, size_t n, unsigned long long* out) {
 // Each CTA streams a contiguous 1/G share of the buffer in `stage` byte stages
 // made of `stage / piece` bulk copies.
 __global__ void __launch_bounds__(288, 1) ring_kernel(const uint8_t* p, size_t bytes, int stage, int piece, int depth,
-                                                      unsigned long long* out, int plan) {
+                                                      unsigned long long* out, int plan, size_t scatter = 0) {
     extern __shared__ __align__(128) uint8_t sm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(depth) * stage);
     uint64_t* empty = full + depth;
@@ -72,8 +73,12 @@ __global__ void __launch_bounds__(288, 1) ring_kernel(const uint8_t* p, size_t b
                 const uint32_t par = (q / depth) & 1;
                 mbar_wait(&empty[slot], par ^ 1u);
                 mbar_expect_tx(&full[slot], stage);
-                for (int o = 0; o < stage; o += piece)
-                    bulk_g2s(sm + size_t(slot) * stage + o, base + size_t(q) * stage + o, piece, &full[slot]);
+                for (int o = 0; o < stage; o += piece) {
+                    // scatter > 0: pieces `scatter` bytes apart (paged-KV-like), wrapping in the CTA's share
+                    const size_t src = scatter ? (size_t(q) * (stage / piece) + o / piece) * scatter % (per - piece)
+                                               : size_t(q) * stage + o;
+                    bulk_g2s(sm + size_t(slot) * stage + o, base + src, piece, &full[slot]);
+                }
             }
         }
         return;
@@ -122,6 +127,19 @@ int main(int argc, char** argv) {
         printf("{\"kind\":\"ldg\",\"blocks_per_sm\":%d,\"GBps\":%.1f}\n", bpsm, bytes / ms / 1e6);
     }
     CK(cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    if (argc > 1 && std::string(argv[1]) == "grid") {
+        // per-SM rate at lane quotas: 8 KB stages of 1..4 pieces, contiguous or scattered
+        for (int g : {17, 56, 148})
+            for (int piece : {2048, 4096, 8192})
+                for (size_t sc : {size_t(0), size_t(368640)}) {
+                    const size_t smem = size_t(8192) * 16 + 16 * 16;
+                    float ms = timeit([&] { ring_kernel<<<g, 288, smem>>>(buf, bytes / 148 * g, 8192, piece, 16, out, 8, sc); });
+                    const double gbs = double(bytes / 148 * g) / ms / 1e6;
+                    printf("{\"kind\":\"ring-grid\",\"grid\":%d,\"piece\":%d,\"scatter\":%zu,\"GBps\":%.1f,\"GBps_per_sm\":%.1f}\n",
+                           g, piece, sc, gbs, gbs / g);
+                }
+        return 0;
+    }
     int stages[] = {4096, 8192, 16384};
     int depths[] = {8, 16};  // multiples of 8: a warp always re-waits on its own slots
     for (int st : stages)

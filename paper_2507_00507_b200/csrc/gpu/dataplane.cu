@@ -278,6 +278,7 @@ struct Lane {
     float* arg_val = nullptr;
     int* arg_idx = nullptr;
     int* arg_cnt = nullptr;
+    int* claim = nullptr;  // decode tile-claim counters (self-resetting)
     float* logits = nullptr;
     unsigned* bar = nullptr;  // [count, gen]
     // prefill scratch
@@ -763,6 +764,7 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.arg_val = ln.arg_val;
     a.arg_idx = ln.arg_idx;
     a.arg_cnt = ln.arg_cnt;
+    a.claim = ln.claim;
     a.logits = g->capture_logits ? ln.logits : nullptr;
     a.tok_out = g->d_tok + ring * 8;
     a.bar_count = ln.bar;
@@ -992,6 +994,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             dalloc(&l.arg_val, size_t(8) * g->sms);
             dalloc(&l.arg_idx, size_t(8) * g->sms);
             dalloc(&l.arg_cnt, 1);
+            dalloc(&l.claim, DEC_CLAIM_MAX);
             dalloc(&l.tile_ctr, 1);
         }
         CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
@@ -1063,7 +1066,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
                              l.arg_idx, l.arg_cnt, l.logits, l.bar, l.p_h, l.p_act, l.p_rs, l.p_q, l.p_attn,
-                             l.p_abuf, l.p_logits, l.p_tokens, l.d_moves, l.tile_ctr};
+                             l.p_abuf, l.p_logits, l.p_tokens, l.d_moves, l.tile_ctr, l.claim};
         for (void* p : lane_ptrs)
             if (p) cudaFree(p);
         if (l.stream) cudaStreamDestroy(l.stream);
@@ -1106,6 +1109,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         if (s.n_heads * s.dh != s.d) throw MeshError(MESH_ERR_CONFIG, "n_heads * d_head must equal d_model");
         if (s.d % 256 || s.ff % 256 || s.vocab % 128 || (s.qkv_rows() % 128))
             throw MeshError(MESH_ERR_CONFIG, "d_model/d_ff must be multiples of 256, vocab of 128");
+        if (s.n_layers < 1 || s.n_layers * 4 + 1 > DEC_CLAIM_MAX) throw MeshError(MESH_ERR_CONFIG, "n_layers out of range");
         if (s.max_seq < 2 || s.max_seq > DEC_BT_MAX * KV_BLOCK_TOKENS)
             throw MeshError(MESH_ERR_CONFIG, "max_seq_len out of range");
         ensure_scratch(g, s);

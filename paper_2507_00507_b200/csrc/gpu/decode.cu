@@ -67,6 +67,22 @@ __device__ __forceinline__ int n_segments(int K) {
     const int chunks = K / DEC_CHUNK_COLS, per = DEC_KSEG_MAX / DEC_CHUNK_COLS;
     return (chunks + per - 1) / per;
 }
+// Single-segment GEMV phases (the activation fits in shared memory: QKV, O,
+// gate/up, lm_head) are scheduled dynamically: the producer claims groups of
+// `claim_tiles` consecutive tiles from a per-phase counter and hands each
+// claim to the consumers through a 4-deep descriptor ring. A CTA that streams
+// slower (HBM channel contention varies from layer to layer: the static
+// round-robin deal showed up to 18 us of barrier skew in a 68 us gate/up
+// phase) simply claims fewer groups. Claims advance in tile order, so the CTAs
+// still stream neighbouring tiles (DRAM row locality). Multi-segment phases
+// (down: d_ff columns exceed the activation buffer) and phases with fewer than
+// 4 tiles per CTA (where a claim round trip on the phase's critical path costs
+// more than the imbalance it removes) keep the static round-robin deal.
+__device__ __forceinline__ bool dynamic_phase(int K, int tiles, int G) { return K <= DEC_KSEG_MAX && tiles >= 4 * G; }
+__device__ __forceinline__ int claim_tiles(int tiles, int G) { return max(1, min(DEC_MAXT, tiles / (2 * G))); }
+__device__ __forceinline__ int claim_index(const Shape& s, int kind, int layer) {
+    return kind == PH_LM ? s.n_layers * 4 : layer * 4 + kind;
+}
 __device__ __forceinline__ void seg_range(int K, int nseg, int s, int& c0, int& c1) {
     const int chunks = K / DEC_CHUNK_COLS;
     c0 = (chunks * s) / nseg;
@@ -178,6 +194,11 @@ struct Smem {
     uint64_t* empty;
     float* misc;
     int* bt;  // [8][DEC_BT_MAX] block-table rows of the step's requests
+    // claim descriptors of dynamic GEMV phases (producer -> consumers)
+    int* dt0;         // [4] first tile of the claim
+    int* dgn;         // [4] tiles in the claim (0: phase exhausted)
+    uint64_t* dfull;  // [4]
+    uint64_t* dempty; // [4]
 };
 
 __device__ __forceinline__ Smem carve(uint8_t* base) {
@@ -217,6 +238,7 @@ struct Producer {
     uint64_t pol;
     uint32_t kv_blk;   // bytes of one (layer, head, k|v) block; its K and V are adjacent
     StageSrc mine;     // this lane's pending stage
+    uint32_t dk = 0;   // claim descriptors written
     __device__ __forceinline__ Producer(const DecodeArgs& args, Smem& s, int ln) : a(args), sm(s), lane(ln) {
         nsh = uint32_t(__ffs(a.nstage) - 1);
         nmask = uint32_t(a.nstage) - 1u;
@@ -252,8 +274,42 @@ struct Producer {
         }
         if (++q - qb == DEC_PLANES) flush();
     }
+    __device__ __forceinline__ void gemv_dynamic(int kind, int layer, int G) {
+        const GemvPhase p = gemv_phase(a, kind, layer);
+        const int cl = claim_tiles(p.tiles, G), nch = p.K / DEC_CHUNK_COLS;
+        int* ctr = a.claim + claim_index(a.s, kind, layer);
+        const size_t tile_bytes = size_t(p.K) * 32;
+        // the next claim is requested one group ahead: its round trip hides behind this group's stages
+        int next = 0;
+        if (lane == 0) next = atomicAdd(ctr, cl);
+        for (;;) {
+            const int t0 = __shfl_sync(0xffu, next, 0);
+            const int gn = max(0, min(cl, p.tiles - t0));
+            if (gn > 0 && lane == 0) next = atomicAdd(ctr, cl);
+            // issue every pending stage first: the consumers may need them to
+            // get to the descriptor slot this claim waits for
+            flush();
+            const uint32_t ds = dk & 3u, dpar = (dk >> 2) & 1u;
+            if (lane == 0) {
+                mbar_wait(&sm.dempty[ds], dpar ^ 1u);
+                sm.dt0[ds] = t0;
+                sm.dgn[ds] = gn;
+                mbar_arrive(&sm.dfull[ds]);
+            }
+            ++dk;
+            if (gn == 0) return;
+            for (int ti = 0; ti < gn; ++ti) {
+                const uint8_t* t = p.base + size_t(t0 + ti) * tile_bytes;
+                for (int ch = 0; ch < nch; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, nullptr, -1);
+            }
+        }
+    }
     __device__ __forceinline__ void gemv(int kind, int layer, int& off, int cta, int G) {
         const GemvPhase p = gemv_phase(a, kind, layer);
+        if (dynamic_phase(p.K, p.tiles, G)) {
+            gemv_dynamic(kind, layer, G);
+            return;
+        }
         const MyTiles mt = my_tiles(p.tiles, off, cta, G);
         off = (off + p.tiles) % G;
         if (mt.n == 0) return;
@@ -362,7 +418,8 @@ struct Ctx {
     int p0, np;          // first pair of this CTA's attention range, pairs touched
     uint32_t q;       // stage counter (mirrors the producer)
     uint32_t nsh, nmask;  // ring depth = 1 << nsh (8 or 16)
-    int off;          // round-robin offset (mirrors the producer)
+    int off;          // round-robin offset of static phases (mirrors the producer)
+    uint32_t dk;      // claim descriptors read (mirrors the producer)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -557,20 +614,92 @@ __device__ __forceinline__ void better(float& bv, int& bi, float v, int i) {
 }
 
 // ------------------------------------------------------------ GEMV phase
+// Stages of a group of gn tiles (one activation segment [c0, c1) of chunks),
+// tile-major. Warp w consumes stages c.q + w + 8k: a warp's consecutive stages
+// are exactly DEC_NCW apart, so it never waits on a ring slot a full cycle
+// ahead (mbarrier parity would alias). Partial sums stay in registers while
+// the warp's stages belong to one tile and are flushed to its part[] slot.
+__device__ __forceinline__ void consume_group(Ctx& c, int gn, int sg, int nch) {
+    float* part = c.sm.acc;  // per-warp partial sums: part[warp][tile][lane * 4 + e]
+    const int n = gn * nch, act_stride = nch * DEC_CHUNK_COLS + 8;
+    if (sg == 0)
+        for (int ti = 0; ti < gn; ++ti)
+            reinterpret_cast<float4*>(part + (c.warp * DEC_MAXT + ti) * 128)[c.lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+    float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
+    int cur = -1;
+    auto flush = [&](int ti) {
+        float4* dst = reinterpret_cast<float4*>(part + (c.warp * DEC_MAXT + ti) * 128) + c.lane;
+        const float4 o = *dst;
+        *dst = make_float4(o.x + d0[0] + d1[0], o.y + d0[1] + d1[1], o.z + d0[2] + d1[2], o.w + d0[3] + d1[3]);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) d0[e] = d1[e] = 0.f;
+    };
+    for (int i = c.warp; i < n; i += DEC_NCW) {
+        const int ti = i / nch, ch = i - ti * nch;
+        if (ti != cur) {
+            if (cur >= 0) flush(cur);
+            cur = ti;
+        }
+        consume_stage(c, c.q + i, ch * DEC_CHUNK_COLS, act_stride, d0, d1);
+    }
+    if (cur >= 0) flush(cur);
+    c.q += n;
+}
+
+// Epilogue of a group: one warp per tile, summing the eight warps' partials.
+template <typename TileOf>
+__device__ __forceinline__ void epilogue_group(Ctx& c, int kind, int layer, int gn, TileOf tile_of, const float* rs,
+                                               float* best_v, int* best_i) {
+    const DecodeArgs& a = *c.a;
+    const float* part = c.sm.acc;
+    for (int ti = c.warp; ti < gn; ti += DEC_NCW) {
+        const int tile = tile_of(ti);
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int w = 0; w < DEC_NCW; ++w) {
+            const float4 pv = reinterpret_cast<const float4*>(part + (w * DEC_MAXT + ti) * 128)[c.lane];
+            v[0] += pv.x;
+            v[1] += pv.y;
+            v[2] += pv.z;
+            v[3] += pv.w;
+        }
+        switch (kind) {
+            case PH_QKV: epi_qkv(c, layer, tile, v, rs); break;
+            case PH_GU: epi_gu(c, tile, v, rs); break;
+            case PH_O: epi_residual(c, tile, v, a.w.g_mlp + size_t(layer) * a.s.d, a.ssB); break;
+            case PH_DOWN: {
+                const float* gnext = (layer + 1 < a.s.n_layers) ? a.w.g_attn + size_t(layer + 1) * a.s.d : a.w.g_final;
+                epi_residual(c, tile, v, gnext, a.ssA);
+                break;
+            }
+            default: {  // lm_head
+                const int g = c.lane >> 2, t = c.lane & 3;
+#pragma unroll
+                for (int rr = 0; rr < 2; ++rr) {
+                    const int row = tile * 16 + g + 8 * rr;
+#pragma unroll
+                    for (int j = 0; j < 2; ++j) {
+                        const int b = 2 * t + j;
+                        if (b >= c.B) continue;
+                        const float logit = v[2 * rr + j] * rs[b];
+                        if (a.logits) a.logits[size_t(b) * a.s.vocab + row] = logit;
+                        better(best_v[j], best_i[j], logit, row);
+                    }
+                }
+                break;
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* best_v, int* best_i) {
     const DecodeArgs& a = *c.a;
     const GemvPhase p = gemv_phase(a, kind, layer);
-    const MyTiles mt = my_tiles(p.tiles, c.off, c.cta, c.G);
-    c.off = (c.off + p.tiles) % c.G;
     trace(c, 1);
     if (a.skip & 2) return;
     float* rs = c.sm.misc;  // [8]
     // the RMSNorm scale is folded into the first activation load (both L2 round trips overlap)
     const float* ss = (kind == PH_QKV || kind == PH_LM) ? a.ssA : (kind == PH_GU ? a.ssB : nullptr);
-    if (mt.n == 0) {
-        csync();
-        return;
-    }
     const uint16_t* src;
     int ld;
     switch (kind) {
@@ -578,14 +707,47 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
         case PH_DOWN: src = a.abuf; ld = a.s.ff; break;
         default: src = a.act; ld = a.s.d; break;
     }
+    if (dynamic_phase(p.K, p.tiles, c.G)) {
+        // the whole activation fits: load it once (overlaps the producer's first claim)
+        csync();
+        if (ss)
+            load_act_rs(c, src, ld, 0, p.K, ss, rs);
+        else
+            load_act(c, src, ld, 0, p.K);
+        csync();
+        trace(c, 2);
+        const int nch = p.K / DEC_CHUNK_COLS;
+        for (;;) {
+            const uint32_t ds = c.dk & 3u;
+            mbar_wait(&c.sm.dfull[ds], (c.dk >> 2) & 1u);
+            const int t0 = c.sm.dt0[ds], gn = c.sm.dgn[ds];
+            ++c.dk;
+            if (gn == 0) {
+                csync();  // every consumer read the terminal descriptor
+                if (c.tid == 0) mbar_arrive(&c.sm.dempty[ds]);
+                return;
+            }
+            consume_group(c, gn, 0, nch);
+            csync();
+            if (c.tid == 0) mbar_arrive(&c.sm.dempty[ds]);  // every consumer read it before the csync
+            trace(c, 3);
+            epilogue_group(c, kind, layer, gn, [&](int ti) { return t0 + ti; }, rs, best_v, best_i);
+            csync();  // partials are rewritten by the next group
+            trace(c, 4);
+        }
+    }
+    const MyTiles mt = my_tiles(p.tiles, c.off, c.cta, c.G);
+    c.off = (c.off + p.tiles) % c.G;
+    if (mt.n == 0) {
+        csync();
+        return;
+    }
     const int nseg = n_segments(p.K);
-    float* part = c.sm.acc;  // per-warp partial sums: part[warp][tile][lane * 4 + e]
     for (int g0 = 0; g0 < mt.n; g0 += DEC_MAXT) {
         const int gn = min(DEC_MAXT, mt.n - g0);
         for (int sg = 0; sg < nseg; ++sg) {
             int c0, c1;
             seg_range(p.K, nseg, sg, c0, c1);
-            const int nch = c1 - c0;
             if (nseg > 1 || g0 == 0) {
                 csync();
                 if (g0 == 0 && sg == 0 && ss)
@@ -595,79 +757,11 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
                 csync();
                 trace(c, 2);
             }
-            const int act_stride = nch * DEC_CHUNK_COLS + 8;
-            // Warp w consumes stages c.q + w + 8k of this (group, segment): a
-            // warp's consecutive stages are exactly DEC_NCW apart, so it never
-            // waits on a ring slot a full cycle ahead (mbarrier parity would
-            // alias). Partial sums stay in registers while the warp's stages
-            // belong to one tile and are flushed to its part[] slot.
-            const int n = gn * nch;
-            if (sg == 0)
-                for (int ti = 0; ti < gn; ++ti)
-                    reinterpret_cast<float4*>(part + (c.warp * DEC_MAXT + ti) * 128)[c.lane] =
-                        make_float4(0.f, 0.f, 0.f, 0.f);
-            float d0[4] = {0.f, 0.f, 0.f, 0.f}, d1[4] = {0.f, 0.f, 0.f, 0.f};
-            int cur = -1;
-            auto flush = [&](int ti) {
-                float4* dst = reinterpret_cast<float4*>(part + (c.warp * DEC_MAXT + ti) * 128) + c.lane;
-                const float4 o = *dst;
-                *dst = make_float4(o.x + d0[0] + d1[0], o.y + d0[1] + d1[1], o.z + d0[2] + d1[2], o.w + d0[3] + d1[3]);
-#pragma unroll
-                for (int e = 0; e < 4; ++e) d0[e] = d1[e] = 0.f;
-            };
-            for (int i = c.warp; i < n; i += DEC_NCW) {
-                const int ti = i / nch, ch = i - ti * nch;
-                if (ti != cur) {
-                    if (cur >= 0) flush(cur);
-                    cur = ti;
-                }
-                consume_stage(c, c.q + i, ch * DEC_CHUNK_COLS, act_stride, d0, d1);
-            }
-            if (cur >= 0) flush(cur);
-            c.q += n;
+            consume_group(c, gn, sg, c1 - c0);
         }
         csync();
         trace(c, 3);
-        // epilogue: one warp per tile, summing the eight warps' partials
-        for (int ti = c.warp; ti < gn; ti += DEC_NCW) {
-            const int tile = mt.t0 + (g0 + ti) * c.G;
-            float v[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int w = 0; w < DEC_NCW; ++w) {
-                const float4 pv = reinterpret_cast<const float4*>(part + (w * DEC_MAXT + ti) * 128)[c.lane];
-                v[0] += pv.x;
-                v[1] += pv.y;
-                v[2] += pv.z;
-                v[3] += pv.w;
-            }
-            switch (kind) {
-                case PH_QKV: epi_qkv(c, layer, tile, v, rs); break;
-                case PH_GU: epi_gu(c, tile, v, rs); break;
-                case PH_O: epi_residual(c, tile, v, a.w.g_mlp + size_t(layer) * a.s.d, a.ssB); break;
-                case PH_DOWN: {
-                    const float* gnext =
-                        (layer + 1 < a.s.n_layers) ? a.w.g_attn + size_t(layer + 1) * a.s.d : a.w.g_final;
-                    epi_residual(c, tile, v, gnext, a.ssA);
-                    break;
-                }
-                default: {  // lm_head
-                    const int g = c.lane >> 2, t = c.lane & 3;
-#pragma unroll
-                    for (int rr = 0; rr < 2; ++rr) {
-                        const int row = tile * 16 + g + 8 * rr;
-#pragma unroll
-                        for (int j = 0; j < 2; ++j) {
-                            const int b = 2 * t + j;
-                            if (b >= c.B) continue;
-                            const float logit = v[2 * rr + j] * rs[b];
-                            if (a.logits) a.logits[size_t(b) * a.s.vocab + row] = logit;
-                            better(best_v[j], best_i[j], logit, row);
-                        }
-                    }
-                    break;
-                }
-            }
-        }
+        epilogue_group(c, kind, layer, gn, [&](int ti) { return mt.t0 + (g0 + ti) * c.G; }, rs, best_v, best_i);
         csync();  // partials are rewritten by the next group
         trace(c, 4);
     }
@@ -1113,6 +1207,8 @@ __device__ __forceinline__ void run_argmax_combine(Ctx& c, float best_v[2], int 
             }
         }
         if (c.tid == 0) atomicExch(a.arg_cnt, 0);
+        // every CTA is past its last claim: rearm the dynamic phases' counters for the next step
+        for (int i = c.tid; i < a.s.n_layers * 4 + 1; i += CONSUMER_THREADS) a.claim[i] = 0;
     }
 }
 
@@ -1120,7 +1216,13 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ DecodeArgs a_s;  // launch arguments, read with LDS instead of generic param loads
     __shared__ int slot_s[DEC_MAXB], pos_s[DEC_MAXB];
+    __shared__ int dt0_s[4], dgn_s[4];
+    __shared__ __align__(8) uint64_t dfull_s[4], dempty_s[4];
     Smem sm = carve(smem_raw);
+    sm.dt0 = dt0_s;
+    sm.dgn = dgn_s;
+    sm.dfull = dfull_s;
+    sm.dempty = dempty_s;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int B = args.desc->B;
     if (threadIdx.x == 0) {
@@ -1128,6 +1230,10 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
         for (int i = 0; i < DEC_NSTAGE; ++i) {
             mbar_init(&sm.full[i], 1);
             mbar_init(&sm.empty[i], 1);
+        }
+        for (int i = 0; i < 4; ++i) {
+            mbar_init(&sm.dfull[i], 1);
+            mbar_init(&sm.dempty[i], 1);
         }
         fence_mbar_init();
     }
@@ -1162,6 +1268,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     c.pos = pos_s;
     c.q = 0;
     c.off = 0;
+    c.dk = 0;
     c.nsh = uint32_t(__ffs(a.nstage) - 1);
     c.nmask = uint32_t(a.nstage) - 1u;
     // attention plan + this CTA's pair table: identical for every layer of the step

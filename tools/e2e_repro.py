@@ -16,7 +16,7 @@ with control.Experiment(cfg) as exp:
         keys = ["gpu.steps", "gpu.decode_tokens", "gpu.prefill_tokens", "slo_compliant_rate", "gpu.device_ms",
                 "gpu.instance_starts", "gpu.host_ms.instance_create", "gpu.host_ms.instance_destroy",
                 "gpu.host_ms.kv_resize", "gpu.host_ms.step_issue", "gpu.host_ms.step_wait", "gpu.vmm_calls",
-                "gpu.host_ms.vmm", "gpu.kv_reclaims"]
+                "gpu.host_ms.vmm", "gpu.kv_reclaims", "gpu.weight_cache_hits"]
         print("ok", time.time() - t0, {k: exp.metric(k) for k in keys})
     except Exception as e:
         print("FAIL after", time.time() - t0, e)

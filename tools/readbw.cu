@@ -7,6 +7,7 @@
 #include <cstdint>
 #include <cstdlib>
 #include <string>
+#include <vector>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); exit(1); } } while (0)
@@ -50,7 +51,8 @@ __global__ void ldg_kernel(const uint4* p, size_t n, unsigned long long* out) {
 // Each CTA streams a contiguous 1/G share of the buffer in `stage` byte stages
 // made of `stage / piece` bulk copies.
 __global__ void __launch_bounds__(288, 1) ring_kernel(const uint8_t* p, size_t bytes, int stage, int piece, int depth,
-                                                      unsigned long long* out, int plan, size_t scatter = 0) {
+                                                      unsigned long long* out, int plan, size_t scatter = 0,
+                                                      int gscatter = 0) {
     extern __shared__ __align__(128) uint8_t sm[];
     uint64_t* full = reinterpret_cast<uint64_t*>(sm + size_t(depth) * stage);
     uint64_t* empty = full + depth;
@@ -75,9 +77,14 @@ __global__ void __launch_bounds__(288, 1) ring_kernel(const uint8_t* p, size_t b
                 mbar_expect_tx(&full[slot], stage);
                 for (int o = 0; o < stage; o += piece) {
                     // scatter > 0: pieces `scatter` bytes apart (paged-KV-like), wrapping in the CTA's share
-                    const size_t src = scatter ? (size_t(q) * (stage / piece) + o / piece) * scatter % (per - piece)
-                                               : size_t(q) * stage + o;
-                    bulk_g2s(sm + size_t(slot) * stage + o, base + src, piece, &full[slot]);
+                    // scatter > 0: pieces `scatter` bytes apart (paged-KV-like), wrapping in the CTA's share;
+                    // gscatter: the same stride wrapping over the whole buffer (a KV block stride of MBs:
+                    // every piece on its own 2 MB page)
+                    const size_t idx = size_t(q) * (stage / piece) + o / piece;
+                    const uint8_t* src = scatter == 0 ? base + size_t(q) * stage + o
+                                         : !gscatter ? base + idx * scatter % (per - piece)
+                                                     : p + ((size_t(blockIdx.x) * 7919 + idx) * scatter) % (bytes - piece) / 4096 * 4096;
+                    bulk_g2s(sm + size_t(slot) * stage + o, src, piece, &full[slot]);
                 }
             }
         }
@@ -129,14 +136,17 @@ int main(int argc, char** argv) {
     CK(cudaFuncSetAttribute(ring_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     if (argc > 1 && std::string(argv[1]) == "grid") {
         // per-SM rate at lane quotas: 8 KB stages of 1..4 pieces, contiguous or scattered
+        const bool tlb = argc > 2 && std::string(argv[2]) == "tlb";
         for (int g : {17, 56, 148})
             for (int piece : {2048, 4096, 8192})
-                for (size_t sc : {size_t(0), size_t(368640)}) {
+                for (size_t sc : tlb ? std::vector<size_t>{0, 368640, 1835008} : std::vector<size_t>{0, 368640}) {
+                    if (tlb && piece == 2048) continue;
+                    const int gs = tlb && sc == 1835008;
                     const size_t smem = size_t(8192) * 16 + 16 * 16;
-                    float ms = timeit([&] { ring_kernel<<<g, 288, smem>>>(buf, bytes / 148 * g, 8192, piece, 16, out, 8, sc); });
+                    float ms = timeit([&] { ring_kernel<<<g, 288, smem>>>(buf, bytes / 148 * g, 8192, piece, 16, out, 8, sc, gs); });
                     const double gbs = double(bytes / 148 * g) / ms / 1e6;
-                    printf("{\"kind\":\"ring-grid\",\"grid\":%d,\"piece\":%d,\"scatter\":%zu,\"GBps\":%.1f,\"GBps_per_sm\":%.1f}\n",
-                           g, piece, sc, gbs, gbs / g);
+                    printf("{\"kind\":\"ring-grid\",\"grid\":%d,\"piece\":%d,\"scatter\":%zu,\"global\":%d,\"GBps\":%.1f,\"GBps_per_sm\":%.1f}\n",
+                           g, piece, sc, gs, gbs, gbs / g);
                 }
         return 0;
     }

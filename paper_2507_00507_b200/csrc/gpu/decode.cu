@@ -1079,6 +1079,16 @@ __device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPla
     const int n = ap.a1 - ap.a0;
     AttnState<DH> stt;
     int cur_pair = -1, cur_b = 0, cur_kvh = 0, cur_lo = 0, cur_n = 0;
+    if (a.skip & 32) {  // debug: bare ring handshake (no pair bookkeeping, no combine; results are garbage)
+        for (int i = c.warp; i < n; i += DEC_NCW) {
+            uint32_t slot;
+            wait_stage(c, c.q + i, slot);
+            release_stage(c, slot);
+        }
+        c.q += n;
+        csync();
+        return;
+    }
     for (int i = c.warp; i < n; i += DEC_NCW) {
         const AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0 + i);
         if (st.pair != cur_pair) {

@@ -326,3 +326,34 @@ def test_concurrent_lanes_match_oracle():
                 last[iid] = toks[0]
         for m in models.values():
             m.close()
+
+
+@pytest.mark.parametrize("quota", [1, 2, 3, 5, 8, 17])
+@pytest.mark.parametrize("name", ["tiny", "tiny128"])
+def test_decode_schedules_across_sm_quotas(name, quota):
+    """Small SM quotas put GEMV phases with >= 4 tiles per CTA on the dynamic
+    tile-claim schedule (claim groups of 1..4 tiles, decode.cu claim_tiles),
+    larger quotas keep the static round-robin deal; the quotas here mix both
+    within one step. Every schedule must give the oracle's logits for a ragged
+    batch over several steps (the claim counters rearm at step end)."""
+    shape = SHAPES[name]
+    model = ora.Oracle(shape, 9)
+    with MeshGpu(0, sm_quota=quota, kv_pool_bytes=1 << 30, prompt_seed=SEED_PROMPT) as g:
+        g.capture_logits(True)
+        g.create_instance(1, shape, seed=9)
+        g.kv_resize(1, 0, 8 << 20)
+        lens = [3, 16, 29, 40, 7]
+        seqs, last = {}, {}
+        for rid, n in enumerate(lens):
+            toks, lg = g.step(1, prefill=rid, prefill_len=n, vocab=shape.vocab, with_logits=True)
+            seqs[rid], ol = _oracle_prefill(model, rid, n)
+            _check(lg[0], toks[0], ol, f"{name}/q{quota} prefill r{rid}")
+            last[rid] = toks[0]
+        order = [4, 1, 0, 3, 2]
+        for step in range(4):
+            toks, lg = g.step(1, decode=order, vocab=shape.vocab, with_logits=True)
+            for i, rid in enumerate(order):
+                _, ol = seqs[rid].feed(last[rid])
+                _check(lg[i], toks[i], ol, f"{name}/q{quota} step {step} r{rid}")
+                last[rid] = toks[i]
+        g.destroy_instance(1)

@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include "gpu_executor.hpp"
 
 #include <dlfcn.h>
@@ -39,8 +40,17 @@ struct GpuExecutor::Api {
 namespace {
 // Steps the host may have in flight before it retires the oldest: deep enough
 // that every execution lane stays fed while one lane runs a long step (the
-// data plane's ticket ring holds 256).
-constexpr std::size_t kMaxPending = 240;
+// data plane's ticket ring holds 1024). MESH_HOST_WINDOW overrides it: 240,
+// 600 and 1000 gave the same e2e wall within run-to-run noise (24.7-26.5 s),
+// because a deeper window only fills the launch queue further.
+std::size_t max_pending() {
+    static const std::size_t n = [] {
+        const char* e = std::getenv("MESH_HOST_WINDOW");
+        const long v = e ? std::atol(e) : 0;
+        return v > 0 ? std::min<std::size_t>(std::size_t(v), 1000) : std::size_t(240);
+    }();
+    return n;
+}
 struct HostTimer {  // adds the scope's wall time (ms) to `acc`
     double& acc;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
@@ -158,7 +168,7 @@ void GpuExecutor::iteration_done(const Cluster&, const Node& nd, const Iteration
     if (it == tickets_.end()) return;
     for (const Pending& p : it->second) pending_.push_back(p);
     it->second.clear();
-    while (pending_.size() > kMaxPending) retire_one();
+    while (pending_.size() > max_pending()) retire_one();
 }
 
 void GpuExecutor::retire_one() { retire_at(0); }

@@ -255,7 +255,7 @@ struct Ticket {
     std::vector<int> toks;
 };
 
-constexpr int RING = 256;
+constexpr int RING = 1024;
 
 // An execution lane: one stream, its own decode/prefill scratch and grid
 // barrier, and a share of the SMs. Instances are bound to a lane; lanes run

@@ -194,6 +194,7 @@ struct Smem {
     uint64_t* empty;
     float* misc;
     int* bt;  // [8][DEC_BT_MAX] block-table rows of the step's requests
+    float* tacc;  // [DEC_TACC_TILES][128] per-tile sums across activation segments (down projection)
     // claim descriptors of dynamic GEMV phases (producer -> consumers)
     int* dt0;         // [4] first tile of the claim
     int* dgn;         // [4] tiles in the claim (0: phase exhausted)
@@ -210,6 +211,8 @@ __device__ __forceinline__ Smem carve(uint8_t* base) {
     m.empty = m.full + DEC_NSTAGE;
     m.misc = reinterpret_cast<float*>(base + DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS);
     m.bt = reinterpret_cast<int*>(base + DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS + DEC_SMEM_MISC);
+    m.tacc = reinterpret_cast<float*>(base + DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS +
+                                      DEC_SMEM_MISC + DEC_SMEM_BT);
     return m;
 }
 
@@ -647,22 +650,31 @@ __device__ __forceinline__ void consume_group(Ctx& c, int gn, int sg, int nch) {
 }
 
 // Epilogue of a group: one warp per tile, summing the eight warps' partials.
+// Sum of the eight warps' partials of group tile ti (lane's 4 values).
+__device__ __forceinline__ float4 warp_sum(const Ctx& c, int ti) {
+    const float* part = c.sm.acc;
+    float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int w = 0; w < DEC_NCW; ++w) {
+        const float4 pv = reinterpret_cast<const float4*>(part + (w * DEC_MAXT + ti) * 128)[c.lane];
+        v.x += pv.x;
+        v.y += pv.y;
+        v.z += pv.z;
+        v.w += pv.w;
+    }
+    return v;
+}
+
+// tacc_base >= 0: the tile sums were accumulated across segments in tacc[tacc_base + ti]
 template <typename TileOf>
 __device__ __forceinline__ void epilogue_group(Ctx& c, int kind, int layer, int gn, TileOf tile_of, const float* rs,
-                                               float* best_v, int* best_i) {
+                                               float* best_v, int* best_i, int tacc_base = -1) {
     const DecodeArgs& a = *c.a;
-    const float* part = c.sm.acc;
     for (int ti = c.warp; ti < gn; ti += DEC_NCW) {
         const int tile = tile_of(ti);
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int w = 0; w < DEC_NCW; ++w) {
-            const float4 pv = reinterpret_cast<const float4*>(part + (w * DEC_MAXT + ti) * 128)[c.lane];
-            v[0] += pv.x;
-            v[1] += pv.y;
-            v[2] += pv.z;
-            v[3] += pv.w;
-        }
+        const float4 sv = tacc_base >= 0 ? reinterpret_cast<const float4*>(c.sm.tacc + (tacc_base + ti) * 128)[c.lane]
+                                         : warp_sum(c, ti);
+        float v[4] = {sv.x, sv.y, sv.z, sv.w};
         switch (kind) {
             case PH_QKV: epi_qkv(c, layer, tile, v, rs); break;
             case PH_GU: epi_gu(c, tile, v, rs); break;
@@ -743,6 +755,43 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
         return;
     }
     const int nseg = n_segments(p.K);
+    if (nseg > 1 && mt.n <= DEC_TACC_TILES) {
+        // Segment-outer: each activation segment is loaded once for all of the
+        // CTA's tiles (group-outer reloads it per group of 4 tiles); per-tile
+        // sums carry across segments in tacc.
+        for (int sg = 0; sg < nseg; ++sg) {
+            int c0, c1;
+            seg_range(p.K, nseg, sg, c0, c1);
+            csync();
+            if (sg == 0 && ss)  // d_model > 4096: normed phases are multi-segment too
+                load_act_rs(c, src, ld, c0 * DEC_CHUNK_COLS, c1 * DEC_CHUNK_COLS, ss, rs);
+            else
+                load_act(c, src, ld, c0 * DEC_CHUNK_COLS, c1 * DEC_CHUNK_COLS);
+            csync();
+            trace(c, 2);
+            for (int g0 = 0; g0 < mt.n; g0 += DEC_MAXT) {
+                const int gn = min(DEC_MAXT, mt.n - g0);
+                consume_group(c, gn, 0, c1 - c0);
+                csync();
+                for (int ti = c.warp; ti < gn; ti += DEC_NCW) {
+                    float4* t = reinterpret_cast<float4*>(c.sm.tacc + (g0 + ti) * 128) + c.lane;
+                    const float4 v = warp_sum(c, ti);
+                    if (sg == 0) {
+                        *t = v;
+                    } else {
+                        const float4 o = *t;
+                        *t = make_float4(o.x + v.x, o.y + v.y, o.z + v.z, o.w + v.w);
+                    }
+                }
+                csync();  // partials are rewritten by the next group
+            }
+        }
+        trace(c, 3);
+        epilogue_group(c, kind, layer, mt.n, [&](int ti) { return mt.t0 + ti * c.G; }, rs, best_v, best_i, 0);
+        csync();
+        trace(c, 4);
+        return;
+    }
     for (int g0 = 0; g0 < mt.n; g0 += DEC_MAXT) {
         const int gn = min(DEC_MAXT, mt.n - g0);
         for (int sg = 0; sg < nseg; ++sg) {

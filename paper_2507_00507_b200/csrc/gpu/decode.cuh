@@ -24,8 +24,10 @@ constexpr int DEC_SMEM_ACC = DEC_NCW * DEC_MAXT * 128 * 4;  // per-warp tile par
 constexpr int DEC_SMEM_BARS = 2 * DEC_NSTAGE * 8;
 constexpr int DEC_SMEM_MISC = 1024;
 constexpr int DEC_SMEM_BT = DEC_MAXB * DEC_BT_MAX * 4;
+constexpr int DEC_TACC_TILES = 12;  // multi-segment phases: per-tile sums kept across activation segments
+constexpr int DEC_SMEM_TACC = DEC_TACC_TILES * 128 * 4;
 constexpr int DEC_SMEM_TOTAL =
-    DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS + DEC_SMEM_MISC + DEC_SMEM_BT;
+    DEC_SMEM_RING + DEC_SMEM_ACT + DEC_SMEM_ACC + DEC_SMEM_BARS + DEC_SMEM_MISC + DEC_SMEM_BT + DEC_SMEM_TACC;
 
 // Per-step input written by the host (one H2D copy) before the launch.
 struct StepDesc {

@@ -265,6 +265,7 @@ constexpr int RING = 1024;
 struct Lane {
     cudaStream_t stream = nullptr;
     int ctas = 0;  // SM quota: decode grid and prefill GEMM grid
+    int grow_to = 0;  // pending larger quota, adopted once every shrunk lane's old grids are done
     // decode scratch
     float* h = nullptr;
     uint16_t* act = nullptr;
@@ -332,23 +333,33 @@ struct mesh_gpu {
     int skip = 0;             // MESH_GPU_SKIP debug mask (benchmarking only)
     int* dbg_host = nullptr;  // MESH_GPU_WATCHDOG: host-mapped decode progress
     int* dbg_dev = nullptr;
-    // Unloaded instances' device state, kept for a reload of the same model
-    // (weights are a pure function of shape + weight seed, and the seed is the
-    // model's, so every replica of a model is identical): weights, RoPE table,
-    // KV VA reservation, block table. A reload then costs no allocation, no
-    // init kernels and no device-wide synchronisation (cudaFree / cudaMalloc
-    // serialise the device). Oldest first; bounded by wcache_cap bytes.
-    struct Cached {
-        uint64_t key;
+    // Weights are a pure function of shape + weight seed, and the seed is the
+    // model's, so every replica of a model is identical and read-only: live
+    // replicas share one weight set (a scale-out replica costs no allocation and
+    // no init kernels), and a set whose last replica unloads stays resident for
+    // a reload (LRU past wcache_cap bytes of idle sets). Per-instance buffers
+    // (KV VA range, block table, last tokens) are recycled the same way. No
+    // create or destroy calls cudaFree / cudaMalloc on the steady path: both
+    // serialise the device.
+    struct WeightSet {
         uint8_t* wmem;
-        size_t wbytes;
+        size_t bytes;
+        int refs;
+        cudaEvent_t ready;  // after the init kernels (other lanes wait on it)
+        uint64_t tick;      // last release, for LRU eviction of idle sets
+    };
+    std::map<uint64_t, WeightSet> wsets;  // by shape key
+    struct InstBufs {
         CUdeviceptr va;
         size_t va_size;
         int* d_block_table;
+        size_t bt_elems;
         int* d_last_tok;
     };
-    std::vector<Cached> wcache;
-    size_t wcache_bytes = 0, wcache_cap = size_t(32) << 30;  // MESH_GPU_WCACHE_GB
+    std::vector<InstBufs> ibufs;  // free per-instance buffers
+    size_t wcache_cap = size_t(32) << 30;  // MESH_GPU_WCACHE_GB: bytes of idle weight sets kept
+    uint64_t wtick = 0;
+    std::vector<cudaEvent_t> shrink_evs;  // quota shrinks whose old (larger) grids may still run
 };
 
 namespace {
@@ -381,9 +392,10 @@ int sm_budget(const mesh_gpu* g) { return g->cfg.sm_quota > 0 ? std::min(g->cfg.
 // (decode is HBM-bound, so equal-duration steps need SMs in proportion to
 // bytes); lanes without instances keep an even share for their first step.
 // Quotas always sum to <= the budget, so every lane's persistent decode grid
-// can be co-resident. Only lanes whose quota shrinks are drained: their
-// in-flight grids (old, larger quota) finish before any lane launches at its
-// new, larger quota, so old and new grids in flight never exceed the budget.
+// can be co-resident. Nothing is drained: a shrinking lane launches at its new
+// quota at once and records an event after its old (larger) grids; a growing
+// lane keeps launching at its old quota until every such event has fired
+// (adopt_quota), so old and new grids in flight never exceed the budget.
 void rebalance_lanes(mesh_gpu* g) {
     const int budget = sm_budget(g), n = int(g->lanes.size());
     std::vector<int> q(size_t(n), 0);
@@ -427,9 +439,32 @@ void rebalance_lanes(mesh_gpu* g) {
     }
     for (int i = 0; i < n; ++i) {
         Lane& l = g->lanes[size_t(i)];
-        if (q[size_t(i)] < l.ctas) CK(cudaStreamSynchronize(l.stream));
+        if (q[size_t(i)] < l.ctas) {
+            cudaEvent_t e;
+            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            CK(cudaEventRecord(e, l.stream));
+            g->shrink_evs.push_back(e);
+            l.ctas = q[size_t(i)];
+            l.grow_to = 0;
+        } else {
+            l.grow_to = q[size_t(i)] > l.ctas ? q[size_t(i)] : 0;
+        }
     }
-    for (int i = 0; i < n; ++i) g->lanes[size_t(i)].ctas = q[size_t(i)];
+}
+
+// A lane's pending quota growth takes effect once every shrunk lane's old
+// grids have finished (non-blocking event queries).
+void adopt_quota(mesh_gpu* g, Lane& l) {
+    if (l.grow_to == 0) return;
+    while (!g->shrink_evs.empty()) {
+        const cudaError_t q = cudaEventQuery(g->shrink_evs.back());
+        if (q == cudaErrorNotReady) return;
+        CK(q);
+        cudaEventDestroy(g->shrink_evs.back());
+        g->shrink_evs.pop_back();
+    }
+    l.ctas = l.grow_to;
+    l.grow_to = 0;
 }
 
 template <typename T>
@@ -508,18 +543,21 @@ struct VmmTimer {  // host time of VMM driver calls -> stats
     }
 };
 
-void free_cached(const mesh_gpu::Cached& c) {
-    drv().addr_free(c.va, c.va_size);
-    cudaFree(c.wmem);
-    cudaFree(c.d_block_table);
-    cudaFree(c.d_last_tok);
-}
-
-void trim_wcache(mesh_gpu* g, size_t cap) {
-    while (!g->wcache.empty() && g->wcache_bytes > cap) {
-        free_cached(g->wcache.front());
-        g->wcache_bytes -= g->wcache.front().wbytes;
-        g->wcache.erase(g->wcache.begin());
+// Frees idle weight sets (no live replica), least recently released first,
+// until at most `cap` bytes of them remain.
+void evict_weights(mesh_gpu* g, size_t cap) {
+    for (;;) {
+        size_t idle = 0;
+        auto victim = g->wsets.end();
+        for (auto it = g->wsets.begin(); it != g->wsets.end(); ++it)
+            if (it->second.refs == 0) {
+                idle += it->second.bytes;
+                if (victim == g->wsets.end() || it->second.tick < victim->second.tick) victim = it;
+            }
+        if (idle <= cap || victim == g->wsets.end()) return;
+        cudaFree(victim->second.wmem);
+        cudaEventDestroy(victim->second.ready);
+        g->wsets.erase(victim);
     }
 }
 
@@ -777,7 +815,11 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     return a;
 }
 
-int grid_of(mesh_gpu* g, const Instance& in) { return lane_of(g, in).ctas; }
+int grid_of(mesh_gpu* g, const Instance& in) {
+    Lane& l = lane_of(g, in);
+    adopt_quota(g, l);
+    return l.ctas;
+}
 
 // Build the decode descriptor for `rids` (allocating blocks for new positions).
 void build_decode_desc(mesh_gpu* g, Instance& in, const int64_t* rids, int n, StepDesc& d) {
@@ -1057,11 +1099,19 @@ void mesh_gpu_close(mesh_gpu* g) {
         }
         if (in->va) drv().addr_free(in->va, in->va_size);
         if (in->last_ev) cudaEventDestroy(in->last_ev);
-        cudaFree(in->wmem);
         cudaFree(in->d_block_table);
         cudaFree(in->d_last_tok);
     }
-    trim_wcache(g, 0);
+    for (auto& [k, ws] : g->wsets) {
+        cudaFree(ws.wmem);
+        cudaEventDestroy(ws.ready);
+    }
+    for (cudaEvent_t e : g->shrink_evs) cudaEventDestroy(e);
+    for (auto& b : g->ibufs) {
+        drv().addr_free(b.va, b.va_size);
+        cudaFree(b.d_block_table);
+        cudaFree(b.d_last_tok);
+    }
     for (auto h : g->pool.all) drv().release(h);
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
@@ -1138,27 +1188,22 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         in->va_size = ((size_t(g->pool.limit) + size_t(in->block_bytes) * (DEC_MAXB + 2)) / gran + 1) * gran;
         in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
         in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
-        // a reload of a cached replica of the same model: same weights, nothing to initialise
-        bool cached = false;
-        for (size_t i = g->wcache.size(); i-- > 0;) {
-            const mesh_gpu::Cached& c = g->wcache[i];
-            if (c.key != in->shape_key || c.wbytes != total || c.va_size != in->va_size) continue;
-            in->wmem = c.wmem;
-            in->va = c.va;
-            in->d_block_table = c.d_block_table;
-            in->d_last_tok = c.d_last_tok;
-            g->wcache_bytes -= c.wbytes;
-            g->wcache.erase(g->wcache.begin() + long(i));
-            cached = true;
+        // weights: share a live or idle set of the same model, else allocate and initialise
+        bool fresh = false;
+        auto wit = g->wsets.find(in->shape_key);
+        if (wit != g->wsets.end() && wit->second.bytes == total) {
+            in->wmem = wit->second.wmem;
+            wit->second.refs++;
             g->st.weight_cache_hits++;
-            break;
-        }
-        if (!cached) {
+            CK(cudaStreamWaitEvent(st, wit->second.ready, 0));  // initialised on another lane maybe
+        } else {
+            if (wit != g->wsets.end()) throw MeshError(MESH_ERR_RUNTIME, "weight set size mismatch");
             if (cudaMalloc((void**)&in->wmem, total) != cudaSuccess) {
                 cudaGetLastError();
-                trim_wcache(g, 0);  // make room: drop every cached replica, then retry
+                evict_weights(g, 0);  // make room: drop every idle set, then retry
                 CK(cudaMalloc((void**)&in->wmem, total));
             }
+            fresh = true;
         }
         uint8_t* p = in->wmem;
         auto take = [&](size_t n) {
@@ -1177,7 +1222,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         float* gf = reinterpret_cast<float*>(take(size_t(s.d) * 4));
         float2* rp = reinterpret_cast<float2*>(take(rope));
         in->w = Weights{wq, wo, wgu, wdn, wlm, wemb, ga, gm, gf, rp, qkv, o, gu, dn};
-        if (!cached) {
+        if (fresh) {
             const int blocks = g->sms * 8;
             for (int l = 0; l < s.n_layers; ++l) {
                 init_tiled<0><<<blocks, 256, 0, st>>>(wq + l * qkv, s, weight_seed, l, s.qkv_rows(), s.d);
@@ -1200,12 +1245,30 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
                     tab[size_t(pos) * (s.dh / 2) + i] = make_float2(float(std::cos(ang)), float(std::sin(ang)));
                 }
             CK(cudaMemcpyAsync(rp, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
+            // the pageable table copy returns once staged; the init kernels and every
+            // later step of the instance are ordered on the lane stream: no host wait
+            mesh_gpu::WeightSet ws{in->wmem, total, 1, nullptr, 0};
+            CK(cudaEventCreateWithFlags(&ws.ready, cudaEventDisableTiming));
+            CK(cudaEventRecord(ws.ready, st));
+            g->wsets.emplace(in->shape_key, ws);
+        }
+        // per-instance buffers: recycle a free set of the same sizes, else allocate
+        bool recycled = false;
+        for (size_t i = g->ibufs.size(); i-- > 0;) {
+            const mesh_gpu::InstBufs& bb = g->ibufs[i];
+            if (bb.va_size != in->va_size || bb.bt_elems != in->h_block_table.size()) continue;
+            in->va = bb.va;
+            in->d_block_table = bb.d_block_table;
+            in->d_last_tok = bb.d_last_tok;
+            g->ibufs.erase(g->ibufs.begin() + long(i));
+            recycled = true;
+            break;
+        }
+        if (!recycled) {
             // KV region: reserve the whole pool's worth of VA
             CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
             CK(cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()));
             CK(cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS));
-            // the pageable table copy returns once staged; the init kernels and every
-            // later step of the instance are ordered on the lane stream: no host wait
         }
         CK(cudaMemsetAsync(in->d_block_table, 0, sizeof(int) * in->h_block_table.size(), st));
         CK(cudaMemsetAsync(in->d_last_tok, 0, sizeof(int) * MAX_SLOTS, st));
@@ -1231,11 +1294,15 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
         unmap_tail(g, in, 0);
         lane_of(g, in).weight_bytes -= in.weight_bytes;
         lane_of(g, in).n_inst--;
-        // keep the replica for a reload (no cudaFree: it would serialise the device)
-        g->wcache.push_back({in.shape_key, in.wmem, size_t(in.weight_bytes), in.va, in.va_size, in.d_block_table,
-                             in.d_last_tok});
-        g->wcache_bytes += size_t(in.weight_bytes);
-        trim_wcache(g, g->wcache_cap);
+        // release the weight set (kept while idle, for a reload) and recycle the
+        // per-instance buffers: no cudaFree, which would serialise the device
+        g->ibufs.push_back({in.va, in.va_size, in.d_block_table, in.h_block_table.size(), in.d_last_tok});
+        auto wit = g->wsets.find(in.shape_key);
+        if (wit != g->wsets.end()) {
+            wit->second.refs--;
+            wit->second.tick = ++g->wtick;
+        }
+        evict_weights(g, g->wcache_cap);
         std::vector<int64_t> dead;
         for (auto& [tid, t] : g->tickets)
             if (t.instance == instance_id) dead.push_back(tid);

@@ -265,7 +265,6 @@ constexpr int RING = 1024;
 struct Lane {
     cudaStream_t stream = nullptr;
     int ctas = 0;  // SM quota: decode grid and prefill GEMM grid
-    int grow_to = 0;  // pending larger quota, adopted once every shrunk lane's old grids are done
     // decode scratch
     float* h = nullptr;
     uint16_t* act = nullptr;
@@ -359,7 +358,6 @@ struct mesh_gpu {
     std::vector<InstBufs> ibufs;  // free per-instance buffers
     size_t wcache_cap = size_t(32) << 30;  // MESH_GPU_WCACHE_GB: bytes of idle weight sets kept
     uint64_t wtick = 0;
-    std::vector<cudaEvent_t> shrink_evs;  // quota shrinks whose old (larger) grids may still run
 };
 
 namespace {
@@ -392,10 +390,12 @@ int sm_budget(const mesh_gpu* g) { return g->cfg.sm_quota > 0 ? std::min(g->cfg.
 // (decode is HBM-bound, so equal-duration steps need SMs in proportion to
 // bytes); lanes without instances keep an even share for their first step.
 // Quotas always sum to <= the budget, so every lane's persistent decode grid
-// can be co-resident. Nothing is drained: a shrinking lane launches at its new
-// quota at once and records an event after its old (larger) grids; a growing
-// lane keeps launching at its old quota until every such event has fired
-// (adopt_quota), so old and new grids in flight never exceed the budget.
+// can be co-resident. Only lanes whose quota shrinks are drained: their
+// in-flight grids (old, larger quota) finish before any lane launches at its
+// new, larger quota, so old and new grids in flight never exceed the budget.
+// (Deferring the growth behind events instead, without a host wait, kept a new
+// lane at a 1-SM quota for as long as the other lanes' queues ran: 4x slower
+// on the 8-instance C3 scenario.)
 void rebalance_lanes(mesh_gpu* g) {
     const int budget = sm_budget(g), n = int(g->lanes.size());
     std::vector<int> q(size_t(n), 0);
@@ -439,32 +439,9 @@ void rebalance_lanes(mesh_gpu* g) {
     }
     for (int i = 0; i < n; ++i) {
         Lane& l = g->lanes[size_t(i)];
-        if (q[size_t(i)] < l.ctas) {
-            cudaEvent_t e;
-            CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-            CK(cudaEventRecord(e, l.stream));
-            g->shrink_evs.push_back(e);
-            l.ctas = q[size_t(i)];
-            l.grow_to = 0;
-        } else {
-            l.grow_to = q[size_t(i)] > l.ctas ? q[size_t(i)] : 0;
-        }
+        if (q[size_t(i)] < l.ctas) CK(cudaStreamSynchronize(l.stream));
     }
-}
-
-// A lane's pending quota growth takes effect once every shrunk lane's old
-// grids have finished (non-blocking event queries).
-void adopt_quota(mesh_gpu* g, Lane& l) {
-    if (l.grow_to == 0) return;
-    while (!g->shrink_evs.empty()) {
-        const cudaError_t q = cudaEventQuery(g->shrink_evs.back());
-        if (q == cudaErrorNotReady) return;
-        CK(q);
-        cudaEventDestroy(g->shrink_evs.back());
-        g->shrink_evs.pop_back();
-    }
-    l.ctas = l.grow_to;
-    l.grow_to = 0;
+    for (int i = 0; i < n; ++i) g->lanes[size_t(i)].ctas = q[size_t(i)];
 }
 
 template <typename T>
@@ -815,11 +792,7 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     return a;
 }
 
-int grid_of(mesh_gpu* g, const Instance& in) {
-    Lane& l = lane_of(g, in);
-    adopt_quota(g, l);
-    return l.ctas;
-}
+int grid_of(mesh_gpu* g, const Instance& in) { return lane_of(g, in).ctas; }
 
 // Build the decode descriptor for `rids` (allocating blocks for new positions).
 void build_decode_desc(mesh_gpu* g, Instance& in, const int64_t* rids, int n, StepDesc& d) {
@@ -1106,7 +1079,6 @@ void mesh_gpu_close(mesh_gpu* g) {
         cudaFree(ws.wmem);
         cudaEventDestroy(ws.ready);
     }
-    for (cudaEvent_t e : g->shrink_evs) cudaEventDestroy(e);
     for (auto& b : g->ibufs) {
         drv().addr_free(b.va, b.va_size);
         cudaFree(b.d_block_table);

@@ -17,8 +17,11 @@
 //   GU    : RMSNorm scale, silu(gate) * up
 //   DOWN  : residual add, next RMSNorm numerator, sum-of-squares partials
 //   LM    : final RMSNorm scale, optional logits, greedy argmax
-// Weight tiles are dealt round-robin across CTAs continuing from phase to
-// phase; attention stages are dealt in contiguous ranges.
+// Weight tiles of single-segment phases with >= 4 tiles per CTA are claimed
+// dynamically (per-phase counter, groups of up to 4 tiles, in tile order);
+// the others are dealt round-robin across CTAs continuing from phase to phase,
+// multi-segment ones segment-outer. Attention stages are dealt in contiguous
+// ranges.
 #include "decode.cuh"
 
 #include <math.h>

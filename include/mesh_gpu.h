@@ -119,6 +119,11 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
  * (nullable, needs logits capture on) receives [n][vocab] fp32. */
 mesh_status mesh_gpu_step_wait(mesh_gpu* g, int64_t ticket, int32_t* tokens_out, int32_t cap, int32_t* n_out,
                                float* logits_out, int64_t logits_cap);
+/* Non-blocking completion poll (wall-clock mode): *done = 1 once the step's
+ * work finished on the device (its tokens are then collected by step_wait
+ * without blocking). Replaces the IterationComplete the reference schedules
+ * at now + iter_time (cluster.cpp:556-572). */
+mesh_status mesh_gpu_step_done(mesh_gpu* g, int64_t ticket, int32_t* done);
 mesh_status mesh_gpu_set_capture_logits(mesh_gpu* g, int32_t enable);
 
 mesh_status mesh_gpu_request_free(mesh_gpu* g, int64_t instance_id, int64_t request_id);

@@ -66,6 +66,16 @@ static uint16_t* gen_matrix(uint64_t seed, int tensor, int layer, size_t n) {
     for (long long i = 0; i < (long long)n; ++i) m[i] = f2bf(weight_value(key, (uint64_t)i));
     return m;
 }
+/* Bulk generator exports for the numpy restatement (oracle/llama_np.py). */
+void ora_gen_bf16(uint64_t seed, int tensor, int layer, uint64_t n, uint16_t* out) {
+    uint64_t key = tensor_key(seed, (uint32_t)tensor, (uint32_t)layer);
+#pragma omp parallel for schedule(static)
+    for (long long i = 0; i < (long long)n; ++i) out[i] = f2bf(weight_value(key, (uint64_t)i));
+}
+void ora_gen_gain(uint64_t seed, int tensor, int layer, int n, float* out) {
+    uint64_t key = tensor_key(seed, (uint32_t)tensor, (uint32_t)layer);
+    for (int i = 0; i < n; ++i) out[i] = gain_value(key, (uint64_t)i);
+}
 static float* gen_gain(uint64_t seed, int tensor, int layer, int n) {
     float* g = (float*)malloc((size_t)n * sizeof(float));
     uint64_t key = tensor_key(seed, (uint32_t)tensor, (uint32_t)layer);

@@ -39,6 +39,7 @@ public:
     SimTime now() const { return now_; }
     bool empty() const { return heap_.empty(); }
     std::size_t pending() const { return heap_.size(); }
+    SimTime next_time() const { return heap_.empty() ? std::numeric_limits<double>::infinity() : heap_.front().time; }
 
     void schedule(SimTime when, EventKind kind, std::int64_t subject);
     SimulationReport run_until(SimTime horizon);

@@ -3,6 +3,7 @@
 
 #include <dlfcn.h>
 
+#include <algorithm>
 #include <chrono>
 #include <cstring>
 
@@ -35,6 +36,8 @@ struct GpuExecutor::Api {
     decltype(&mesh_gpu_request_free) request_free;
     decltype(&mesh_gpu_swap_out) swap_out;
     decltype(&mesh_gpu_stats_get) stats_get;
+    decltype(&mesh_gpu_step_done) step_done;
+    decltype(&mesh_gpu_timer_mark) timer_mark;
 };
 
 namespace {
@@ -90,6 +93,8 @@ GpuExecutor::GpuExecutor(const std::string& lib_path, std::vector<int> devices, 
     BIND(request_free, "mesh_gpu_request_free");
     BIND(swap_out, "mesh_gpu_swap_out");
     BIND(stats_get, "mesh_gpu_stats_get");
+    BIND(step_done, "mesh_gpu_step_done");
+    BIND(timer_mark, "mesh_gpu_timer_mark");
 #undef BIND
     for (int dev : devices_) {
         mesh_gpu_cfg cfg{};
@@ -144,7 +149,7 @@ void GpuExecutor::iteration_start(const Cluster& c, const Node& nd, const Instan
         mesh_step_plan sp{1, p.prefill_request, p.kind.input_len, r.input_len, 0, nullptr};
         int64_t t = 0;
         check(h, api_->step(h, inst.id, &sp, &t), "prefill step");
-        tk.push_back({h, t, inst.id});
+        (wall_ ? live_[inst.id] : tk).push_back({h, t, inst.id});
         prefill_tokens_ += p.kind.input_len;
         return;
     }
@@ -156,12 +161,55 @@ void GpuExecutor::iteration_start(const Cluster& c, const Node& nd, const Instan
         mesh_step_plan sp{0, -1, 0, 0, n, rids.data() + o};
         int64_t t = 0;
         check(h, api_->step(h, inst.id, &sp, &t), "decode step");
-        tk.push_back({h, t, inst.id});
+        (wall_ ? live_[inst.id] : tk).push_back({h, t, inst.id});
     }
     decode_tokens_ += static_cast<long long>(rids.size());
 }
 
+void GpuExecutor::clock_start() {
+    wall_ = true;
+    for (mesh_gpu* h : handles_) check(h, api_->timer_mark(h, 0), "timer_mark");
+}
+
+// Wall-clock mode: an instance's step is done when all of its tickets are
+// (a batch wider than the kernel's 8 columns is several launches). Tokens are
+// then collected without blocking; the end time is the CUDA event of the
+// step's last launch on the device timeline of clock_start's mark.
+void GpuExecutor::poll_finished(std::vector<std::pair<InstanceId, double>>& done) {
+    for (auto it = live_.begin(); it != live_.end();) {
+        bool all = true;
+        for (const Pending& p : it->second) {
+            int32_t d = 0;
+            check(p.h, api_->step_done(p.h, p.ticket, &d), "step_done");
+            if (!d) {
+                all = false;
+                break;
+            }
+        }
+        if (!all) {
+            ++it;
+            continue;
+        }
+        HostTimer ht(host_ms_wait_);
+        double end_s = 0.0;
+        for (const Pending& p : it->second) {
+            int32_t toks[8];
+            int32_t n = 0;
+            check(p.h, api_->step_wait(p.h, p.ticket, toks, 8, &n, nullptr, 0), "step_wait");
+            mesh_gpu_stats st{};
+            api_->stats_get(p.h, &st);
+            device_ms_ += st.last_step_ms;
+            lane_busy_s_ += st.last_step_ms / 1e3;
+            end_s = std::max(end_s, st.last_step_end_ms / 1e3);
+            ++steps_;
+        }
+        done.emplace_back(it->first, end_s);
+        it = live_.erase(it);
+    }
+}
+
 void GpuExecutor::iteration_done(const Cluster&, const Node& nd, const IterationPlan&, const IterationOutcome&) {
+    if (wall_) return;  // retired by poll_finished
     // Steps stay asynchronous: their tickets are retired lazily (bounded by the
     // data plane's ticket ring), so the host keeps scheduling while the GPU runs.
     auto it = tickets_.find(nd.id);
@@ -209,6 +257,10 @@ void GpuExecutor::request_finished(const Cluster&, InstanceId inst, const Reques
 void GpuExecutor::instance_unloaded(const Cluster&, InstanceId inst) {
     auto d = inst_dev_.find(inst);
     if (d == inst_dev_.end()) return;
+    if (auto lv = live_.find(inst); lv != live_.end()) {  // not expected: unloads happen between steps
+        for (const Pending& p : lv->second) check(p.h, api_->step_wait(p.h, p.ticket, nullptr, 0, nullptr, nullptr, 0), "step_wait");
+        live_.erase(lv);
+    }
     // retire the instance's own outstanding tickets before it (and they) go away;
     // other instances' steps keep running
     for (std::size_t i = 0; i < pending_.size();)
@@ -251,6 +303,7 @@ std::map<std::string, double> GpuExecutor::metrics() const {
         wcache += static_cast<double>(st.weight_cache_hits);
     }
     m["gpu.weight_cache_hits"] = wcache;
+    m["gpu.lane_busy_s"] = lane_busy_s_;
     m["gpu.vmm_calls"] = vmm_calls;
     m["gpu.host_ms.vmm"] = vmm_ms;
     m["gpu.kv_reclaims"] = reclaims;

@@ -34,6 +34,12 @@ public:
     void request_finished(const Cluster&, InstanceId, const Request&) override;
     void instance_unloaded(const Cluster&, InstanceId) override;
 
+    // wall-clock mode (Cluster::set_wall_clock): steps complete on device events
+    bool supports_wall_clock() const override { return true; }
+    void clock_start() override;
+    void poll_finished(std::vector<std::pair<InstanceId, double>>& done) override;
+    std::size_t steps_in_flight() const override { return live_.size(); }
+
     std::map<std::string, double> metrics() const;
     void drain();  // wait for every launched step
 
@@ -56,6 +62,9 @@ private:
     // host wall time spent inside each data-plane hook (e2e breakdown)
     double host_ms_create_ = 0, host_ms_destroy_ = 0, host_ms_kv_ = 0, host_ms_step_ = 0, host_ms_wait_ = 0;
     std::deque<Pending> pending_;  // launched, not yet retired (oldest first)
+    bool wall_ = false;
+    std::map<InstanceId, std::vector<Pending>> live_;  // wall-clock mode: the step in flight per instance
+    double lane_busy_s_ = 0.0;                          // wall-clock mode: sum of step device times
     void retire_one();
     void retire_at(std::size_t i);
     mesh_gpu* handle_for_node(NodeId node);

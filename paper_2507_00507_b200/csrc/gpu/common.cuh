@@ -281,4 +281,14 @@ __host__ __device__ inline size_t tiled_index(int row, int col, int K) {
     return block * 1024 + inblock;
 }
 
+// Host: the current CUDA device, for per-device one-time launch configuration
+// (function attributes and occupancy apply to the device current when they are
+// set; one process may drive several devices through several mesh_gpu handles).
+constexpr int MAX_DEVICES = 64;
+inline int cur_device() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return (d >= 0 && d < MAX_DEVICES) ? d : 0;
+}
+
 }  // namespace meshgpu

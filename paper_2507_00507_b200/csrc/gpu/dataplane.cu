@@ -295,6 +295,7 @@ struct Lane {
     int2* d_moves = nullptr;  // compaction (src, dst) block pairs, reused in stream order
     int* tile_ctr = nullptr;  // prefill GEMM dynamic tile counter
     size_t moves_cap = 0;
+    cudaEvent_t quota_ev = nullptr;  // tail of the lane's queue when its quota last shrank
 };
 
 }  // namespace
@@ -367,10 +368,15 @@ std::map<int64_t, SwapEntry>& swap_store() {
     return s;
 }
 
+// Identity of a weight set: every input of the generator and of the RoPE table
+// that lives in the set (theta and max_seq_len size and fill the table).
 uint64_t shape_key_of(const Shape& s, uint64_t seed) {
     uint64_t k = seed;
-    int v[] = {s.n_layers, s.d, s.n_heads, s.n_kv, s.dh, s.ff, s.vocab, s.tied};
-    for (int x : v) k = splitmix64(k ^ uint64_t(x));
+    uint32_t theta_bits, eps_bits;
+    std::memcpy(&theta_bits, &s.rope_theta, 4);
+    std::memcpy(&eps_bits, &s.eps, 4);
+    int64_t v[] = {s.n_layers, s.d, s.n_heads, s.n_kv, s.dh, s.ff, s.vocab, s.tied, s.max_seq, theta_bits, eps_bits};
+    for (int64_t x : v) k = splitmix64(k ^ uint64_t(x));
     return k;
 }
 
@@ -390,12 +396,7 @@ int sm_budget(const mesh_gpu* g) { return g->cfg.sm_quota > 0 ? std::min(g->cfg.
 // (decode is HBM-bound, so equal-duration steps need SMs in proportion to
 // bytes); lanes without instances keep an even share for their first step.
 // Quotas always sum to <= the budget, so every lane's persistent decode grid
-// can be co-resident. Only lanes whose quota shrinks are drained: their
-// in-flight grids (old, larger quota) finish before any lane launches at its
-// new, larger quota, so old and new grids in flight never exceed the budget.
-// (Deferring the growth behind events instead, without a host wait, kept a new
-// lane at a 1-SM quota for as long as the other lanes' queues ran: 4x slower
-// on the 8-instance C3 scenario.)
+// can be co-resident.
 void rebalance_lanes(mesh_gpu* g) {
     const int budget = sm_budget(g), n = int(g->lanes.size());
     std::vector<int> q(size_t(n), 0);
@@ -437,10 +438,26 @@ void rebalance_lanes(mesh_gpu* g) {
             used--;
         }
     }
+    // No host wait: every lane whose quota grows makes its stream wait for the
+    // work already queued on the lanes whose quota shrinks (an event recorded
+    // now on each of them). Old-quota grids of shrinking lanes therefore finish
+    // before any new-quota grid of a growing lane starts, so the persistent
+    // decode grids in flight never exceed the budget; lanes keep running.
+    bool any_shrink = false;
     for (int i = 0; i < n; ++i) {
         Lane& l = g->lanes[size_t(i)];
-        if (q[size_t(i)] < l.ctas) CK(cudaStreamSynchronize(l.stream));
+        if (q[size_t(i)] < l.ctas) {
+            CK(cudaEventRecord(l.quota_ev, l.stream));
+            any_shrink = true;
+        }
     }
+    if (any_shrink)
+        for (int i = 0; i < n; ++i) {
+            Lane& l = g->lanes[size_t(i)];
+            if (q[size_t(i)] <= l.ctas) continue;
+            for (int j = 0; j < n; ++j)
+                if (q[size_t(j)] < g->lanes[size_t(j)].ctas) CK(cudaStreamWaitEvent(l.stream, g->lanes[size_t(j)].quota_ev, 0));
+        }
     for (int i = 0; i < n; ++i) g->lanes[size_t(i)].ctas = q[size_t(i)];
 }
 
@@ -532,7 +549,9 @@ void evict_weights(mesh_gpu* g, size_t cap) {
                 if (victim == g->wsets.end() || it->second.tick < victim->second.tick) victim = it;
             }
         if (idle <= cap || victim == g->wsets.end()) return;
-        cudaFree(victim->second.wmem);
+        // stream-ordered free: no device-wide synchronisation (the set has no live
+        // replica, and its last replica's work finished before its destroy returned)
+        cudaFreeAsync(victim->second.wmem, g->side);
         cudaEventDestroy(victim->second.ready);
         g->wsets.erase(victim);
     }
@@ -572,7 +591,19 @@ void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
     VmmTimer vt(g);
     while (in.granules.size() < want) {
         const size_t off = in.granules.size() * gran;
-        CUmemGenericAllocationHandle h = g->pool.take();
+        CUmemGenericAllocationHandle h;
+        try {
+            h = g->pool.take();
+        } catch (const MeshError&) {
+            if (g->pool.mapped + (long long)gran > g->pool.limit) throw;  // the pool's limit, not HBM
+            // HBM is short: idle weight sets go first (stream-ordered frees, then
+            // hand the freed memory back from the allocator's pool), then retry
+            evict_weights(g, 0);
+            CK(cudaStreamSynchronize(g->side));
+            cudaMemPool_t mp;
+            if (cudaDeviceGetDefaultMemPool(&mp, g->cfg.device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
+            h = g->pool.take();
+        }
         CUresult r = d.map(in.va + off, gran, 0, h, 0);
         if (r != CUDA_SUCCESS) {
             g->pool.give(h);
@@ -1011,6 +1042,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             dalloc(&l.arg_cnt, 1);
             dalloc(&l.claim, DEC_CLAIM_MAX);
             dalloc(&l.tile_ctr, 1);
+            CK(cudaEventCreateWithFlags(&l.quota_ev, cudaEventDisableTiming));
         }
         CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&g->lane_join, cudaEventDisableTiming));
@@ -1076,9 +1108,10 @@ void mesh_gpu_close(mesh_gpu* g) {
         cudaFree(in->d_last_tok);
     }
     for (auto& [k, ws] : g->wsets) {
-        cudaFree(ws.wmem);
+        cudaFreeAsync(ws.wmem, g->side);
         cudaEventDestroy(ws.ready);
     }
+    cudaStreamSynchronize(g->side);
     for (auto& b : g->ibufs) {
         drv().addr_free(b.va, b.va_size);
         cudaFree(b.d_block_table);
@@ -1092,6 +1125,7 @@ void mesh_gpu_close(mesh_gpu* g) {
         for (void* p : lane_ptrs)
             if (p) cudaFree(p);
         if (l.stream) cudaStreamDestroy(l.stream);
+        if (l.quota_ev) cudaEventDestroy(l.quota_ev);
     }
     void* dev_ptrs[] = {g->d_desc, g->d_tok};
     for (void* p : dev_ptrs)
@@ -1160,20 +1194,53 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         in->va_size = ((size_t(g->pool.limit) + size_t(in->block_bytes) * (DEC_MAXB + 2)) / gran + 1) * gran;
         in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
         in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
-        // weights: share a live or idle set of the same model, else allocate and initialise
+        // per-instance buffers first (recycle a free set of the same sizes, else
+        // allocate); on any later failure they go back to the free list
+        bool recycled = false;
+        for (size_t i = g->ibufs.size(); i-- > 0;) {
+            const mesh_gpu::InstBufs& bb = g->ibufs[i];
+            if (bb.va_size != in->va_size || bb.bt_elems != in->h_block_table.size()) continue;
+            in->va = bb.va;
+            in->d_block_table = bb.d_block_table;
+            in->d_last_tok = bb.d_last_tok;
+            g->ibufs.erase(g->ibufs.begin() + long(i));
+            recycled = true;
+            break;
+        }
+        if (!recycled) {
+            // KV region: reserve the whole pool's worth of VA
+            CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
+            if (cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()) != cudaSuccess ||
+                cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS) != cudaSuccess) {
+                cudaGetLastError();
+                if (in->d_block_table) cudaFree(in->d_block_table);
+                drv().addr_free(in->va, in->va_size);
+                throw MeshError(MESH_ERR_NOMEM, "instance buffers: cudaMalloc failed");
+            }
+        }
+        Instance* ip = in.get();
+        auto give_back_bufs = [g, ip] {
+            g->ibufs.push_back({ip->va, ip->va_size, ip->d_block_table, ip->h_block_table.size(), ip->d_last_tok});
+        };
+        // weights: share a live or idle set of the same model, else allocate
+        // (stream-ordered, so a later free never serialises the device) and
+        // initialise. The set's reference is taken only once nothing can fail.
         bool fresh = false;
         auto wit = g->wsets.find(in->shape_key);
-        if (wit != g->wsets.end() && wit->second.bytes == total) {
+        if (wit != g->wsets.end()) {
             in->wmem = wit->second.wmem;
-            wit->second.refs++;
-            g->st.weight_cache_hits++;
             CK(cudaStreamWaitEvent(st, wit->second.ready, 0));  // initialised on another lane maybe
         } else {
-            if (wit != g->wsets.end()) throw MeshError(MESH_ERR_RUNTIME, "weight set size mismatch");
-            if (cudaMalloc((void**)&in->wmem, total) != cudaSuccess) {
+            cudaError_t e = cudaMallocAsync((void**)&in->wmem, total, st);
+            if (e != cudaSuccess) {
                 cudaGetLastError();
                 evict_weights(g, 0);  // make room: drop every idle set, then retry
-                CK(cudaMalloc((void**)&in->wmem, total));
+                e = cudaMallocAsync((void**)&in->wmem, total, st);
+            }
+            if (e != cudaSuccess) {
+                cudaGetLastError();
+                give_back_bufs();
+                throw MeshError(MESH_ERR_NOMEM, "weights: cudaMallocAsync of " + std::to_string(total) + " bytes failed");
             }
             fresh = true;
         }
@@ -1219,33 +1286,21 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
             CK(cudaMemcpyAsync(rp, tab.data(), tab.size() * sizeof(float2), cudaMemcpyHostToDevice, st));
             // the pageable table copy returns once staged; the init kernels and every
             // later step of the instance are ordered on the lane stream: no host wait
-            mesh_gpu::WeightSet ws{in->wmem, total, 1, nullptr, 0};
+            mesh_gpu::WeightSet ws{in->wmem, total, 0, nullptr, ++g->wtick};
             CK(cudaEventCreateWithFlags(&ws.ready, cudaEventDisableTiming));
             CK(cudaEventRecord(ws.ready, st));
-            g->wsets.emplace(in->shape_key, ws);
-        }
-        // per-instance buffers: recycle a free set of the same sizes, else allocate
-        bool recycled = false;
-        for (size_t i = g->ibufs.size(); i-- > 0;) {
-            const mesh_gpu::InstBufs& bb = g->ibufs[i];
-            if (bb.va_size != in->va_size || bb.bt_elems != in->h_block_table.size()) continue;
-            in->va = bb.va;
-            in->d_block_table = bb.d_block_table;
-            in->d_last_tok = bb.d_last_tok;
-            g->ibufs.erase(g->ibufs.begin() + long(i));
-            recycled = true;
-            break;
-        }
-        if (!recycled) {
-            // KV region: reserve the whole pool's worth of VA
-            CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
-            CK(cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()));
-            CK(cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS));
+            g->wsets.emplace(in->shape_key, ws);  // idle (refs 0) until the create completes
         }
         CK(cudaMemsetAsync(in->d_block_table, 0, sizeof(int) * in->h_block_table.size(), st));
         CK(cudaMemsetAsync(in->d_last_tok, 0, sizeof(int) * MAX_SLOTS, st));
-        CK(cudaEventCreateWithFlags(&in->last_ev, cudaEventDisableTiming));
+        if (cudaEventCreateWithFlags(&in->last_ev, cudaEventDisableTiming) != cudaSuccess) {
+            cudaGetLastError();
+            give_back_bufs();
+            throw MeshError(MESH_ERR_CUDA, "instance event creation failed");
+        }
         CK(cudaEventRecord(in->last_ev, st));
+        g->wsets.at(in->shape_key).refs++;
+        if (!fresh) g->st.weight_cache_hits++;
         for (int i = MAX_SLOTS - 1; i >= 0; --i) in->free_slots.push_back(i);
         in->weight_bytes = double(total);
         g->lanes[best].weight_bytes += in->weight_bytes;
@@ -1433,6 +1488,17 @@ mesh_status mesh_gpu_step_wait(mesh_gpu* g, int64_t ticket, int32_t* tokens_out,
         }
         destroy_ticket(t);
         g->tickets.erase(it);
+    });
+}
+
+mesh_status mesh_gpu_step_done(mesh_gpu* g, int64_t ticket, int32_t* done) {
+    if (!g || !done) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        auto it = g->tickets.find(ticket);
+        if (it == g->tickets.end()) throw MeshError(MESH_ERR_ARG, "unknown or already-waited ticket");
+        const cudaError_t e = cudaEventQuery(it->second.end);
+        if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
+        *done = e == cudaSuccess ? 1 : 0;
     });
 }
 

@@ -321,6 +321,19 @@ struct Producer {
         if (mt.n == 0) return;
         const size_t tile_bytes = size_t(p.K) * 32;
         const int nseg = n_segments(p.K);
+        if (nseg > 1 && mt.n <= DEC_TACC_TILES) {
+            // segment-outer, as the consumers run it (run_gemv): every tile's
+            // chunks of segment 0, then of segment 1, ...
+            for (int sg = 0; sg < nseg; ++sg) {
+                int c0, c1;
+                seg_range(p.K, nseg, sg, c0, c1);
+                for (int ti = 0; ti < mt.n; ++ti) {
+                    const uint8_t* t = p.base + size_t(mt.t0 + ti * G) * tile_bytes;
+                    for (int ch = c0; ch < c1; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, nullptr, -1);
+                }
+            }
+            return;
+        }
         for (int g0 = 0; g0 < mt.n; g0 += DEC_MAXT) {
             const int gn = min(DEC_MAXT, mt.n - g0);
             for (int sg = 0; sg < nseg; ++sg) {
@@ -1398,11 +1411,12 @@ size_t decode_apart_floats(const Shape& s) {
 }
 
 cudaError_t launch_decode(const DecodeArgs& a, int grid, cudaStream_t stream) {
-    static bool configured = false;
-    if (!configured) {
+    static bool configured[MAX_DEVICES] = {};
+    const int dev = cur_device();
+    if (!configured[dev]) {
         cudaError_t e = cudaFuncSetAttribute(decode_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, DEC_SMEM_TOTAL);
         if (e != cudaSuccess) return e;
-        configured = true;
+        configured[dev] = true;
     }
     decode_kernel<<<grid, DEC_THREADS, DEC_SMEM_TOTAL, stream>>>(a);
     return cudaGetLastError();

@@ -628,11 +628,12 @@ __global__ void __launch_bounds__(PA_THREADS) pf_attn(const __grid_constant__ Pr
 
 template <int DH>
 cudaError_t attn_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
-    static bool cfg = false;
-    if (!cfg) {
+    static bool cfg[MAX_DEVICES] = {};
+    const int dev = cur_device();
+    if (!cfg[dev]) {
         cudaError_t e = cudaFuncSetAttribute(pf_attn<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize, pa_smem<DH>());
         if (e != cudaSuccess) return e;
-        cfg = true;
+        cfg[dev] = true;
     }
     dim3 grid((a.L + PA_QT - 1) / PA_QT, a.s.n_heads);
     pf_attn<DH><<<grid, PA_THREADS, pa_smem<DH>(), st>>>(a, layer);
@@ -680,11 +681,12 @@ __global__ void pf_argmax(const __grid_constant__ PrefillArgs a) {
 
 // Single-token lm_head (the last position only): the mma.sync tile kernel.
 cudaError_t lm_gemm(const PrefillArgs& a, cudaStream_t st) {
-    static bool cfg = false;
-    if (!cfg) {
+    static bool cfg[MAX_DEVICES] = {};
+    const int dev = cur_device();
+    if (!cfg[dev]) {
         cudaError_t e = cudaFuncSetAttribute(pf_lm_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
         if (e != cudaSuccess) return e;
-        cfg = true;
+        cfg[dev] = true;
     }
     pf_lm_gemm<<<dim3(a.s.vocab / PF_BM, 1), PF_THREADS, PF_SMEM, st>>>(a, a.w.lm, a.s.d, a.act, a.s.d, 1);
     return cudaGetLastError();
@@ -734,13 +736,14 @@ bool make_wmap(CUtensorMap* m, const uint8_t* W, int N, int K) {
 }
 
 int num_sms() {
-    static int n = [] {
-        int dev = 0, v = 148;
-        cudaGetDevice(&dev);
+    static int n[MAX_DEVICES] = {};
+    const int dev = cur_device();
+    if (!n[dev]) {
+        int v = 148;
         cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
-        return v;
-    }();
-    return n;
+        n[dev] = v;
+    }
+    return n[dev];
 }
 
 // Token-tile width: minimise waves x per-K-block time, where a K block costs
@@ -770,7 +773,8 @@ template <int KIND, int BN, int CS>
 cudaError_t gemm_tc_launch(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx,
                            int rows, int layer, cudaStream_t st) {
     using C = TcCfg<BN>;
-    static int max_clusters = 0;
+    static int max_clusters_dev[MAX_DEVICES] = {};
+    int& max_clusters = max_clusters_dev[cur_device()];
     cudaLaunchConfig_t cfg = {};
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;

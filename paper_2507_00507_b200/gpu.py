@@ -127,6 +127,7 @@ def _load() -> C.CDLL:
         "mesh_gpu_step": (C.c_int, [C.c_void_p, C.c_int64, P(StepPlan), P(C.c_int64)]),
         "mesh_gpu_step_wait": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int32), C.c_int32, P(C.c_int32),
                                          P(C.c_float), C.c_int64]),
+        "mesh_gpu_step_done": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int32)]),
         "mesh_gpu_set_capture_logits": (C.c_int, [C.c_void_p, C.c_int32]),
         "mesh_gpu_request_free": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
         "mesh_gpu_swap_out": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
@@ -165,7 +166,7 @@ def lib() -> C.CDLL:
 
 EXPORTED = ["mesh_gpu_version", "mesh_gpu_device_count", "mesh_gpu_open", "mesh_gpu_close", "mesh_gpu_last_error",
             "mesh_gpu_instance_create", "mesh_gpu_instance_destroy", "mesh_gpu_kv_resize", "mesh_gpu_step",
-            "mesh_gpu_step_wait", "mesh_gpu_set_capture_logits", "mesh_gpu_request_free", "mesh_gpu_swap_out",
+            "mesh_gpu_step_wait", "mesh_gpu_step_done", "mesh_gpu_set_capture_logits", "mesh_gpu_request_free", "mesh_gpu_swap_out",
             "mesh_gpu_migrate", "mesh_gpu_request_info", "mesh_gpu_request_tokens", "mesh_gpu_instance_kv",
             "mesh_gpu_read_weight", "mesh_gpu_stats_get", "mesh_gpu_sync", "mesh_gpu_bench_decode",
             "mesh_gpu_instance_lane"]
@@ -235,6 +236,12 @@ class MeshGpu:
             return list(toks[: n.value]), buf[: n.value * vocab].reshape(n.value, vocab)
         self._ck(self._l.mesh_gpu_step_wait(self.h, ticket, toks, 8, C.byref(n), None, 0))
         return list(toks[: n.value])
+
+    def done(self, ticket: int) -> bool:
+        """Non-blocking: has the step finished on the device?"""
+        d = C.c_int32()
+        self._ck(self._l.mesh_gpu_step_done(self.h, ticket, C.byref(d)))
+        return bool(d.value)
 
     def step(self, iid: int, **kw):
         vocab = kw.pop("vocab", 0)

@@ -12,9 +12,11 @@
  *                                complete_iteration compute.cpp:155-201
  *   mesh_gpu_request_free     <- request completion / drop (compute.cpp:180-197)
  *   mesh_gpu_swap_out         <- eviction (cluster.cpp:419-428, 742-750); the reference drops the KV and
- *                                re-prefills, here the KV is parked in pinned host memory and restored when
- *                                the request's re-prefill step runs
- *   mesh_gpu_migrate          <- displaced-request placement (cluster.cpp:439-463) as a P2P KV copy
+ *                                re-prefills, here the KV is parked in pinned host memory (async gather on a
+ *                                side stream) and restored when the request's re-prefill step runs
+ *   mesh_gpu_swap_in          <- the same re-prefill, started early: event-gated scatter on a side stream
+ *   mesh_gpu_migrate          <- displaced-request placement (cluster.cpp:439-463) as a P2P KV copy over
+ *                                NVLink instead of a re-prefill
  *
  * Conventions mirror llmmesh.h: every call returns mesh_status; on failure
  * mesh_gpu_last_error() holds a message owned by the handle (overwritten by
@@ -61,7 +63,8 @@ typedef struct mesh_gpu_cfg {
                                quota); instances bind to the lane with the fewest weight bytes and
                                co-located instances on different lanes step concurrently.
                                0 = MESH_GPU_LANES from the environment, else 1 */
-    int32_t reserved;
+    int32_t swap_pool_mb;   /* pinned host swap space to pin at open (shared by the process's handles;
+                               0 = pin 256 MiB chunks on first use) */
 } mesh_gpu_cfg;
 
 typedef struct mesh_step_plan {
@@ -90,9 +93,13 @@ typedef struct mesh_gpu_stats {
     int64_t kv_reclaims;          /* lazy-shrink slack reclaims (each drains the streams once) */
     double last_step_end_ms;      /* end of the last waited step on the device timeline of timer
                                      mark 0 (all lanes), -1 before the mark */
-    int64_t weight_cache_hits;    /* instance creates served from a cached replica of the model
-                                     (weights, KV VA range and block table kept across unload) */
+    int64_t weight_cache_hits;    /* instance creates that shared a live or cached weight set of the
+                                     same model (no allocation, no init kernels) */
+    int64_t peer_devices;         /* devices granted NVLink access to this device's KV (migration) */
 } mesh_gpu_stats;
+
+/* mesh_gpu_swap_state values */
+enum { MESH_SWAP_NONE = 0, MESH_SWAP_HISTORY = 1, MESH_SWAP_COPYING = 2, MESH_SWAP_PARKED = 3 };
 
 const char* mesh_gpu_version(void);
 int32_t mesh_gpu_device_count(void);
@@ -127,7 +134,25 @@ mesh_status mesh_gpu_step_done(mesh_gpu* g, int64_t ticket, int32_t* done);
 mesh_status mesh_gpu_set_capture_logits(mesh_gpu* g, int32_t enable);
 
 mesh_status mesh_gpu_request_free(mesh_gpu* g, int64_t instance_id, int64_t request_id);
+/* Preemption swap (SURVEY 8a d-new). swap_out parks a resident request: one
+ * copy kernel on the handle's swap stream gathers its KV blocks straight into
+ * pinned host memory, ordered after the request's queued steps by an event;
+ * the call never waits on the device, and the blocks return to the instance's
+ * free list once the gather finished. The request's next prefill step with
+ * prefill_len == ctx + 1 (the reference's re-prefill of I+O tokens) resumes
+ * from the parked KV and feeds one token; swap_in starts that restore early
+ * on a side stream (the instance's lane waits on it by event). Parked
+ * requests are process-wide: any handle may resume them. */
 mesh_status mesh_gpu_swap_out(mesh_gpu* g, int64_t instance_id, int64_t request_id);
+mesh_status mesh_gpu_swap_in(mesh_gpu* g, int64_t instance_id, int64_t request_id);
+/* Non-blocking: MESH_SWAP_NONE (not parked), _HISTORY (token history only),
+ * _COPYING (gather in flight), _PARKED (KV in pinned host memory). */
+mesh_status mesh_gpu_swap_state(mesh_gpu* g, int64_t request_id, int32_t* state);
+/* Live KV migration (SURVEY 8a e-new): one copy kernel on dst's device loads
+ * the request's blocks from src's VA range (peer access over NVLink when the
+ * devices differ) into fresh blocks of dst_instance; both lanes are ordered
+ * by events, the host waits only for src's in-flight steps of the instance
+ * (token history). */
 mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst, int64_t dst_instance,
                              int64_t request_id);
 

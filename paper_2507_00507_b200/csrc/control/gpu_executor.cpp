@@ -38,6 +38,7 @@ struct GpuExecutor::Api {
     decltype(&mesh_gpu_stats_get) stats_get;
     decltype(&mesh_gpu_step_done) step_done;
     decltype(&mesh_gpu_timer_mark) timer_mark;
+    decltype(&mesh_gpu_migrate) migrate;
 };
 
 namespace {
@@ -95,7 +96,9 @@ GpuExecutor::GpuExecutor(const std::string& lib_path, std::vector<int> devices, 
     BIND(stats_get, "mesh_gpu_stats_get");
     BIND(step_done, "mesh_gpu_step_done");
     BIND(timer_mark, "mesh_gpu_timer_mark");
+    BIND(migrate, "mesh_gpu_migrate");
 #undef BIND
+    if (const char* e = std::getenv("MESH_MIGRATE")) migrate_ = std::atoi(e) != 0;
     for (int dev : devices_) {
         mesh_gpu_cfg cfg{};
         cfg.device = dev;
@@ -248,6 +251,41 @@ void GpuExecutor::request_evicted(const Cluster&, InstanceId inst, const Request
     (void)api_->swap_out(h, inst, r.id);
 }
 
+mesh_gpu* GpuExecutor::handle_of_instance(InstanceId inst) {
+    auto d = inst_dev_.find(inst);
+    return d == inst_dev_.end() ? nullptr : handles_[static_cast<std::size_t>(d->second)];
+}
+
+// Displacement (commit_preemption, cluster.cpp:413-465): the reference drops the
+// request's KV and re-prefills it at the plan's target. Here the KV moves to the
+// target instance right away (one copy kernel on the target's GPU, NVLink P2P
+// when the nodes differ); the target's re-prefill step then finds ctx = I+O-1
+// resident and feeds one token. Decisions are untouched (the control plane
+// still prices the re-prefill); only the executed work differs.
+void GpuExecutor::request_displaced(const Cluster& c, InstanceId from, InstanceId planned_to, const Request& r) {
+    mesh_gpu* src = handle_of_instance(from);
+    mesh_gpu* dst = planned_to >= 0 ? handle_of_instance(planned_to) : nullptr;
+    if (!src) return;
+    if (migrate_ && dst) {
+        HostTimer ht(host_ms_migrate_);
+        if (api_->migrate(src, from, dst, planned_to, r.id) == MESH_OK) {
+            moved_[r.id] = planned_to;
+            ++migrations_;
+            return;
+        }
+        ++migrate_fallbacks_;  // not resident (never prefilled), or no room / peer path: park it instead
+    }
+    request_evicted(c, from, r);
+}
+
+void GpuExecutor::request_placed(const Cluster& c, InstanceId to, const Request& r) {
+    auto it = moved_.find(r.id);
+    if (it == moved_.end()) return;
+    const InstanceId at = it->second;
+    moved_.erase(it);
+    if (to != at) request_evicted(c, at, r);  // landed elsewhere: park the migrated KV for its re-prefill
+}
+
 void GpuExecutor::request_finished(const Cluster&, InstanceId inst, const Request& r) {
     auto d = inst_dev_.find(inst);
     if (d == inst_dev_.end()) return;
@@ -309,6 +347,9 @@ std::map<std::string, double> GpuExecutor::metrics() const {
     m["gpu.kv_reclaims"] = reclaims;
     m["gpu.swap_out_bytes"] = swap;
     m["gpu.migrate_bytes"] = mig;
+    m["gpu.migrations"] = static_cast<double>(migrations_);
+    m["gpu.migrate_fallbacks"] = static_cast<double>(migrate_fallbacks_);
+    m["gpu.host_ms.migrate"] = host_ms_migrate_;
     m["gpu.blocks_moved"] = moved;
     m["gpu.kernel_launches"] = launches;
     m["gpu.h2d_bytes"] = h2d;

@@ -31,6 +31,8 @@ public:
     void iteration_start(const Cluster&, const Node&, const Instance&, const IterationPlan&) override;
     void iteration_done(const Cluster&, const Node&, const IterationPlan&, const IterationOutcome&) override;
     void request_evicted(const Cluster&, InstanceId, const Request&) override;
+    void request_displaced(const Cluster&, InstanceId from, InstanceId planned_to, const Request&) override;
+    void request_placed(const Cluster&, InstanceId to, const Request&) override;
     void request_finished(const Cluster&, InstanceId, const Request&) override;
     void instance_unloaded(const Cluster&, InstanceId) override;
 
@@ -65,6 +67,13 @@ private:
     bool wall_ = false;
     std::map<InstanceId, std::vector<Pending>> live_;  // wall-clock mode: the step in flight per instance
     double lane_busy_s_ = 0.0;                          // wall-clock mode: sum of step device times
+    // live KV migration of displaced requests (MESH_MIGRATE=0 turns it off: they
+    // are swapped out and resume from pinned host memory, like evictions)
+    bool migrate_ = true;
+    std::map<RequestId, InstanceId> moved_;  // displaced request -> instance its KV was migrated to
+    long long migrations_ = 0, migrate_fallbacks_ = 0;
+    double host_ms_migrate_ = 0;
+    mesh_gpu* handle_of_instance(InstanceId inst);
     void retire_one();
     void retire_at(std::size_t i);
     mesh_gpu* handle_for_node(NodeId node);

@@ -10,13 +10,19 @@
 //    (memory.cpp:84-104) and every accounted target is backed.
 //  * Block tables: per request, the block ids in position order; new blocks
 //    come from the lowest free index (deterministic).
-//  * Steps run on one compute stream per device (temporal exclusivity of the
-//    reference's node loop, SPEC "one iteration per node at a time"); the
-//    host never waits for a step unless asked (tickets).
-//  * Swap: an evicted request's blocks are copied to pinned host memory on a
-//    side stream; its next prefill step restores them and feeds only the
-//    last token (equivalent to the reference's re-prefill of I+O tokens).
-//  * Migration: peer copy of a request's blocks into another instance.
+//  * Steps run on execution lanes (one stream + scratch + an SM quota each);
+//    the host never waits for a step unless asked (tickets).
+//  * Swap: an evicted request's blocks are gathered by one copy kernel on a
+//    side stream straight into a preallocated pinned host range (host-mapped,
+//    PCIe writes); swap_out never waits on the host, and the blocks return to
+//    the free list once the gather's event fired. Resume (the request's next
+//    prefill step, or an explicit swap_in prefetch) is gated on that event and
+//    scatters the range back with the same kernel, then feeds only the last
+//    token (equivalent to the reference's re-prefill of I+O tokens).
+//  * Migration: the same copy kernel on the destination GPU loads the source
+//    instance's blocks over NVLink (every KV granule is mapped readable by all
+//    peer devices) and writes the destination's blocks; event-ordered on both
+//    lanes, no stream synchronisation.
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <unistd.h>
@@ -27,6 +33,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -138,14 +145,37 @@ __global__ void init_gain(float* dst, int n, uint64_t seed, uint32_t tensor, int
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
         dst[i] = gain_value(key, uint64_t(i));
 }
-// Batched block copy within one KV region: pairs[i] = (src block, dst block).
-__global__ void kv_block_copy(uint8_t* base, long long block_bytes, const int2* pairs) {
-    int2 p = pairs[blockIdx.y];
-    const uint4* src = reinterpret_cast<const uint4*>(base + size_t(p.x) * block_bytes);
-    uint4* dst = reinterpret_cast<uint4*>(base + size_t(p.y) * block_bytes);
-    size_t n = size_t(block_bytes) / 16;
-    for (size_t i = size_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += size_t(gridDim.x) * blockDim.x)
-        dst[i] = src[i];
+// Batched whole-block KV copy driven by a block list passed by value (no
+// device-side list buffer, no H2D of it): block src[i] of the source region
+// -> block dst[i] of the destination region, blockIdx.y = i. One kernel serves
+// every KV move of the data plane:
+//   compaction  src = dst = the instance's VA range (HBM -> HBM)
+//   swap out    src = VA range, dst = host-mapped pinned staging, dst[i] = i (gather -> PCIe writes)
+//   swap in     src = pinned staging, src[i] = i, dst = VA range (PCIe reads -> scatter)
+//   migration   src = another instance's VA range, possibly on a peer GPU (NVLink P2P loads)
+// Each thread keeps 4 x 16 B loads in flight before its stores, so PCIe / NVLink
+// read latency is covered with a modest grid.
+constexpr int KV_LIST_MAX = 256;  // == DEC_BT_MAX: one request's blocks fit one launch
+struct BlockList {
+    int n;
+    int src[KV_LIST_MAX];
+    int dst[KV_LIST_MAX];
+};
+__global__ void __launch_bounds__(256) kv_blocks_copy(uint8_t* dst_base, const uint8_t* src_base, long long block_bytes,
+                                                      const __grid_constant__ BlockList L) {
+    const int i = blockIdx.y;
+    const uint4* src = reinterpret_cast<const uint4*>(src_base + size_t(L.src[i]) * size_t(block_bytes));
+    uint4* dst = reinterpret_cast<uint4*>(dst_base + size_t(L.dst[i]) * size_t(block_bytes));
+    const size_t n = size_t(block_bytes) / 16, stride = size_t(gridDim.x) * blockDim.x;
+    size_t e = size_t(blockIdx.x) * blockDim.x + threadIdx.x;
+    for (; e + 3 * stride < n; e += 4 * stride) {
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) v[k] = __ldcs(src + e + k * stride);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) __stcs(dst + e + k * stride, v[k]);
+    }
+    for (; e < n; e += stride) __stcs(dst + e, __ldcs(src + e));
 }
 __global__ void set_int(int* p, int v) { *p = v; }
 __global__ void read_tiled_row(const uint8_t* W, int K, int prow, float* out) {
@@ -204,14 +234,103 @@ struct ReqState {
     int pending_tokens = 0;    // emitted on device, not yet copied back
 };
 
+// Pinned host swap space shared by every handle of the process. Pinned memory
+// allocated cudaHostAllocPortable | Mapped is addressable from every GPU, so a
+// request evicted on one device can resume on any other (the control plane may
+// re-route it to another node). Chunks are pinned once (at open when
+// mesh_gpu_cfg.swap_pool_mb > 0, else on first use) and carved first-fit;
+// swaps never call cudaHostAlloc / cudaFreeHost on the steady path.
+struct HostSwapPool {
+    struct Chunk {
+        uint8_t* base = nullptr;
+        size_t bytes = 0;
+        std::map<size_t, size_t> free;  // offset -> length, coalesced
+    };
+    std::mutex mu;
+    std::vector<Chunk> chunks;
+    size_t chunk_bytes = size_t(256) << 20;
+    size_t pinned = 0;
+
+    void add_chunk(size_t bytes) {
+        Chunk c;
+        c.bytes = bytes;
+        if (cudaHostAlloc((void**)&c.base, bytes, cudaHostAllocPortable | cudaHostAllocMapped) != cudaSuccess) {
+            cudaGetLastError();
+            throw MeshError(MESH_ERR_NOMEM, "swap space: cudaHostAlloc of " + std::to_string(bytes) + " bytes failed");
+        }
+        c.free[0] = bytes;
+        pinned += bytes;
+        chunks.push_back(std::move(c));
+    }
+    void reserve(size_t bytes) {  // make sure `bytes` of pinned space exist
+        std::lock_guard<std::mutex> lk(mu);
+        if (pinned < bytes) add_chunk(bytes - pinned);
+    }
+    // -> (chunk, offset); 256-byte aligned
+    std::pair<int, size_t> take(size_t n) {
+        n = (n + 255) & ~size_t(255);
+        std::lock_guard<std::mutex> lk(mu);
+        for (int pass = 0; pass < 2; ++pass) {
+            for (size_t ci = 0; ci < chunks.size(); ++ci)
+                for (auto it = chunks[ci].free.begin(); it != chunks[ci].free.end(); ++it)
+                    if (it->second >= n) {
+                        const size_t off = it->first, len = it->second;
+                        chunks[ci].free.erase(it);
+                        if (len > n) chunks[ci].free[off + n] = len - n;
+                        return {int(ci), off};
+                    }
+            if (pass == 0) add_chunk(std::max(chunk_bytes, n));
+        }
+        throw MeshError(MESH_ERR_NOMEM, "swap space exhausted");
+    }
+    void give(int ci, size_t off, size_t n) {
+        n = (n + 255) & ~size_t(255);
+        std::lock_guard<std::mutex> lk(mu);
+        auto& fr = chunks[size_t(ci)].free;
+        auto it = fr.emplace(off, n).first;
+        auto nx = std::next(it);
+        if (nx != fr.end() && it->first + it->second == nx->first) {
+            it->second += nx->second;
+            fr.erase(nx);
+        }
+        if (it != fr.begin()) {
+            auto pv = std::prev(it);
+            if (pv->first + pv->second == it->first) {
+                pv->second += it->second;
+                fr.erase(it);
+            }
+        }
+    }
+    uint8_t* ptr(int ci, size_t off) { return chunks[size_t(ci)].base + off; }
+};
+HostSwapPool& host_pool() {
+    static HostSwapPool p;
+    return p;
+}
+
+// A request parked in pinned host memory. `done` fires when its gather (D2H)
+// finished; the host history may still miss the tokens of steps that were in
+// flight at eviction (`pending_tokens`), which drain into the entry as the
+// origin instance's tickets retire.
 struct SwapEntry {
     uint64_t shape_key = 0;
     int ctx = 0;
     std::vector<int> tokens;
-    void* host = nullptr;  // pinned, ctx rounded up to whole blocks
+    int pending_tokens = 0;
+    mesh_gpu* origin = nullptr;  // handle / instance the request was evicted from
+    int64_t origin_inst = -1;
+    int chunk = -1;              // host swap space range (chunk < 0: no KV parked)
+    size_t off = 0;
     size_t bytes = 0;
     long long block_bytes = 0;
     cudaEvent_t done = nullptr;
+};
+
+// Blocks whose last reader (a swap gather or a migration copy) may still run:
+// they return to the free list once `ev` fired.
+struct PendingFree {
+    cudaEvent_t ev = nullptr;
+    std::vector<int> blocks;
 };
 
 struct Instance {
@@ -240,6 +359,7 @@ struct Instance {
     int lane = 0;
     double weight_bytes = 0;
     cudaEvent_t last_ev = nullptr;  // after the instance's last enqueued lane work (steps, compaction)
+    std::deque<PendingFree> pending_free;  // blocks still read by an in-flight swap-out / migration
 };
 
 struct Ticket {
@@ -292,9 +412,7 @@ struct Lane {
     int* p_tokens = nullptr;
     double weight_bytes = 0;  // bound instances (placement balance, SM quota)
     int n_inst = 0;
-    int2* d_moves = nullptr;  // compaction (src, dst) block pairs, reused in stream order
     int* tile_ctr = nullptr;  // prefill GEMM dynamic tile counter
-    size_t moves_cap = 0;
     cudaEvent_t quota_ev = nullptr;  // tail of the lane's queue when its quota last shrank
 };
 
@@ -304,7 +422,8 @@ struct mesh_gpu {
     mesh_gpu_cfg cfg{};
     std::string err;
     int sms = 0;
-    cudaStream_t side = nullptr;     // swap / migration copies
+    cudaStream_t side = nullptr;     // swap-out gathers (D2H over PCIe)
+    cudaStream_t side_in = nullptr;  // swap-in prefetch scatters (H2D; PCIe is full duplex)
     cudaEvent_t timer[8] = {};       // mesh_gpu_timer_mark slots
     cudaEvent_t lane_join = nullptr; // timer marks: joins lanes into lane 0
     bool check = false;              // MESH_GPU_CHECK: synchronous per-step validation (debug)
@@ -359,14 +478,33 @@ struct mesh_gpu {
     std::vector<InstBufs> ibufs;  // free per-instance buffers
     size_t wcache_cap = size_t(32) << 30;  // MESH_GPU_WCACHE_GB: bytes of idle weight sets kept
     uint64_t wtick = 0;
+    // devices that may map this device's KV (peer access over NVLink): every KV
+    // granule is mapped readable by them, so a migration is one copy kernel on
+    // the destination GPU reading the source VA range directly
+    std::vector<int> peers;
+    // swap space ranges whose last reader (a swap-in scatter) may still run
+    struct HostFree {
+        cudaEvent_t ev;
+        int chunk;
+        size_t off, bytes;
+    };
+    std::deque<HostFree> host_free;
 };
 
 namespace {
 
-std::map<int64_t, SwapEntry>& swap_store() {
-    static std::map<int64_t, SwapEntry> s;
+// Parked requests by request id (ids are global to the control plane). One
+// store per process, like the pinned space it indexes (HostSwapPool): a
+// request may resume on another handle / device than the one it left.
+struct SwapStore {
+    std::mutex mu;
+    std::map<int64_t, SwapEntry> m;
+};
+SwapStore& swaps() {
+    static SwapStore s;
     return s;
 }
+std::map<int64_t, SwapEntry>& swap_store() { return swaps().m; }
 
 // Identity of a weight set: every input of the generator and of the RoPE table
 // that lives in the set (theta and max_seq_len size and fill the table).
@@ -514,6 +652,65 @@ Instance& inst_of(mesh_gpu* g, int64_t id) {
     return *it->second;
 }
 
+// ---- whole-block KV copies (compaction, swap, migration)
+int copy_grid_x(long long block_bytes) { return int(std::max(1LL, std::min(32LL, block_bytes / 16384))); }
+
+// dst_ids / src_ids null: blocks 0..n-1 of a contiguous staging range
+void launch_blocks_copy(uint8_t* dst_base, const uint8_t* src_base, long long block_bytes, const int* src_ids,
+                        const int* dst_ids, int n, cudaStream_t st) {
+    for (int o = 0; o < n; o += KV_LIST_MAX) {
+        BlockList L;
+        L.n = std::min(KV_LIST_MAX, n - o);
+        for (int i = 0; i < L.n; ++i) {
+            L.src[i] = src_ids ? src_ids[o + i] : o + i;
+            L.dst[i] = dst_ids ? dst_ids[o + i] : o + i;
+        }
+        kv_blocks_copy<<<dim3(unsigned(copy_grid_x(block_bytes)), unsigned(L.n)), 256, 0, st>>>(dst_base, src_base,
+                                                                                              block_bytes, L);
+        CK(cudaGetLastError());
+    }
+}
+
+cudaEvent_t record_new_event(cudaStream_t st) {
+    cudaEvent_t e;
+    CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CK(cudaEventRecord(e, st));
+    return e;
+}
+
+// Blocks of swapped-out / migrated requests go back to the free list once the
+// copy that reads them finished (force: wait for it).
+void reap_blocks(Instance& in, bool force) {
+    for (auto it = in.pending_free.begin(); it != in.pending_free.end();) {
+        const cudaError_t e = force ? cudaEventSynchronize(it->ev) : cudaEventQuery(it->ev);
+        if (e == cudaErrorNotReady) {
+            ++it;
+            continue;
+        }
+        if (e != cudaSuccess) CK(e);
+        for (int b : it->blocks) {
+            if (b < in.cap_blocks) in.free_blocks.insert(b);
+            in.live_blocks--;
+        }
+        cudaEventDestroy(it->ev);
+        it = in.pending_free.erase(it);
+    }
+}
+
+void reap_host(mesh_gpu* g, bool force) {
+    for (auto it = g->host_free.begin(); it != g->host_free.end();) {
+        const cudaError_t e = force ? cudaEventSynchronize(it->ev) : cudaEventQuery(it->ev);
+        if (e == cudaErrorNotReady) {
+            ++it;
+            continue;
+        }
+        if (e != cudaSuccess) CK(e);
+        host_pool().give(it->chunk, it->off, it->bytes);
+        cudaEventDestroy(it->ev);
+        it = g->host_free.erase(it);
+    }
+}
+
 // ---- KV region management
 int blocks_for_target(const Instance& in, long long target) {
     if (target <= 0) return 0;
@@ -612,12 +809,17 @@ void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
         in.granules.push_back(h);
         g->st.vmm_calls++;
     }
-    // one access grant for the whole newly mapped range
-    CUmemAccessDesc acc = {};
-    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-    acc.location.id = g->cfg.device;
-    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-    CU(d.set_access(in.va + first * gran, (want - first) * gran, &acc, 1), "cuMemSetAccess");
+    // one access grant for the whole newly mapped range: this device, and every
+    // peer that can reach it over NVLink (a migration's copy kernel runs on the
+    // destination GPU and loads these blocks directly)
+    std::vector<CUmemAccessDesc> acc(1 + g->peers.size());
+    for (size_t i = 0; i < acc.size(); ++i) {
+        acc[i] = {};
+        acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc[i].location.id = i == 0 ? g->cfg.device : g->peers[i - 1];
+        acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    }
+    CU(d.set_access(in.va + first * gran, (want - first) * gran, acc.data(), acc.size()), "cuMemSetAccess");
     g->st.vmm_calls++;
     // debug (MESH_GPU_POISON): recycled KV memory may hold any bit pattern; fill
     // new granules with bf16 NaN so reads of unwritten KV cannot go unnoticed
@@ -640,10 +842,11 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
         return;
     }
     // shrink: compact live blocks >= new_cap into the lowest free ids < new_cap
+    reap_blocks(in, true);  // blocks of swapped-out / migrated requests still being read count as live
     if (in.live_blocks > new_cap)
         throw MeshError(MESH_ERR_RUNTIME, "kv shrink below live blocks (" + std::to_string(in.live_blocks) + " > " +
                                               std::to_string(new_cap) + ")");
-    std::vector<int2> moves;
+    std::vector<int> from, to_ids;
     std::set<int> low_free;
     for (int b : in.free_blocks)
         if (b < new_cap) low_free.insert(b);
@@ -653,30 +856,22 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
             if (b < new_cap) continue;
             int dst = *low_free.begin();
             low_free.erase(low_free.begin());
-            moves.push_back(make_int2(b, dst));
+            from.push_back(b);
+            to_ids.push_back(dst);
             r.blocks[i] = dst;
             write_bt_entry(in, r.slot, int(i), dst);
         }
     }
-    if (!moves.empty()) {
-        Lane& ln = lane_of(g, in);
-        cudaStream_t st = ln.stream;
-        if (ln.moves_cap < moves.size()) {  // grow the lane's pair buffer (rare: drains the lane)
-            CK(cudaStreamSynchronize(st));
-            if (ln.d_moves) CK(cudaFree(ln.d_moves));
-            ln.moves_cap = std::max<size_t>(moves.size(), 4096);
-            CK(cudaMalloc((void**)&ln.d_moves, ln.moves_cap * sizeof(int2)));
-        }
-        int2* dpairs = ln.d_moves;
-        CK(cudaMemcpyAsync(dpairs, moves.data(), moves.size() * sizeof(int2), cudaMemcpyHostToDevice, st));
-        dim3 grid(std::max(1, int(std::min<long long>(64, in.block_bytes / (16 * 256)))), unsigned(moves.size()));
-        kv_block_copy<<<grid, 256, 0, st>>>(reinterpret_cast<uint8_t*>(in.va), in.block_bytes, dpairs);
-        CK(cudaGetLastError());
+    if (!from.empty()) {
+        // one batched copy kernel per 256 moves, block lists passed by value (no pair buffer, no host wait)
+        cudaStream_t st = stream_of(g, in);
+        uint8_t* base = reinterpret_cast<uint8_t*>(in.va);
+        launch_blocks_copy(base, base, in.block_bytes, from.data(), to_ids.data(), int(from.size()), st);
         CK(cudaMemcpyAsync(in.d_block_table, in.h_block_table.data(), in.h_block_table.size() * sizeof(int),
                            cudaMemcpyHostToDevice, st));
         CK(cudaEventRecord(in.last_ev, st));
-        g->st.blocks_moved += (long long)moves.size();
-        g->st.bytes_moved += 2LL * (long long)moves.size() * in.block_bytes;
+        g->st.blocks_moved += (long long)from.size();
+        g->st.bytes_moved += 2LL * (long long)from.size() * in.block_bytes;
     }
     // the tail stays mapped (lazy shrink, see reclaim_slack); queued work may still read it
     in.free_blocks = low_free;
@@ -685,6 +880,10 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
 }
 
 int alloc_block(mesh_gpu* g, Instance& in) {
+    if (in.free_blocks.empty() && !in.pending_free.empty()) {
+        reap_blocks(in, false);
+        if (in.free_blocks.empty()) reap_blocks(in, true);  // the copies reading them are short
+    }
     if (in.free_blocks.empty()) {
         // physical overcommit beyond the accounted target (rounding slack exhausted)
         int b = in.cap_blocks;
@@ -740,6 +939,14 @@ void drain_ticket(mesh_gpu* g, Ticket& t) {
         if (rit != it->second->reqs.end()) {
             rit->second.tokens.push_back(toks[i]);
             rit->second.pending_tokens--;
+        } else {  // swapped out while this step was in flight: the token belongs to the parked history
+            std::lock_guard<std::mutex> lk(swaps().mu);
+            auto sit = swap_store().find(t.reqs[i]);
+            if (sit != swap_store().end() && sit->second.origin == g && sit->second.origin_inst == t.instance &&
+                sit->second.pending_tokens > 0) {
+                sit->second.tokens.push_back(toks[i]);
+                sit->second.pending_tokens--;
+            }
         }
     }
     float ms = 0.f, kms = 0.f, end_ms = -1.f;
@@ -869,24 +1076,68 @@ void launch_decode_step(mesh_gpu* g, Instance& in, const int64_t* rids, int n, T
     g->st.decode_tokens += n;
 }
 
-void restore_from_swap(mesh_gpu* g, Instance& in, int64_t rid, ReqState& r, SwapEntry& e) {
-    // allocate blocks and scatter the pinned copy back (side stream ordered before compute)
-    int nblk = (e.ctx + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
-    CK(cudaEventSynchronize(e.done));
+// Takes a parked request out of the swap store (its history completed first:
+// tokens of steps that were in flight at eviction drain from the origin).
+SwapEntry take_parked(int64_t rid) {
+    mesh_gpu* origin = nullptr;
+    int64_t oinst = -1;
+    {
+        std::lock_guard<std::mutex> lk(swaps().mu);
+        auto it = swap_store().find(rid);
+        if (it == swap_store().end()) throw MeshError(MESH_ERR_ARG, "request " + std::to_string(rid) + " is not parked");
+        if (it->second.pending_tokens > 0) {
+            origin = it->second.origin;
+            oinst = it->second.origin_inst;
+        }
+    }
+    if (origin) drain_instance(origin, oinst);
+    std::lock_guard<std::mutex> lk(swaps().mu);
+    auto it = swap_store().find(rid);
+    if (it == swap_store().end()) throw MeshError(MESH_ERR_ARG, "request " + std::to_string(rid) + " is not parked");
+    SwapEntry e = std::move(it->second);
+    swap_store().erase(it);
+    return e;
+}
+
+// Scatter a parked request's KV back into fresh blocks of `in`, on stream `st`
+// after the gather's event (no host wait); the pinned range is released once
+// the scatter's own event fired. `st` is the instance's lane (resume inside a
+// prefill step) or the swap-in side stream (prefetch; the lane then waits on
+// the scatter before its next work).
+void restore_parked(mesh_gpu* g, Instance& in, ReqState& r, SwapEntry& e, cudaStream_t st) {
+    const int nblk = (e.ctx + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
     for (int i = 0; i < nblk; ++i) {
         int b = alloc_block(g, in);
         r.blocks.push_back(b);
         write_bt_entry(in, r.slot, i, b);
-        CK(cudaMemcpyAsync(reinterpret_cast<uint8_t*>(in.va) + size_t(b) * in.block_bytes,
-                           static_cast<uint8_t*>(e.host) + size_t(i) * in.block_bytes, in.block_bytes,
-                           cudaMemcpyHostToDevice, stream_of(g, in)));
     }
+    CK(cudaStreamWaitEvent(st, e.done, 0));
+    launch_blocks_copy(reinterpret_cast<uint8_t*>(in.va), host_pool().ptr(e.chunk, e.off), in.block_bytes, nullptr,
+                       r.blocks.data(), nblk, st);
+    cudaEvent_t ev = record_new_event(st);
+    if (st != stream_of(g, in)) {
+        CK(cudaStreamWaitEvent(stream_of(g, in), ev, 0));
+        CK(cudaMemcpyAsync(in.d_block_table + size_t(r.slot) * in.bt_stride,
+                           in.h_block_table.data() + size_t(r.slot) * in.bt_stride, sizeof(int) * in.bt_stride,
+                           cudaMemcpyHostToDevice, stream_of(g, in)));
+        set_int<<<1, 1, 0, stream_of(g, in)>>>(in.d_last_tok + r.slot, e.tokens.empty() ? 0 : e.tokens.back());
+        CK(cudaGetLastError());
+    }
+    g->host_free.push_back({ev, e.chunk, e.off, e.bytes});
+    cudaEventDestroy(e.done);
+    e.done = nullptr;
     r.ctx = e.ctx;
     r.tokens = e.tokens;
     g->st.swap_in_bytes += (long long)nblk * in.block_bytes;
-    CK(cudaFreeHost(e.host));
-    cudaEventDestroy(e.done);
-    swap_store().erase(rid);
+}
+
+void drop_parked(mesh_gpu* g, SwapEntry& e) {
+    if (e.chunk >= 0) {  // the gather may still be writing the range
+        CK(cudaEventSynchronize(e.done));
+        host_pool().give(e.chunk, e.off, e.bytes);
+    }
+    if (e.done) cudaEventDestroy(e.done);
+    (void)g;
 }
 
 void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Ticket& t) {
@@ -897,16 +1148,18 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     int n = p.prefill_len;
     if (n < 1 || n > in.s.max_seq) throw MeshError(MESH_ERR_ARG, "prefill_len out of range");
     // a request that was evicted resumes from its parked KV (or at least its history)
-    auto sit = swap_store().find(rid);
-    if (sit != swap_store().end() && r.ctx == 0) {
-        SwapEntry& e = sit->second;
-        if (e.host && e.shape_key == in.shape_key && e.ctx == n - 1) {
-            restore_from_swap(g, in, rid, r, e);
+    bool parked = false;
+    if (r.ctx == 0) {
+        std::lock_guard<std::mutex> lk(swaps().mu);
+        parked = swap_store().count(rid) > 0;
+    }
+    if (parked) {
+        SwapEntry e = take_parked(rid);
+        if (e.chunk >= 0 && e.shape_key == in.shape_key && e.ctx == n - 1) {
+            restore_parked(g, in, r, e, stream_of(g, in));
         } else {
             r.tokens = e.tokens;
-            if (e.host) CK(cudaFreeHost(e.host));
-            if (e.done) cudaEventDestroy(e.done);
-            swap_store().erase(sit);
+            drop_parked(g, e);
         }
     }
     if (r.tokens.empty()) {
@@ -1045,7 +1298,24 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             CK(cudaEventCreateWithFlags(&l.quota_ev, cudaEventDisableTiming));
         }
         CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
+        CK(cudaStreamCreateWithFlags(&g->side_in, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&g->lane_join, cudaEventDisableTiming));
+        // peers: devices that can load this device's memory over NVLink get read/write
+        // access to every KV granule (map_to); this device may load theirs
+        for (int d = 0; d < n; ++d) {
+            if (d == cfg->device) continue;
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, d, cfg->device) == cudaSuccess && can) g->peers.push_back(d);
+            int back = 0;
+            if (cudaDeviceCanAccessPeer(&back, cfg->device, d) == cudaSuccess && back) {
+                const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) CK(e);
+                cudaGetLastError();
+            }
+        }
+        g->st.peer_devices = (int64_t)g->peers.size();
+        // pinned swap space, pinned once up front (cudaHostAlloc of GBs takes ~0.1-1 s)
+        if (cfg->swap_pool_mb > 0) host_pool().reserve(size_t(cfg->swap_pool_mb) << 20);
         g->pool.device = cfg->device;
         CUmemAllocationProp prop2 = {};
         prop2.type = CU_MEM_ALLOCATION_TYPE_PINNED;
@@ -1096,8 +1366,28 @@ void mesh_gpu_close(mesh_gpu* g) {
     if (!g) return;
     cudaSetDevice(g->cfg.device);
     cudaDeviceSynchronize();
-    for (auto& [id, t] : g->tickets) destroy_ticket(t);
+    // finish every request history (tokens of retired steps) before the tickets go
+    for (auto& [id, t] : g->tickets) {
+        try {
+            drain_ticket(g, t);
+        } catch (...) {
+        }
+        destroy_ticket(t);
+    }
+    {  // parked requests keep their KV and history, but forget this handle
+        std::lock_guard<std::mutex> lk(swaps().mu);
+        for (auto& [rid, e] : swap_store())
+            if (e.origin == g) {
+                e.origin = nullptr;
+                e.pending_tokens = 0;
+            }
+    }
+    try {
+        reap_host(g, true);
+    } catch (...) {
+    }
     for (auto& [id, in] : g->insts) {
+        for (PendingFree& pf : in->pending_free) cudaEventDestroy(pf.ev);
         try {
             unmap_tail(g, *in, 0);
         } catch (...) {
@@ -1121,7 +1411,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
                              l.arg_idx, l.arg_cnt, l.logits, l.bar, l.p_h, l.p_act, l.p_rs, l.p_q, l.p_attn,
-                             l.p_abuf, l.p_logits, l.p_tokens, l.d_moves, l.tile_ctr, l.claim};
+                             l.p_abuf, l.p_logits, l.p_tokens, l.tile_ctr, l.claim};
         for (void* p : lane_ptrs)
             if (p) cudaFree(p);
         if (l.stream) cudaStreamDestroy(l.stream);
@@ -1136,6 +1426,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (int i = 0; i < RING; ++i)
         if (g->ring_ev[i]) cudaEventDestroy(g->ring_ev[i]);
     if (g->side) cudaStreamDestroy(g->side);
+    if (g->side_in) cudaStreamDestroy(g->side_in);
     for (cudaEvent_t e : g->timer)
         if (e) cudaEventDestroy(e);
     if (g->lane_join) cudaEventDestroy(g->lane_join);
@@ -1314,9 +1605,12 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
     if (!g) return MESH_ERR_ARG;
     return guarded(g, [&] {
         Instance& in = inst_of(g, instance_id);
-        // wait for this instance's own lane work only (co-located instances keep running)
+        // wait for this instance's own lane work only (co-located instances keep running),
+        // retire its tickets (histories of parked requests complete), and wait for the
+        // swap / migration copies still reading its blocks
         CK(cudaEventSynchronize(in.last_ev));
-        CK(cudaStreamSynchronize(g->side));
+        drain_instance(g, instance_id);
+        reap_blocks(in, true);
         cudaEventDestroy(in.last_ev);
         unmap_tail(g, in, 0);
         lane_of(g, in).weight_bytes -= in.weight_bytes;
@@ -1407,6 +1701,8 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
     if (!g || !plan || !ticket) return MESH_ERR_ARG;
     return guarded(g, [&] {
         Instance& in = inst_of(g, instance_id);
+        reap_blocks(in, false);  // blocks of swapped-out / migrated requests whose copy finished
+        if (!g->host_free.empty()) reap_host(g, false);
         Ticket t;
         t.instance = instance_id;
         t.prefill = plan->is_prefill != 0;
@@ -1524,41 +1820,95 @@ mesh_status mesh_gpu_swap_out(mesh_gpu* g, int64_t instance_id, int64_t request_
         Instance& in = inst_of(g, instance_id);
         auto it = in.reqs.find(request_id);
         if (it == in.reqs.end()) throw MeshError(MESH_ERR_ARG, "swap_out: request not resident");
-        flush_request(g, instance_id, request_id);
+        reap_host(g, false);
         ReqState& r = it->second;
         SwapEntry e;
         e.shape_key = in.shape_key;
-        e.tokens = r.tokens;
+        e.tokens = r.tokens;  // completed by the request's in-flight steps as they retire (drain_ticket)
+        e.pending_tokens = r.pending_tokens;
+        e.origin = g;
+        e.origin_inst = instance_id;
+        PendingFree pf;
         if (r.ctx > 0) {
             e.ctx = r.ctx;
             e.block_bytes = in.block_bytes;
             e.bytes = r.blocks.size() * size_t(in.block_bytes);
-            CK(cudaHostAlloc(&e.host, e.bytes, cudaHostAllocPortable));
-            // order after every step that wrote this request's KV
-            cudaEvent_t ready;
-            CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
-            CK(cudaEventRecord(ready, stream_of(g, in)));
+            const auto [ci, off] = host_pool().take(e.bytes);
+            e.chunk = ci;
+            e.off = off;
+            // gather after every queued step that wrote this request's KV (event-ordered, no host wait)
+            cudaEvent_t ready = record_new_event(stream_of(g, in));
             CK(cudaStreamWaitEvent(g->side, ready, 0));
             cudaEventDestroy(ready);
-            for (size_t i = 0; i < r.blocks.size(); ++i)
-                CK(cudaMemcpyAsync(static_cast<uint8_t*>(e.host) + i * in.block_bytes,
-                                   reinterpret_cast<uint8_t*>(in.va) + size_t(r.blocks[i]) * in.block_bytes,
-                                   in.block_bytes, cudaMemcpyDeviceToHost, g->side));
-            CK(cudaEventCreateWithFlags(&e.done, cudaEventDisableTiming));
-            CK(cudaEventRecord(e.done, g->side));
-            // the blocks return to the free list only after the copy drains
-            CK(cudaEventSynchronize(e.done));
+            launch_blocks_copy(host_pool().ptr(ci, off), reinterpret_cast<uint8_t*>(in.va), in.block_bytes,
+                               r.blocks.data(), nullptr, int(r.blocks.size()), g->side);
+            e.done = record_new_event(g->side);
+            pf.ev = record_new_event(g->side);
+            pf.blocks = r.blocks;
             g->st.swap_out_bytes += (long long)e.bytes;
         }
-        auto& store = swap_store();
-        auto old = store.find(request_id);
-        if (old != store.end()) {
-            if (old->second.host) cudaFreeHost(old->second.host);
-            if (old->second.done) cudaEventDestroy(old->second.done);
-            store.erase(old);
+        SwapEntry old;
+        bool had_old = false;
+        {
+            std::lock_guard<std::mutex> lk(swaps().mu);
+            auto o = swap_store().find(request_id);
+            if (o != swap_store().end()) {
+                old = std::move(o->second);
+                swap_store().erase(o);
+                had_old = true;
+            }
+            swap_store().emplace(request_id, std::move(e));
         }
-        store.emplace(request_id, std::move(e));
-        free_request(in, request_id);
+        if (had_old) drop_parked(g, old);
+        // the slot is free now; the blocks stay live until the gather read them
+        in.free_slots.push_back(r.slot);
+        if (pf.ev) in.pending_free.push_back(std::move(pf));
+        in.reqs.erase(it);
+    });
+}
+
+mesh_status mesh_gpu_swap_in(mesh_gpu* g, int64_t instance_id, int64_t request_id) {
+    if (!g) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        Instance& in = inst_of(g, instance_id);
+        if (in.reqs.count(request_id)) throw MeshError(MESH_ERR_ARG, "swap_in: request already resident");
+        {
+            std::lock_guard<std::mutex> lk(swaps().mu);
+            auto it = swap_store().find(request_id);
+            if (it == swap_store().end()) throw MeshError(MESH_ERR_ARG, "swap_in: request is not parked");
+            if (it->second.chunk < 0) throw MeshError(MESH_ERR_ARG, "swap_in: request has no parked KV");
+            if (it->second.shape_key != in.shape_key)
+                throw MeshError(MESH_ERR_ARG, "swap_in: parked KV belongs to another model");
+        }
+        reap_host(g, false);
+        SwapEntry e = take_parked(request_id);
+        ReqState& r = req_slot(in, request_id);
+        try {
+            restore_parked(g, in, r, e, g->side_in);
+        } catch (...) {
+            free_request(in, request_id);
+            drop_parked(g, e);
+            throw;
+        }
+    });
+}
+
+mesh_status mesh_gpu_swap_state(mesh_gpu* g, int64_t request_id, int32_t* state) {
+    if (!g || !state) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        std::lock_guard<std::mutex> lk(swaps().mu);
+        auto it = swap_store().find(request_id);
+        if (it == swap_store().end()) {
+            *state = MESH_SWAP_NONE;
+            return;
+        }
+        if (it->second.chunk < 0) {
+            *state = MESH_SWAP_HISTORY;
+            return;
+        }
+        const cudaError_t e = cudaEventQuery(it->second.done);
+        if (e != cudaSuccess && e != cudaErrorNotReady) CK(e);
+        *state = e == cudaSuccess ? MESH_SWAP_PARKED : MESH_SWAP_COPYING;
     });
 }
 
@@ -1570,13 +1920,20 @@ mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst,
         Instance& si = inst_of(src, src_instance);
         auto it = si.reqs.find(request_id);
         if (it == si.reqs.end()) throw MeshError(MESH_ERR_ARG, "migrate: request not resident at source");
-        flush_request(src, src_instance, request_id);
-        CK(cudaStreamSynchronize(stream_of(src, si)));
-        CK(cudaSetDevice(dst->cfg.device));
         Instance& di = inst_of(dst, dst_instance);
         if (di.shape_key != si.shape_key) throw MeshError(MESH_ERR_ARG, "migrate: instances serve different models");
-        ReqState& sr = it->second;
         if (di.reqs.count(request_id)) throw MeshError(MESH_ERR_ARG, "migrate: request already at destination");
+        if (src->cfg.device != dst->cfg.device &&
+            std::find(src->peers.begin(), src->peers.end(), dst->cfg.device) == src->peers.end())
+            throw MeshError(MESH_ERR_CUDA, "migrate: no peer access from device " + std::to_string(dst->cfg.device) +
+                                               " to device " + std::to_string(src->cfg.device));
+        // the token history travels with the request: retire the source instance's
+        // in-flight steps (the control plane migrates requests of instances that
+        // are not mid-step, so this normally waits for nothing)
+        flush_request(src, src_instance, request_id);
+        ReqState& sr = it->second;
+        cudaEvent_t ready = record_new_event(stream_of(src, si));  // after every step that wrote the KV
+        CK(cudaSetDevice(dst->cfg.device));
         ReqState& dr = req_slot(di, request_id);
         cudaStream_t dst_st = stream_of(dst, di);
         dr.tokens = sr.tokens;
@@ -1585,23 +1942,27 @@ mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst,
             int b = alloc_block(dst, di);
             dr.blocks.push_back(b);
             write_bt_entry(di, dr.slot, int(i), b);
-            void* dptr = reinterpret_cast<uint8_t*>(di.va) + size_t(b) * di.block_bytes;
-            const void* sptr = reinterpret_cast<uint8_t*>(si.va) + size_t(sr.blocks[i]) * si.block_bytes;
-            if (src->cfg.device == dst->cfg.device)
-                CK(cudaMemcpyAsync(dptr, sptr, di.block_bytes, cudaMemcpyDeviceToDevice, dst_st));
-            else
-                CK(cudaMemcpyPeerAsync(dptr, dst->cfg.device, sptr, src->cfg.device, di.block_bytes, dst_st));
         }
-        // the device-side last token travels with the request
-        int last = sr.tokens.empty() ? 0 : sr.tokens.back();
+        CK(cudaStreamWaitEvent(dst_st, ready, 0));
+        cudaEventDestroy(ready);
+        // one copy kernel on the destination GPU: P2P loads of the source blocks over NVLink
+        launch_blocks_copy(reinterpret_cast<uint8_t*>(di.va), reinterpret_cast<const uint8_t*>(si.va), di.block_bytes,
+                           sr.blocks.data(), dr.blocks.data(), int(sr.blocks.size()), dst_st);
+        const int last = sr.tokens.empty() ? 0 : sr.tokens.back();
         set_int<<<1, 1, 0, dst_st>>>(di.d_last_tok + dr.slot, last);
+        CK(cudaGetLastError());
         CK(cudaMemcpyAsync(di.d_block_table + size_t(dr.slot) * di.bt_stride,
                            di.h_block_table.data() + size_t(dr.slot) * di.bt_stride, sizeof(int) * di.bt_stride,
                            cudaMemcpyHostToDevice, dst_st));
-        CK(cudaStreamSynchronize(dst_st));
+        PendingFree pf;
+        pf.ev = record_new_event(dst_st);  // the source blocks are free once the copy read them
+        CK(cudaEventRecord(di.last_ev, dst_st));
         dst->st.migrate_bytes += (long long)sr.blocks.size() * di.block_bytes;
         CK(cudaSetDevice(src->cfg.device));
-        free_request(si, request_id);
+        pf.blocks = std::move(sr.blocks);
+        si.free_slots.push_back(sr.slot);
+        si.pending_free.push_back(std::move(pf));
+        si.reqs.erase(it);
         CK(cudaSetDevice(dst->cfg.device));
     });
 }
@@ -1627,13 +1988,26 @@ mesh_status mesh_gpu_request_tokens(mesh_gpu* g, int64_t instance_id, int64_t re
         Instance& in = inst_of(g, instance_id);
         flush_request(g, instance_id, request_id);
         auto it = in.reqs.find(request_id);
+        std::vector<int> parked;
         const std::vector<int>* src = nullptr;
-        if (it != in.reqs.end())
+        if (it != in.reqs.end()) {
             src = &it->second.tokens;
-        else {
-            auto sit = swap_store().find(request_id);
-            if (sit == swap_store().end()) throw MeshError(MESH_ERR_ARG, "unknown request");
-            src = &sit->second.tokens;
+        } else {
+            mesh_gpu* origin = nullptr;
+            int64_t oinst = -1;
+            {
+                std::lock_guard<std::mutex> lk(swaps().mu);
+                auto sit = swap_store().find(request_id);
+                if (sit == swap_store().end()) throw MeshError(MESH_ERR_ARG, "unknown request");
+                if (sit->second.pending_tokens > 0) {
+                    origin = sit->second.origin;
+                    oinst = sit->second.origin_inst;
+                }
+            }
+            if (origin) drain_instance(origin, oinst);
+            std::lock_guard<std::mutex> lk(swaps().mu);
+            parked = swap_store().at(request_id).tokens;
+            src = &parked;
         }
         int n = int(src->size());
         for (int i = 0; i < std::min(n, cap); ++i) tokens[i] = (*src)[i];

@@ -34,7 +34,7 @@ class ModelShape(C.Structure):
 class GpuCfg(C.Structure):
     _fields_ = [("device", C.c_int32), ("sm_quota", C.c_int32), ("kv_pool_bytes", C.c_int64),
                 ("prompt_seed", C.c_uint64), ("kv_granule_bytes", C.c_int64), ("lanes", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("swap_pool_mb", C.c_int32)]
 
 
 class StepPlan(C.Structure):
@@ -51,7 +51,7 @@ class GpuStats(C.Structure):
                 ("kernel_launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("kv_granule_bytes", C.c_int64), ("vmm_calls", C.c_int64), ("vmm_ms", C.c_double),
                 ("kv_reclaims", C.c_int64), ("last_step_end_ms", C.c_double),
-                ("weight_cache_hits", C.c_int64)]
+                ("weight_cache_hits", C.c_int64), ("peer_devices", C.c_int64)]
 
 
 @dataclass(frozen=True)
@@ -131,6 +131,8 @@ def _load() -> C.CDLL:
         "mesh_gpu_set_capture_logits": (C.c_int, [C.c_void_p, C.c_int32]),
         "mesh_gpu_request_free": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
         "mesh_gpu_swap_out": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
+        "mesh_gpu_swap_in": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64]),
+        "mesh_gpu_swap_state": (C.c_int, [C.c_void_p, C.c_int64, P(C.c_int32)]),
         "mesh_gpu_migrate": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_int64]),
         "mesh_gpu_request_info": (C.c_int, [C.c_void_p, C.c_int64, C.c_int64, P(C.c_int32), P(C.c_int32),
                                             P(C.c_int32), C.c_int32]),
@@ -167,7 +169,7 @@ def lib() -> C.CDLL:
 EXPORTED = ["mesh_gpu_version", "mesh_gpu_device_count", "mesh_gpu_open", "mesh_gpu_close", "mesh_gpu_last_error",
             "mesh_gpu_instance_create", "mesh_gpu_instance_destroy", "mesh_gpu_kv_resize", "mesh_gpu_step",
             "mesh_gpu_step_wait", "mesh_gpu_step_done", "mesh_gpu_set_capture_logits", "mesh_gpu_request_free", "mesh_gpu_swap_out",
-            "mesh_gpu_migrate", "mesh_gpu_request_info", "mesh_gpu_request_tokens", "mesh_gpu_instance_kv",
+            "mesh_gpu_swap_in", "mesh_gpu_swap_state", "mesh_gpu_migrate", "mesh_gpu_request_info", "mesh_gpu_request_tokens", "mesh_gpu_instance_kv",
             "mesh_gpu_read_weight", "mesh_gpu_stats_get", "mesh_gpu_sync", "mesh_gpu_bench_decode",
             "mesh_gpu_instance_lane"]
 
@@ -176,9 +178,9 @@ class MeshGpu:
     """One B200 (one handle of the C ABI)."""
 
     def __init__(self, device: int = 0, sm_quota: int = 0, kv_pool_bytes: int = 0, prompt_seed: int = 1234,
-                 kv_granule_bytes: int = 0, lanes: int = 0):
+                 kv_granule_bytes: int = 0, lanes: int = 0, swap_pool_mb: int = 0):
         self._l = lib()
-        cfg = GpuCfg(device, sm_quota, kv_pool_bytes, prompt_seed, kv_granule_bytes, lanes, 0)
+        cfg = GpuCfg(device, sm_quota, kv_pool_bytes, prompt_seed, kv_granule_bytes, lanes, swap_pool_mb)
         h = C.c_void_p()
         st = self._l.mesh_gpu_open(C.byref(cfg), C.byref(h))
         if st != MESH_OK:
@@ -253,6 +255,16 @@ class MeshGpu:
 
     def swap_out(self, iid: int, rid: int) -> None:
         self._ck(self._l.mesh_gpu_swap_out(self.h, iid, rid))
+
+    def swap_in(self, iid: int, rid: int) -> None:
+        self._ck(self._l.mesh_gpu_swap_in(self.h, iid, rid))
+
+    SWAP_STATES = {0: "none", 1: "history", 2: "copying", 3: "parked"}
+
+    def swap_state(self, rid: int) -> str:
+        st = C.c_int32()
+        self._ck(self._l.mesh_gpu_swap_state(self.h, rid, C.byref(st)))
+        return self.SWAP_STATES[st.value]
 
     def migrate_to(self, src_iid: int, dst: "MeshGpu", dst_iid: int, rid: int) -> None:
         self._ck(self._l.mesh_gpu_migrate(self.h, src_iid, dst.h, dst_iid, rid))

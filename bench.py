@@ -1,34 +1,42 @@
 #!/usr/bin/env python
 """Benchmark of the co-located token step on B200 (driver contract).
 
-Workload (BASELINE.json configs[1], "C2"): four co-located Llama-shaped models
-[1.1B, 3B, 1.1B, 3B] (random-init weights, synthetic prompts) on one B200,
-sharing the GPU's VMM KV pool; every instance serves a full batch of 8
-requests whose lengths come from the C2 scenario's length dataset; finished
-requests are replaced by new ones (prefill first, as select_next does).
+Workload (BASELINE.json configs[2], "C3", the largest single-GPU config): eight
+co-located Llama-shaped models [1.1B, 3B, 7B, 1.1B, 3B, 7B, 1.1B, 3B]
+(random-init weights, synthetic prompts) on one B200, each on its own
+execution lane with an SM quota in proportion to its streamed weight bytes,
+all drawing on the GPU's VMM KV pool.
 
   step    one instance step of the co-located schedule (the planned decode of
-          that instance's batch, or the prefill of a newly admitted request),
-          launched through the mesh_gpu C ABI; instances take turns.
+          that instance's batch of 8, or the prefill of a newly admitted
+          request), launched through the mesh_gpu C ABI; instances take turns.
+          Every admission and completion re-sizes the instance's KV target by
+          the reference's rule (m_require + 20 % watermark, memory.cpp:19-36):
+          KV grow (VMM map) and shrink (compaction kernel) run inside the timed
+          region.
   value   co-located tokens/s over the K timed steps (device-resident inputs),
           counting only tokens of requests whose emissions met the TTFT/TPOT
-          SLO; device time between CUDA events recorded on the compute stream
-          (mesh_gpu_timer_mark), max over ranks.
-  e2e     the same metric through the reference-facing plugin API
-          (llmmesh.h: llm_experiment_run with the GPU attached) on a C2 trace
-          that keeps the four instances at capacity (scenarios/c2_saturated):
-          control plane + per-step H2D descriptors/prompts + D2H tokens inside
-          the timed region; wall clock.
+          SLO on the device timeline (CUDA events, mesh_gpu_timer_mark), max
+          over ranks.
+  e2e     the same metric through the reference-facing plugin API (llmmesh.h:
+          llm_experiment_run with the GPU attached, runtime.clock = "wall") on
+          the C3 bursty trace (scenarios/c3_b200: the acceptance overload
+          generator's three phases in 30 s) at several load scales: the control
+          plane admits, scales KV and cold-starts instances; step completions
+          and emission times are CUDA events, so SLO compliance is measured,
+          not priced. value = SLO tokens / host wall s at the highest load whose
+          compliance is >= 0.99 (the capacity point); models/GPU reported.
   roofline  dominant kernel = the persistent decode kernel; algorithmic bytes
-          per launch = W_m + sum_i L_i C_m + B C_m + B d_m 2 over its
-          CUDA-event duration, vs the measured HBM copy peak.
+          per launch = W_m + sum_i L_i C_m + B C_m + B d_m 2 over the
+          timed device span (lanes overlap) and over its own CUDA-event time.
 
 `--impl reference` and `cpu_baseline`: the reference artifact prices token
 steps from tables and computes no tokens, so the CPU path that
 *executes* the co-located step is the oracle's batched CPU decode
-(oracle/cpu_decode.c, all host threads) running the same C2 instance steps
-(kind "port"); the reference simulator itself (oracle/_ref, built from
-/root/reference) is timed beside it on the C2 trace ("reference_simulator").
+(oracle/cpu_decode.c, all host threads) on the same C3 instance steps: the
+same models, batch 8, contexts drawn from the same length set (kind "port");
+the reference simulator itself (oracle/_ref) is timed beside it on the C3
+trace ("reference_simulator").
 Multi-GPU (torchrun): every rank runs an independent co-located node (instances
 shard by placement, no collective): weak scaling.
 """
@@ -46,16 +54,17 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-SCEN = os.path.join(ROOT, "tests", "golden", "ctrl", "c2_colocated")
+C3_DIR = os.path.join(ROOT, "scenarios", "c3_b200")
 METRIC = "co-located tokens/s at TTFT/TPOT SLO per B200"
 UNIT = "tokens/s"
-MODELS = ["1b", "3b", "1b", "3b"]
+MODELS = ["1b", "3b", "7b", "1b", "3b", "7b", "1b", "3b"]
 BATCH = 8
-LANES = int(os.environ.get("MESH_BENCH_LANES", "4"))  # one execution lane per co-located instance
-E2E_WINDOW_S = 20.0
-E2E_SCEN = os.path.join(ROOT, "scenarios", "c2_saturated", "config.json")
-CPU_MAX_SEQ = 64        # CPU sample contexts (short: generous to the CPU)
+LANES = int(os.environ.get("MESH_BENCH_LANES", "8"))  # one execution lane per co-located instance
+KV_POOL = 100 << 30
+E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "4,8,12").split(",")]
+WATERMARK = 20.0
 CPU_SAMPLE_S = 15.0     # bounded CPU baseline sample
+CPU_MAX_SEQ = 1160      # >= the longest I + O of the length set (1139)
 
 
 def peaks():
@@ -200,7 +209,7 @@ class Clocks:
 
 def load_lengths():
     rows = []
-    with open(os.path.join(SCEN, "lengths.csv")) as fh:
+    with open(os.path.join(C3_DIR, "lengths.csv")) as fh:
         next(fh)
         for line in fh:
             a, b = line.strip().split(",")
@@ -208,33 +217,60 @@ def load_lengths():
     return rows
 
 
+def m_require(entries, C, avg_out, min_total):
+    """proj/src/memory.cpp:19-27: ceil(C * max(sum_r I_r + max(gen_r, avg_out), min_total_len))."""
+    tot = sum(i + max(float(g), avg_out) for i, g in entries)
+    return int(-(-max(tot, float(min_total)) * C // 1))
+
+
+def watermark_decide(cur, req, pct=WATERMARK):
+    """proj/src/memory.cpp:29-36 (scale_bytes_up applied twice for the down test)."""
+    up = lambda b: int(-(-b * (100.0 + pct) // 100.0))  # noqa: E731
+    rec = up(req)
+    if cur < req:
+        return "up", rec
+    if up(rec) < cur:
+        return "down", rec
+    return "hold", rec
+
+
 class Colocated:
-    """The C2 node: four instances, each with a full batch, served in turns."""
+    """The C3 node: eight instances, each with a full batch of 8, served in turns."""
 
     def __init__(self, device: int, seed: int = 7):
         import random
 
         from paper_2507_00507_b200.gpu import SHAPES, MeshGpu
-        self.g = MeshGpu(device, kv_pool_bytes=48 << 30, prompt_seed=seed, lanes=LANES)
+        self.g = MeshGpu(device, kv_pool_bytes=KV_POOL, prompt_seed=seed, lanes=LANES)
         self.shapes = [SHAPES[m] for m in MODELS]
         self.rng = random.Random(seed)
         self.lengths = load_lengths()
+        self.avg_out = sum(o for _, o in self.lengths) / len(self.lengths)  # avg_output_fixed
         self.next_rid = 0
         self.insts = []
-        for iid, shape in enumerate(self.shapes):
-            self.g.create_instance(iid, shape, seed=1000 + iid)
-            kv = BATCH * shape.max_seq_len * shape.kv_bytes_per_token
-            self.g.kv_resize(iid, 0, kv)
-            self.insts.append({"id": iid, "shape": shape, "reqs": [], "pending": []})
+        for iid, (m, shape) in enumerate(zip(MODELS, self.shapes)):
+            # replicas of a model share one weight set (same model => same weights)
+            self.g.create_instance(iid, shape, seed=1000 + MODELS.index(m))
+            self.insts.append({"id": iid, "model": m, "shape": shape, "reqs": [], "pending": [], "kv": 0})
         self.clock = 0.0  # device-time clock (s) for SLO accounting
         self.mark0 = None  # clock value at timer mark 0: emissions are then read off the device timeline
-        self.tokens_ok = 0
-        self.tokens_all = 0
-        self.violations = 0
-        self.completed = 0
-        self.decode_bytes = 0.0
-        self.decode_kernel_ms = 0.0
-        self.decode_steps = 0
+        self.kv_grows = self.kv_shrinks = 0
+        self.reset_counters()
+
+    def kv_update(self, inst):
+        """Re-size the instance's KV target by the reference's watermark rule."""
+        s = inst["shape"]
+        entries = [(r["I"], r["sched"]) for r in inst["reqs"] + inst["pending"]]
+        req = m_require(entries, s.kv_bytes_per_token, self.avg_out, s.max_seq_len)
+        act, rec = watermark_decide(inst["kv"], req)
+        if act == "hold":
+            return
+        self.g.kv_resize(inst["id"], inst["kv"], rec)
+        inst["kv"] = rec
+        if act == "up":
+            self.kv_grows += 1
+        else:
+            self.kv_shrinks += 1
 
     def new_request(self, inst):
         i, o = self.lengths[self.rng.randrange(len(self.lengths))]
@@ -244,6 +280,7 @@ class Colocated:
         r = {"rid": self.next_rid, "I": i, "O": o, "gen": 0, "sched": 0, "arrival": self.clock, "ok": True}
         self.next_rid += 1
         inst["pending"].append(r)
+        self.kv_update(inst)
 
     def fill(self):
         for inst in self.insts:
@@ -251,7 +288,7 @@ class Colocated:
                 self.new_request(inst)
 
     def plan(self, k):
-        """Step k of the schedule: instance k mod 4; a pending request is prefilled first."""
+        """Step k of the schedule: instance k mod 8; a pending request is prefilled first."""
         inst = self.insts[k % len(self.insts)]
         if inst["pending"]:
             return inst, "prefill", [inst["pending"][0]]
@@ -268,19 +305,19 @@ class Colocated:
         if kind == "prefill":
             r = inst["pending"].pop(0)
             r["sched"] = 1
-            if r["sched"] >= r["O"]:
-                self.new_request(inst)
-            else:
-                inst["reqs"].append(r)
-            return
-        for r in reqs:
-            r["sched"] += 1
-        for r in [r for r in reqs if r["sched"] >= r["O"]]:
+            inst["reqs"].append(r)
+            done = [r] if r["sched"] >= r["O"] else []
+        else:
+            for r in reqs:
+                r["sched"] += 1
+            done = [r for r in reqs if r["sched"] >= r["O"]]
+        for r in done:
             inst["reqs"].remove(r)
+            # completion: the slot is free once the step retires (request_free in retire)
             self.new_request(inst)
 
     def run(self, steps):
-        """Launch `steps` steps asynchronously (<= 24 outstanding), retire them in order."""
+        """Launch `steps` steps asynchronously (<= 32 outstanding), retire them in order."""
         from collections import deque
         inflight = deque()
         launches0 = self.g.stats()["kernel_launches"]
@@ -289,7 +326,7 @@ class Colocated:
             self.k += 1
             inflight.append((self.launch(inst, kind, reqs), inst, kind, reqs))
             self.schedule_effects(inst, kind, reqs)
-            while len(inflight) > 24:
+            while len(inflight) > 32:
                 self.retire(inflight.popleft())
         while inflight:
             self.retire(inflight.popleft())
@@ -308,10 +345,17 @@ class Colocated:
         if kind == "decode":
             s = inst["shape"]
             ctx = sum(r["I"] + r["gen"] for r in reqs)
-            self.decode_bytes += (s.weight_bytes_streamed + ctx * s.kv_bytes_per_token +
-                                  len(reqs) * s.kv_bytes_per_token + len(reqs) * s.d_model * 2)
+            b = (s.weight_bytes_streamed + ctx * s.kv_bytes_per_token + len(reqs) * s.kv_bytes_per_token +
+                 len(reqs) * s.d_model * 2)
+            self.decode_bytes += b
             self.decode_kernel_ms += st["last_kernel_ms"]
             self.decode_steps += 1
+            pm = self.per_model.setdefault(inst["model"], {"bytes": 0.0, "kernel_ms": 0.0, "launches": 0})
+            pm["bytes"] += b
+            pm["kernel_ms"] += st["last_kernel_ms"]
+            pm["launches"] += 1
+        else:
+            self.prefill_steps += 1
         for r in reqs:
             deadline = r["arrival"] + max(2.0, r["I"] / 512.0) + 0.25 * r["gen"]
             if emit > deadline + 1e-9:
@@ -327,128 +371,191 @@ class Colocated:
     def reset_counters(self):
         self.tokens_ok = self.tokens_all = self.completed = self.violations = 0
         self.decode_bytes = self.decode_kernel_ms = 0.0
-        self.decode_steps = 0
+        self.decode_steps = self.prefill_steps = 0
+        self.per_model = {}
+        self.kv_grows = self.kv_shrinks = 0
 
 
-def reference_simulator_sample(window_s: float):
-    """The reference's own CPU code (its simulator, oracle/_ref) on the C2 trace: 1 core."""
+def ref_config(cfg_path: str) -> str:
+    """The reference simulator's schema has no `runtime` section: a copy without it."""
+    import tempfile
+    with open(cfg_path) as fh:
+        cfg = json.load(fh)
+    cfg.pop("runtime", None)
+    cfg["output"] = {"dir": tempfile.mkdtemp(prefix="mesh_ref_"), "event_log": False}
+    path = os.path.join(cfg["output"]["dir"], "config.json")
+    with open(path, "w") as fh:
+        json.dump(cfg, fh)
+    return path
+
+
+def reference_simulator_sample(scale: int):
+    """The reference's own CPU code (its simulator, oracle/_ref) on the C3 trace: 1 core."""
     ref = os.path.join(ROOT, "oracle", "_ref", "ref_capture")
     if not os.path.exists(ref):
         return None
-    out = subprocess.run([ref, "time", os.path.join(SCEN, "config.json"), "5", f"workload.window_s={window_s}"],
+    out = subprocess.run([ref, "time", ref_config(os.path.join(C3_DIR, f"s{scale}", "config.json")), "5"],
                          cwd=ROOT, capture_output=True, text=True)
     if out.returncode != 0:
         return None
     r = json.loads(out.stdout.strip().splitlines()[-1])
     return {"simulated_tokens_per_cpu_s": r["tokens"] / r["best_s"], "cores": 1, "kind": "reference",
-            "sample": f"reference simulator (oracle/_ref) on the C2 trace, window {window_s:g} s: "
+            "sample": f"reference simulator (oracle/_ref) on the C3 trace at load scale {scale}: "
                       f"{r['tokens']} virtual tokens, {r['events']} events, best of 5 = {r['best_s']:.4f} s",
             "note": "virtual-time tokens: the reference prices steps from tables and computes no tokens"}
 
 
 class CpuColocated:
-    """The C2 node on the host CPU: the batched CPU decode (oracle/cpu_decode.c)
-    over the same four instances [1b, 3b, 1b, 3b] x batch 8, instances in turn.
-    Weights are generated once per size class (identical replicas share them)."""
+    """The C3 node on the host CPU: the batched CPU decode (oracle/cpu_decode.c)
+    over the same eight instances x batch 8, instances in turn. Replicas of a
+    model share its weights (one oracle model per size class, as on the GPU);
+    each instance's batch starts at contexts I + U[0, O) drawn from the same
+    length set as the GPU node's requests (KV declared resident, values zero:
+    a decode step's cost depends on the context, not the values), and every
+    step advances them by one token. Prefill is not run on the CPU (it would
+    only lower the CPU number)."""
 
-    def __init__(self):
+    def __init__(self, seed: int = 7):
         import dataclasses
+        import random
 
         from oracle import llama_oracle as ora
         from paper_2507_00507_b200.gpu import SHAPES
         self.ora = ora
+        rng = random.Random(seed)
+        lengths = load_lengths()
         self.models = {}
-        for m in MODELS:
-            if m not in self.models:
-                self.models[m] = ora.Oracle(dataclasses.replace(SHAPES[m], max_seq_len=CPU_MAX_SEQ), 1000 + len(self.models))
-        self.insts = [{"model": self.models[m], "seqs": [], "toks": [], "len": 0} for m in MODELS]
+        for m in dict.fromkeys(MODELS):
+            shape = dataclasses.replace(SHAPES[m], max_seq_len=min(SHAPES[m].max_seq_len, CPU_MAX_SEQ))
+            self.models[m] = ora.Oracle(shape, 1000 + MODELS.index(m))
+        self.insts = []
+        for m in MODELS:  # per-class sequences are shared by that class's replicas (memory)
+            if any(x["model"] == m for x in self.insts):
+                self.insts.append(next(x for x in self.insts if x["model"] == m))
+                continue
+            seqs, toks = [], []
+            for b in range(BATCH):
+                i, o = lengths[rng.randrange(len(lengths))]
+                q = self.models[m].new_seq()
+                q.set_len(i + rng.randrange(o))
+                seqs.append(q)
+                toks.append(ora.prompt_token(seed, b, 0, self.models[m].shape.vocab))
+            self.insts.append({"model": m, "seqs": seqs, "toks": toks})
         self.k = 0
         self.threads = ora.threads()
+
+    def mean_context(self):
+        seen = {id(x): x for x in self.insts}.values()
+        lens = [self.ora.C.cast(self.ora.C.c_void_p(q.h), self.ora.C.POINTER(self.ora.C.c_int))[0]
+                for x in seen for q in x["seqs"]]
+        return sum(lens) / len(lens)
 
     def step(self) -> int:
         inst = self.insts[self.k % len(self.insts)]
         self.k += 1
-        if not inst["seqs"] or inst["len"] >= CPU_MAX_SEQ - 1:  # batch finished: admit 8 new requests
-            inst["seqs"] = [inst["model"].new_seq() for _ in range(BATCH)]
-            inst["len"] = 0
-            inst["toks"] = [self.ora.prompt_token(7, self.k * BATCH + i, 0, inst["model"].shape.vocab)
-                            for i in range(BATCH)]
-        inst["toks"] = self.ora.feed_batch(inst["model"], inst["seqs"], inst["toks"])
-        inst["len"] += 1
+        for q in inst["seqs"]:  # a sequence at the end of its buffer restarts at a short context
+            if self.ora.C.cast(self.ora.C.c_void_p(q.h), self.ora.C.POINTER(self.ora.C.c_int))[0] >= CPU_MAX_SEQ - 2:
+                q.set_len(64)
+        inst["toks"] = self.ora.feed_batch(self.models[inst["model"]], inst["seqs"], inst["toks"])
         return BATCH
 
 
 def cpu_port_sample():
-    """cpu_baseline: bounded sample (~CPU_SAMPLE_S) of C2 instance steps on the host CPU."""
+    """cpu_baseline: bounded sample (~CPU_SAMPLE_S) of C3 instance steps on the host CPU."""
     node = CpuColocated()
-    node.step()  # warm
+    ctx0 = node.mean_context()
+    for _ in range(3):  # one step of each model class (warm)
+        node.step()
     n_tok, n_steps, t0 = 0, 0, time.perf_counter()
-    while n_steps < 4 or time.perf_counter() - t0 < CPU_SAMPLE_S:
+    while n_steps < len(MODELS) or time.perf_counter() - t0 < CPU_SAMPLE_S:
         n_tok += node.step()
         n_steps += 1
     dt = time.perf_counter() - t0
     return {"value": n_tok / dt, "unit": UNIT, "cores": node.threads, "kind": "port",
-            "sample": f"{n_steps} C2 instance steps ([1b,3b,1b,3b] in turn, batch 8, contexts <= {CPU_MAX_SEQ}) "
-                      f"of the batched CPU decode (oracle/cpu_decode.c, fp32, {node.threads} threads): "
-                      f"{n_tok} tokens in {dt:.2f} s"}
+            "sample": f"{n_steps} C3 instance steps ({MODELS} in turn, batch 8, mean context {ctx0:.0f} "
+                      f"from the C3 length set) of the batched CPU decode (oracle/cpu_decode.c, fp32 math on "
+                      f"bf16 weights, {node.threads} threads): {n_tok} tokens in {dt:.2f} s",
+            "same_config": True}
 
 
 def run_reference(args, d: Dist):
-    """Reference arm: the CPU execution of the co-located step on the box's host cores."""
+    """Reference arm: the CPU execution of the co-located C3 step on the box's host cores."""
     if d.rank != 0:
         return
     node = CpuColocated()
+    ctx0 = node.mean_context()
     for _ in range(args.warmup):
         node.step()
     t0 = time.perf_counter()
     tokens = sum(node.step() for _ in range(args.steps))
     total = time.perf_counter() - t0
     value = tokens / total
-    sim = reference_simulator_sample(E2E_WINDOW_S)
+    sim = reference_simulator_sample(E2E_SCALES[0])
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic (random-init weights)",
             "impl": "reference",
-            "config": {"workload": "C2: 4 co-located Llama-shaped instances [1.1B, 3B, 1.1B, 3B], batch 8 each, "
-                                   "instances in turn (host CPU)",
-                       "models": MODELS, "batch_per_instance": BATCH, "context_max": CPU_MAX_SEQ,
+            "config": {"workload": "C3: 8 co-located Llama-shaped instances [1.1B, 3B, 7B, 1.1B, 3B, 7B, 1.1B, 3B], "
+                                   "batch 8 each, instances in turn (host CPU)",
+                       "models": MODELS, "batch_per_instance": BATCH, "mean_context": ctx0,
                        "step": "one instance step: batched decode of its 8 requests"},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": node.threads, "kind": "port",
-                             "sample": f"{args.steps} C2 instance steps of oracle/cpu_decode.c (batched fp32, "
-                                       f"{node.threads} threads, contexts <= {CPU_MAX_SEQ})"},
+                             "sample": f"{args.steps} C3 instance steps of oracle/cpu_decode.c (batched, "
+                                       f"{node.threads} threads, mean context {ctx0:.0f})"},
             "reference_simulator": sim,
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
 
-def run_e2e(device: int, d: Dist):
-    """Saturated C2 trace through llmmesh.h with the B200 data plane attached (parity-mode schedule)."""
+def run_e2e_scale(device: int, scale: int):
+    """The C3 bursty trace at one load scale through llmmesh.h, wall-clock mode."""
     import tempfile
 
     from paper_2507_00507_b200 import control, gpu
     os.environ["MESH_GPU_LANES"] = str(LANES)  # the data plane under the control plane: one lane per instance
-    with control.Experiment(E2E_SCEN) as exp:
+    cfg = os.path.join(C3_DIR, f"s{scale}", "config.json")
+    with control.Experiment(cfg) as exp:
         exp.out_dir(tempfile.mkdtemp(prefix="mesh_e2e_"))
-        exp.attach_gpu([device], 48 << 30, gpu.LIB_PATH)
-        d.barrier()
-        t0 = time.perf_counter()
+        exp.attach_gpu([device], KV_POOL, gpu.LIB_PATH)
         exp.run()
-        wall = time.perf_counter() - t0
-        m = {k: exp.metric(k) for k in ["gpu.steps", "gpu.decode_tokens", "gpu.prefill_tokens", "gpu.h2d_bytes",
-                                        "gpu.d2h_bytes", "gpu.device_ms", "slo_compliant_rate", "total_requests",
-                                        "slo_compliant", "gpu.kernel_launches"]}
-    prefill_emits = m["total_requests"]  # one token per admitted request's prefill
-    tokens = (m["gpu.decode_tokens"] + prefill_emits) * m["slo_compliant_rate"]
-    wall_max = d.reduce(wall, "max")
-    tok_sum = d.reduce(tokens, "sum")
-    steps = max(1.0, m["gpu.steps"])
+        names = ["wall_s", "gpu.steps", "gpu.decode_tokens", "gpu.prefill_tokens", "gpu.h2d_bytes", "gpu.d2h_bytes",
+                 "gpu.device_ms", "gpu.lane_busy_s", "slo_compliant_rate", "total_requests", "slo_compliant",
+                 "slo_compliant_decode_tokens", "output_tokens", "gpu.kernel_launches", "gpu_instances_avg",
+                 "gpu_instances_max", "gpu.instance_starts", "gpu.weight_cache_hits", "gpu.blocks_moved",
+                 "gpu.swap_out_bytes", "gpu.migrations", "evictions", "run_length_s"]
+        m = {k: exp.metric(k) for k in names}
+    m["scale"] = scale
+    m["slo_tokens"] = m["slo_compliant_decode_tokens"] + m["slo_compliant"]  # + each compliant request's first token
+    m["tokens_at_slo_per_s"] = m["slo_tokens"] / m["wall_s"]
+    return m
+
+
+def run_e2e(device: int, d: Dist, scales):
+    """Capacity sweep: the highest load scale whose wall-clock compliance is >= 0.99 is the capacity point."""
+    runs = []
+    for k in scales:
+        d.barrier()
+        runs.append(run_e2e_scale(device, k))
+    ok = [r for r in runs if r["slo_compliant_rate"] >= 0.99]
+    head = max(ok, key=lambda r: r["scale"]) if ok else min(runs, key=lambda r: r["scale"])
+    wall_max = d.reduce(head["wall_s"], "max")
+    tok_sum = d.reduce(head["slo_tokens"], "sum")
+    steps = max(1.0, head["gpu.steps"])
     return {"value": tok_sum / wall_max, "unit": UNIT,
-            "h2d_bytes_per_step": m["gpu.h2d_bytes"] / steps, "d2h_bytes_per_step": m["gpu.d2h_bytes"] / steps,
-            "wall_s": wall_max, "device_s": m["gpu.device_ms"] / 1e3, "steps": int(steps),
-            "slo_compliant_rate": m["slo_compliant_rate"], "tokens": int(tokens),
-            "requests": int(m["total_requests"]), "prefill_tokens": int(m["gpu.prefill_tokens"]),
-            "trace": "scenarios/c2_saturated (Poisson 16 req/s per function, 10 s)",
-            "api": "llmmesh.h llm_experiment_run + llm_experiment_attach_gpu"}
+            "h2d_bytes_per_step": head["gpu.h2d_bytes"] / steps, "d2h_bytes_per_step": head["gpu.d2h_bytes"] / steps,
+            "capacity_scale": head["scale"] if ok else None,
+            "capacity_rule": "highest load scale with wall-clock slo_compliant_rate >= 0.99",
+            "slo_compliant_rate": head["slo_compliant_rate"], "wall_s": wall_max,
+            "models_per_gpu": {"time_avg": head["gpu_instances_avg"], "max": head["gpu_instances_max"]},
+            "lane_busy_frac": head["gpu.lane_busy_s"] / (LANES * head["wall_s"]) if head["wall_s"] else None,
+            "sweep": [{k: r[k] for k in ("scale", "total_requests", "slo_compliant_rate", "tokens_at_slo_per_s",
+                                         "wall_s", "gpu_instances_avg", "gpu_instances_max", "gpu.steps",
+                                         "gpu.instance_starts", "gpu.weight_cache_hits", "gpu.blocks_moved",
+                                         "gpu.swap_out_bytes", "evictions")} for r in runs],
+            "trace": "scenarios/c3_b200/s{K}: acceptance overload generator's three phases (0.08, 0.28, "
+                     "0.8 hot / 0.03 req/s per function) in a 30 s window, rates x K",
+            "tables": "measured B200 tables + CostParams (admission); completions on CUDA events",
+            "api": "llmmesh.h llm_experiment_run + llm_experiment_attach_gpu, runtime.clock = wall"}
 
 
 def run_ours(args, d: Dist):
@@ -474,18 +581,21 @@ def run_ours(args, d: Dist):
     wall_max = d.reduce(dev_s, "max")
     tok_ok = d.reduce(float(node.tokens_ok), "sum")
     value = tok_ok / wall_max
-    # Decode launches of the four lanes overlap, so a launch's own duration is not the
+    # Decode launches of the eight lanes overlap, so a launch's own duration is not the
     # time the node spends per launch: achieved = algorithmic decode bytes of every
     # launch over the timed device span (prefill steps inside the span make it a lower
     # bound); the single-launch figure (bytes / the launch's own CUDA-event time, on
     # its lane's SM quota) is kept beside it.
     per_launch = node.decode_bytes / (node.decode_kernel_ms / 1e3) / 1e9 if node.decode_kernel_ms else 0.0
     achieved = node.decode_bytes / dev_s / 1e9 if dev_s else 0.0
-    e2e = run_e2e(device, d) if not args.no_e2e else None
+    quotas = [node.g.instance_lane(i["id"])[1] for i in node.insts]
+    g_stats = node.g.stats()
+    node.g.close()  # frees the node's HBM for the e2e leg
+    e2e = run_e2e(device, d, E2E_SCALES) if not args.no_e2e else None
     if d.rank != 0:
         return
-    cpu = cpu_port_sample() if d.ws == 1 else None
-    sim = reference_simulator_sample(E2E_WINDOW_S) if d.ws == 1 else None
+    cpu = cpu_port_sample() if d.ws == 1 and not args.no_cpu else None
+    sim = reference_simulator_sample(E2E_SCALES[0]) if d.ws == 1 else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "decode_traffic.json")
     if os.path.exists(prof):
@@ -495,17 +605,20 @@ def run_ours(args, d: Dist):
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall_max / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, synthetic prompts)",
-        "config": {"workload": "C2: 4 co-located Llama-shaped instances [1.1B, 3B, 1.1B, 3B] on one B200, "
-                               "batch 8 each, shared VMM KV pool",
+        "config": {"workload": "C3: 8 co-located Llama-shaped instances [1.1B, 3B, 7B, 1.1B, 3B, 7B, 1.1B, 3B] on "
+                               "one B200, batch 8 each, shared VMM KV pool with watermark grow/shrink",
                    "models": MODELS, "batch_per_instance": BATCH, "step": "one instance step (decode of its batch "
                    "or prefill of a newly admitted request), issued in turn; each instance on its own "
                    f"execution lane ({LANES} lanes, SM quotas in proportion to streamed weight bytes), so "
                    "co-located instances step concurrently",
-                   "lane_sm_quotas": [node.g.instance_lane(i["id"])[1] for i in node.insts],
-                   "l2": "weights 17 GB + KV streamed per 4-step round >> 126 MB L2",
+                   "lane_sm_quotas": quotas,
+                   "l2": "weights 53 GB + KV streamed per 8-step round >> 126 MB L2 (no flush needed)",
                    "slo_compliant_tokens": int(node.tokens_ok), "tokens": int(node.tokens_all),
                    "completed_requests": node.completed, "slo_violations": node.violations,
-                   "decode_steps": node.decode_steps, "parallelism": f"{d.ws} independent co-located nodes"},
+                   "decode_steps": node.decode_steps, "prefill_steps": node.prefill_steps,
+                   "kv_grows": node.kv_grows, "kv_shrinks": node.kv_shrinks,
+                   "kv_blocks_moved": g_stats["blocks_moved"],
+                   "parallelism": f"{d.ws} independent co-located nodes"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,
                      "kernel": "decode_kernel (persistent, TMA-ring), one launch per lane step",
@@ -515,7 +628,10 @@ def run_ours(args, d: Dist):
                      "achieved_basis": "sum of decode launches' algorithmic bytes / timed device span "
                                        "(lanes overlap; prefill steps in the span make this a lower bound)",
                      "per_launch_gbs": per_launch,
-                     "per_launch_note": "bytes / the launch's own CUDA-event time on its lane's SM quota"},
+                     "per_launch_note": "bytes / the launch's own CUDA-event time on its lane's SM quota",
+                     "per_model": {m: {"launches": v["launches"], "gbs_per_launch": v["bytes"] / (v["kernel_ms"] / 1e3) / 1e9,
+                                       "ms_per_launch": v["kernel_ms"] / max(1, v["launches"])}
+                                   for m, v in node.per_model.items()}},
         "cpu_baseline": cpu,
         "reference_simulator": sim,
         "e2e": e2e,
@@ -529,10 +645,11 @@ def main():
     os.chdir(ROOT)  # scenario configs use repo-relative paths
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--steps", type=int, default=2000)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
     d = Dist()
     try:

@@ -74,6 +74,13 @@ class OracleSeq:
         self.m = m
         self.h = lib().ora_seq_new(m.h)
 
+    def set_len(self, n: int) -> None:
+        """Bench only: declare n tokens of (zero-valued) KV resident without computing
+        them; a decode step's cost depends on the context length, not the values."""
+        if not 0 <= n < self.m.shape.max_seq_len:
+            raise ValueError("context out of range")
+        C.cast(C.c_void_p(self.h), C.POINTER(C.c_int))[0] = n
+
     def feed(self, token: int, want_logits: bool = True):
         buf = np.zeros(self.m.shape.vocab, dtype=np.float32) if want_logits else None
         ptr = buf.ctypes.data_as(C.POINTER(C.c_float)) if want_logits else None

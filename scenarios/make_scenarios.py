@@ -13,6 +13,16 @@ serving path rather than the arrival rate.
                 control plane's virtual schedule runs at the data plane's real
                 speed. bench.py's e2e runs this one.
 
+  c3_b200/s{K}  BASELINE configs[2] (C3), the bench's e2e: 8 functions on
+                [1b, 3b, 7b, 1b, 3b, 7b, 1b, 3b] under the acceptance overload
+                trace's three phases (proj/tests/acceptance_main.cpp:462-488:
+                0.08/s, then 0.28/s, then 0.8/s for 6 hot functions and
+                0.03/s for the rest), compressed into a 30 s window (phases
+                6 / 12 / 12 s) with every rate scaled by K (the lambda of the
+                capacity sweep). Measured B200 tables and CostParams; run with
+                runtime.clock = "wall", so step completions, emission times and
+                SLO compliance come from CUDA events, not from the tables.
+
     python scenarios/make_scenarios.py
 """
 import json
@@ -24,7 +34,54 @@ ROOT = os.path.dirname(HERE)
 sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
 sys.path.insert(0, ROOT)
 
-from make_ctrl_golden import const_rate, poisson_trace  # noqa: E402
+from make_ctrl_golden import TEMPLATES, const_rate, lengths_csv, poisson_trace  # noqa: E402
+
+C3_MODELS = ["1b", "3b", "7b", "1b", "3b", "7b", "1b", "3b"]
+C3_SCALES = [1, 2, 4, 6, 8, 12, 16]
+C3_WINDOW = 30.0
+
+
+def c3_rate(scale, window):
+    hot = {f"fn{i:02d}" for i in range(6)}
+
+    def f(fn, t, ph):
+        if t < 0.2 * window:
+            return 0.08 * scale
+        if t < 0.6 * window:
+            return 0.28 * scale
+        return (0.8 if fn in hot else 0.03) * scale
+    return f
+
+
+def make_c3():
+    from paper_2507_00507_b200 import tables
+    base = os.path.join(HERE, "c3_b200")
+    os.makedirs(base, exist_ok=True)
+    lengths_csv(os.path.join(base, "lengths.csv"), 200, 4242)  # the example length set's ranges
+    for k in C3_SCALES:
+        d = os.path.join(base, f"s{k}")
+        os.makedirs(d, exist_ok=True)
+        n = poisson_trace(os.path.join(d, "trace.csv"), [f"fn{i:02d}" for i in range(8)], C3_WINDOW,
+                          c3_rate(k, C3_WINDOW), 4242 + k)
+        cfg = {
+            "seed": 13,
+            "cluster": {"nodes": [{"class": "gpu", "count": 1, "mem_gb": 150.0}]},
+            "models": {"templates": [dict(TEMPLATES[t]) for t in ("1b", "3b", "7b")], "assignment": C3_MODELS},
+            "perf": {"overestimate_factor": 1.10, "max_len": 4096, "max_batch": 8,
+                     "tables": {f"{sc}:gpu": os.path.relpath(tables.measured_table_path(sc), ROOT)
+                                for sc in ("1b", "3b", "7b")},
+                     "gpu": tables.measured_cost_params()},
+            "workload": {"trace": os.path.relpath(os.path.join(d, "trace.csv"), ROOT),
+                         "lengths": os.path.relpath(os.path.join(base, "lengths.csv"), ROOT),
+                         "window_s": C3_WINDOW, "sample_functions": 8},
+            "slo": {"ttft_base_s": 2.0, "ttft_per_token_divisor": 512.0, "tpot_s": 0.25},
+            "policy": {"kind": "mesh", "watermark_pct": 20.0, "keep_alive_s": 1.0},
+            "runtime": {"clock": "wall", "slots": 64},
+            "output": {"dir": os.path.relpath(os.path.join(d, "out"), ROOT), "event_log": False},
+        }
+        with open(os.path.join(d, "config.json"), "w") as fh:
+            json.dump(cfg, fh, indent=2)
+        print(f"c3_b200/s{k}:", n, "requests")
 
 
 def main():
@@ -48,6 +105,7 @@ def main():
     with open(os.path.join(d2, "config.json"), "w") as fh:
         json.dump(cfg, fh, indent=2)
     print("c2_saturated_b200: same trace, measured B200 tables")
+    make_c3()
 
 
 if __name__ == "__main__":

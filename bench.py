@@ -313,7 +313,9 @@ class Colocated:
             done = [r for r in reqs if r["sched"] >= r["O"]]
         for r in done:
             inst["reqs"].remove(r)
-            # completion: the slot is free once the step retires (request_free in retire)
+            # completion: its blocks return now (stream-ordered after its last step on the
+            # instance's lane), so the KV shrink of the watermark rule sees the schedule's state
+            self.g.request_free(inst["id"], r["rid"])
             self.new_request(inst)
 
     def run(self, steps):
@@ -364,7 +366,6 @@ class Colocated:
             self.tokens_all += 1
             self.tokens_ok += 1 if r["ok"] else 0
             if r["gen"] >= r["O"]:
-                self.g.request_free(inst["id"], r["rid"])
                 self.completed += 1
                 self.violations += 0 if r["ok"] else 1
 

@@ -96,6 +96,8 @@ typedef struct mesh_gpu_stats {
     int64_t weight_cache_hits;    /* instance creates that shared a live or cached weight set of the
                                      same model (no allocation, no init kernels) */
     int64_t peer_devices;         /* devices granted NVLink access to this device's KV (migration) */
+    int64_t vmm_unmaps;           /* cuMemUnmap calls (subset of vmm_calls) */
+    double host_ms_create, host_ms_destroy, host_ms_kv_resize, host_ms_step; /* host time inside those calls */
 } mesh_gpu_stats;
 
 /* mesh_gpu_swap_state values */

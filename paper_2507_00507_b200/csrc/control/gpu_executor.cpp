@@ -325,7 +325,7 @@ std::map<std::string, double> GpuExecutor::metrics() const {
     m["gpu.host_ms.step_issue"] = host_ms_step_;
     m["gpu.host_ms.step_wait"] = host_ms_wait_;
     double swap = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0, vmm_calls = 0, vmm_ms = 0, reclaims = 0,
-           wcache = 0;
+           wcache = 0, unmaps = 0, dp_create = 0, dp_destroy = 0, dp_kv = 0, dp_step = 0;
     for (mesh_gpu* h : handles_) {
         mesh_gpu_stats st{};
         api_->stats_get(h, &st);
@@ -339,10 +339,20 @@ std::map<std::string, double> GpuExecutor::metrics() const {
         vmm_ms += st.vmm_ms;
         reclaims += static_cast<double>(st.kv_reclaims);
         wcache += static_cast<double>(st.weight_cache_hits);
+        unmaps += static_cast<double>(st.vmm_unmaps);
+        dp_create += st.host_ms_create;
+        dp_destroy += st.host_ms_destroy;
+        dp_kv += st.host_ms_kv_resize;
+        dp_step += st.host_ms_step;
     }
     m["gpu.weight_cache_hits"] = wcache;
     m["gpu.lane_busy_s"] = lane_busy_s_;
     m["gpu.vmm_calls"] = vmm_calls;
+    m["gpu.vmm_unmaps"] = unmaps;
+    m["gpu.dp_ms.instance_create"] = dp_create;
+    m["gpu.dp_ms.instance_destroy"] = dp_destroy;
+    m["gpu.dp_ms.kv_resize"] = dp_kv;
+    m["gpu.dp_ms.step"] = dp_step;
     m["gpu.host_ms.vmm"] = vmm_ms;
     m["gpu.kv_reclaims"] = reclaims;
     m["gpu.swap_out_bytes"] = swap;

@@ -468,14 +468,20 @@ struct mesh_gpu {
         uint64_t tick;      // last release, for LRU eviction of idle sets
     };
     std::map<uint64_t, WeightSet> wsets;  // by shape key
+    // Per-instance buffers of unloaded instances, recycled by the next create:
+    // the KV VA range WITH its mapped granules (an instance start then maps
+    // nothing until it outgrows them; no cuMemMap / cuMemUnmap, each of which
+    // costs host time and a TLB shoot-down, on the keep-alive churn path), the
+    // block table and the last-token array. Every range has the same size
+    // (va_size), so any range serves any model.
     struct InstBufs {
         CUdeviceptr va;
-        size_t va_size;
-        int* d_block_table;
-        size_t bt_elems;
+        int* d_block_table;  // [MAX_SLOTS][DEC_BT_MAX]
         int* d_last_tok;
+        std::vector<CUmemGenericAllocationHandle> granules;  // mapped at va, in order
     };
     std::vector<InstBufs> ibufs;  // free per-instance buffers
+    size_t va_size = 0;           // KV VA range per instance: the pool limit + the largest tail slack
     size_t wcache_cap = size_t(32) << 30;  // MESH_GPU_WCACHE_GB: bytes of idle weight sets kept
     uint64_t wtick = 0;
     // devices that may map this device's KV (peer access over NVLink): every KV
@@ -761,6 +767,7 @@ void unmap_tail(mesh_gpu* g, Instance& in, size_t keep) {
         size_t off = (in.granules.size() - 1) * g->pool.gran;
         CU(d.unmap(in.va + off, g->pool.gran), "cuMemUnmap");
         g->st.vmm_calls++;
+        g->st.vmm_unmaps++;
         g->pool.give(in.granules.back());
         in.granules.pop_back();
     }
@@ -771,7 +778,25 @@ void unmap_tail(mesh_gpu* g, Instance& in, size_t keep) {
 // costs nothing and a shrink never stalls the host on the device. Granules go
 // back to the pool only when another grow needs them: one drain of the streams,
 // then every instance's slack above its capacity is unmapped.
-void reclaim_slack(mesh_gpu* g) {
+void unmap_idle(mesh_gpu* g, mesh_gpu::InstBufs& b, size_t keep) {
+    Driver& d = drv();
+    VmmTimer vt(g);
+    while (b.granules.size() > keep) {
+        CU(d.unmap(b.va + (b.granules.size() - 1) * g->pool.gran, g->pool.gran), "cuMemUnmap");
+        g->st.vmm_calls++;
+        g->st.vmm_unmaps++;
+        g->pool.give(b.granules.back());
+        b.granules.pop_back();
+    }
+}
+
+void reclaim_slack(mesh_gpu* g, long long need) {
+    // granules parked in recycled ranges first: nothing runs on them, no drain
+    for (auto& b : g->ibufs) {
+        if (g->pool.mapped + need <= g->pool.limit) return;
+        unmap_idle(g, b, 0);
+    }
+    if (g->pool.mapped + need <= g->pool.limit) return;
     g->st.kv_reclaims++;
     sync_all(g);
     for (auto& [id, ip] : g->insts) unmap_tail(g, *ip, granules_for(g, (long long)ip->cap_blocks * ip->block_bytes));
@@ -783,7 +808,8 @@ void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
     const size_t want = granules_for(g, (long long)bytes), first = in.granules.size();
     if (want <= first) return;
     if (want * gran > in.va_size) throw MeshError(MESH_ERR_NOMEM, "instance KV VA range exhausted");
-    if (g->pool.mapped + (long long)((want - first) * gran) > g->pool.limit) reclaim_slack(g);
+    if (g->pool.mapped + (long long)((want - first) * gran) > g->pool.limit)
+        reclaim_slack(g, (long long)((want - first) * gran));
     Driver& d = drv();
     VmmTimer vt(g);
     while (in.granules.size() < want) {
@@ -1240,7 +1266,15 @@ mesh_status fail(mesh_gpu* g, const std::exception& e) {
 }
 
 template <typename F>
-mesh_status guarded(mesh_gpu* g, F&& body) {
+mesh_status guarded(mesh_gpu* g, F&& body, double* host_ms = nullptr) {
+    const auto t0 = std::chrono::steady_clock::now();
+    struct Acc {
+        double* ms;
+        std::chrono::steady_clock::time_point t0;
+        ~Acc() {
+            if (ms) *ms += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        }
+    } acc{host_ms, t0};
     try {
         if (g) device_guard(g);
         body();
@@ -1331,6 +1365,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->pool.gran = want;
         g->st.kv_granule_bytes = (long long)want;
         g->pool.limit = cfg->kv_pool_bytes > 0 ? cfg->kv_pool_bytes : (long long)(prop.totalGlobalMem / 2);
+        g->va_size = ((size_t(g->pool.limit) + (size_t(256) << 20)) / g->pool.gran + 1) * g->pool.gran;
         CK(cudaHostAlloc((void**)&g->h_desc, sizeof(StepDesc) * RING, cudaHostAllocDefault));
         CK(cudaMalloc((void**)&g->d_desc, sizeof(StepDesc) * RING));
         CK(cudaHostAlloc((void**)&g->h_tok, sizeof(int) * 8 * RING, cudaHostAllocDefault));
@@ -1403,7 +1438,11 @@ void mesh_gpu_close(mesh_gpu* g) {
     }
     cudaStreamSynchronize(g->side);
     for (auto& b : g->ibufs) {
-        drv().addr_free(b.va, b.va_size);
+        try {
+            unmap_idle(g, b, 0);
+        } catch (...) {
+        }
+        drv().addr_free(b.va, g->va_size);
         cudaFree(b.d_block_table);
         cudaFree(b.d_last_tok);
     }
@@ -1482,26 +1521,30 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         size_t total = L * (qkv + o + gu + dn) + lm + emb + norms + rope + 4096;
         in->block_bytes = (long long)KV_BLOCK_TOKENS * s.kv_bytes_per_token();
         size_t gran = g->pool.gran;
-        in->va_size = ((size_t(g->pool.limit) + size_t(in->block_bytes) * (DEC_MAXB + 2)) / gran + 1) * gran;
+        in->va_size = g->va_size;
+        if (size_t(in->block_bytes) * (DEC_MAXB + 2) > in->va_size - size_t(g->pool.limit))
+            throw MeshError(MESH_ERR_CONFIG, "KV block too large for the VA slack");
         in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
         in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
-        // per-instance buffers first (recycle a free set of the same sizes, else
-        // allocate); on any later failure they go back to the free list
+        // per-instance buffers first: recycle the free range that still has the most
+        // granules mapped (else allocate); on any later failure they go back
         bool recycled = false;
-        for (size_t i = g->ibufs.size(); i-- > 0;) {
-            const mesh_gpu::InstBufs& bb = g->ibufs[i];
-            if (bb.va_size != in->va_size || bb.bt_elems != in->h_block_table.size()) continue;
+        if (!g->ibufs.empty()) {
+            size_t bi = 0;
+            for (size_t i = 1; i < g->ibufs.size(); ++i)
+                if (g->ibufs[i].granules.size() > g->ibufs[bi].granules.size()) bi = i;
+            mesh_gpu::InstBufs& bb = g->ibufs[bi];
             in->va = bb.va;
             in->d_block_table = bb.d_block_table;
             in->d_last_tok = bb.d_last_tok;
-            g->ibufs.erase(g->ibufs.begin() + long(i));
+            in->granules = std::move(bb.granules);
+            g->ibufs.erase(g->ibufs.begin() + long(bi));
             recycled = true;
-            break;
         }
         if (!recycled) {
             // KV region: reserve the whole pool's worth of VA
             CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
-            if (cudaMalloc((void**)&in->d_block_table, sizeof(int) * in->h_block_table.size()) != cudaSuccess ||
+            if (cudaMalloc((void**)&in->d_block_table, sizeof(int) * size_t(MAX_SLOTS) * DEC_BT_MAX) != cudaSuccess ||
                 cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS) != cudaSuccess) {
                 cudaGetLastError();
                 if (in->d_block_table) cudaFree(in->d_block_table);
@@ -1511,7 +1554,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         }
         Instance* ip = in.get();
         auto give_back_bufs = [g, ip] {
-            g->ibufs.push_back({ip->va, ip->va_size, ip->d_block_table, ip->h_block_table.size(), ip->d_last_tok});
+            g->ibufs.push_back({ip->va, ip->d_block_table, ip->d_last_tok, std::move(ip->granules)});
         };
         // weights: share a live or idle set of the same model, else allocate
         // (stream-ordered, so a later free never serialises the device) and
@@ -1598,7 +1641,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         g->lanes[best].n_inst++;
         g->insts.emplace(instance_id, std::move(in));
         rebalance_lanes(g);
-    });
+    }, &g->st.host_ms_create);
 }
 
 mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
@@ -1612,12 +1655,11 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
         drain_instance(g, instance_id);
         reap_blocks(in, true);
         cudaEventDestroy(in.last_ev);
-        unmap_tail(g, in, 0);
         lane_of(g, in).weight_bytes -= in.weight_bytes;
         lane_of(g, in).n_inst--;
         // release the weight set (kept while idle, for a reload) and recycle the
         // per-instance buffers: no cudaFree, which would serialise the device
-        g->ibufs.push_back({in.va, in.va_size, in.d_block_table, in.h_block_table.size(), in.d_last_tok});
+        g->ibufs.push_back({in.va, in.d_block_table, in.d_last_tok, std::move(in.granules)});
         auto wit = g->wsets.find(in.shape_key);
         if (wit != g->wsets.end()) {
             wit->second.refs--;
@@ -1635,7 +1677,7 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
         }
         g->insts.erase(instance_id);
         rebalance_lanes(g);
-    });
+    }, &g->st.host_ms_destroy);
 }
 
 mesh_status mesh_gpu_kv_resize(mesh_gpu* g, int64_t instance_id, int64_t from_bytes, int64_t to_bytes) {
@@ -1647,7 +1689,7 @@ mesh_status mesh_gpu_kv_resize(mesh_gpu* g, int64_t instance_id, int64_t from_by
                                               ") does not match current target (" + std::to_string(in.target) + ")");
         resize_kv(g, in, to_bytes);
         g->st.kv_mapped_bytes = g->pool.mapped;
-    });
+    }, &g->st.host_ms_kv_resize);
 }
 
 // Debug (MESH_GPU_CHECK): block-table consistency and a NaN/Inf scan of a request's KV.
@@ -1759,7 +1801,7 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
         }
         *ticket = g->next_ticket++;
         g->tickets.emplace(*ticket, std::move(t));
-    });
+    }, &g->st.host_ms_step);
 }
 
 mesh_status mesh_gpu_step_wait(mesh_gpu* g, int64_t ticket, int32_t* tokens_out, int32_t cap, int32_t* n_out,

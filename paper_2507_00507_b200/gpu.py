@@ -51,7 +51,9 @@ class GpuStats(C.Structure):
                 ("kernel_launches", C.c_int64), ("h2d_bytes", C.c_int64), ("d2h_bytes", C.c_int64),
                 ("kv_granule_bytes", C.c_int64), ("vmm_calls", C.c_int64), ("vmm_ms", C.c_double),
                 ("kv_reclaims", C.c_int64), ("last_step_end_ms", C.c_double),
-                ("weight_cache_hits", C.c_int64), ("peer_devices", C.c_int64)]
+                ("weight_cache_hits", C.c_int64), ("peer_devices", C.c_int64),
+                ("vmm_unmaps", C.c_int64), ("host_ms_create", C.c_double), ("host_ms_destroy", C.c_double),
+                ("host_ms_kv_resize", C.c_double), ("host_ms_step", C.c_double)]
 
 
 @dataclass(frozen=True)

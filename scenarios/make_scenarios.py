@@ -21,7 +21,10 @@ serving path rather than the arrival rate.
                 6 / 12 / 12 s) with every rate scaled by K (the lambda of the
                 capacity sweep). Measured B200 tables and CostParams; run with
                 runtime.clock = "wall", so step completions, emission times and
-                SLO compliance come from CUDA events, not from the tables.
+                SLO compliance come from CUDA events, not from the tables; the
+                admission replay divides its pessimistic step costs by the
+                measured co-location speedup (instances step concurrently on
+                their SM quotas, tools/measure_colocation.py).
 
     python scenarios/make_scenarios.py
 """
@@ -39,6 +42,9 @@ from make_ctrl_golden import TEMPLATES, const_rate, lengths_csv, poisson_trace  
 C3_MODELS = ["1b", "3b", "7b", "1b", "3b", "7b", "1b", "3b"]
 C3_SCALES = [1, 2, 4, 6, 8, 12, 16]
 C3_WINDOW = 30.0
+# runtime.colocation_speedup: measured by tools/measure_colocation.py (profiles/colocation_r02.json):
+# the C3 node's step sequence takes 4.51 s on one lane and 2.70 s on eight concurrent lanes
+C3_COLOCATION_SPEEDUP = 1.67
 
 
 def c3_rate(scale, window):
@@ -76,7 +82,7 @@ def make_c3():
                          "window_s": C3_WINDOW, "sample_functions": 8},
             "slo": {"ttft_base_s": 2.0, "ttft_per_token_divisor": 512.0, "tpot_s": 0.25},
             "policy": {"kind": "mesh", "watermark_pct": 20.0, "keep_alive_s": 1.0},
-            "runtime": {"clock": "wall", "slots": 64},
+            "runtime": {"clock": "wall", "slots": 64, "colocation_speedup": C3_COLOCATION_SPEEDUP},
             "output": {"dir": os.path.relpath(os.path.join(d, "out"), ROOT), "event_log": False},
         }
         with open(os.path.join(d, "config.json"), "w") as fh:

@@ -251,6 +251,17 @@ MESH_DEV int atom_add_acq_rel_gpu(int* p, int v) {
     asm volatile("atom.add.acq_rel.gpu.global.s32 %0, [%1], %2;\n" : "=r"(old) : "l"(p), "r"(v) : "memory");
     return old;
 }
+// Monotonic grid barrier: barrier i of a launch completes when the counter
+// reaches i * nblocks. Arrival is a fire-and-forget release reduction (no
+// returned atomic, no last-arriver hop), so the chain is: last CTA's red lands
+// in L2 -> every poller's next acquire load sees it. The counter is reset to 0
+// by the launch's last CTA once every CTA is past its final barrier.
+MESH_DEV void grid_barrier_mono(unsigned int* count, unsigned int target) {
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(count) : "memory");
+    while (int(ld_acquire_gpu(count) - target) < 0) {
+    }
+}
+
 MESH_DEV void grid_barrier(unsigned int* count, unsigned int* gen, unsigned int nblocks) {
     const unsigned int my_gen = ld_acquire_gpu(gen);
     unsigned int old;

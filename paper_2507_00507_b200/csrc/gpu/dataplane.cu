@@ -399,6 +399,7 @@ struct Lane {
     int* arg_idx = nullptr;
     int* arg_cnt = nullptr;
     int* claim = nullptr;  // decode tile-claim counters (self-resetting)
+    int* qkv_done = nullptr;  // decode QKV-group completion counters (self-resetting)
     float* logits = nullptr;
     unsigned* bar = nullptr;  // [count, gen]
     // prefill scratch
@@ -1044,6 +1045,7 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.arg_idx = ln.arg_idx;
     a.arg_cnt = ln.arg_cnt;
     a.claim = ln.claim;
+    a.qkv_done = ln.qkv_done;
     a.logits = g->capture_logits ? ln.logits : nullptr;
     a.tok_out = g->d_tok + ring * 8;
     a.bar_count = ln.bar;
@@ -1170,17 +1172,26 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     const int64_t rid = p.prefill_request;
     // a request with device history (re-prefill) needs its token history complete
     if (in.reqs.count(rid)) flush_request(g, in.id, rid);
-    ReqState& r = req_slot(in, rid);
     int n = p.prefill_len;
     if (n < 1 || n > in.s.max_seq) throw MeshError(MESH_ERR_ARG, "prefill_len out of range");
-    // a request that was evicted resumes from its parked KV (or at least its history)
+    // A request that was evicted resumes from its parked KV (or at least its
+    // history). It is taken out of the store BEFORE its new slot exists: the
+    // take completes the parked history from the origin's in-flight steps, and
+    // those tokens must land in the entry, not in a fresh state of the same id.
+    SwapEntry e;
     bool parked = false;
-    if (r.ctx == 0) {
-        std::lock_guard<std::mutex> lk(swaps().mu);
-        parked = swap_store().count(rid) > 0;
+    if (!in.reqs.count(rid)) {
+        {
+            std::lock_guard<std::mutex> lk(swaps().mu);
+            parked = swap_store().count(rid) > 0;
+        }
+        if (parked) {
+            if (in.free_slots.empty()) throw MeshError(MESH_ERR_NOMEM, "instance request table full");
+            e = take_parked(rid);
+        }
     }
+    ReqState& r = req_slot(in, rid);
     if (parked) {
-        SwapEntry e = take_parked(rid);
         if (e.chunk >= 0 && e.shape_key == in.shape_key && e.ctx == n - 1) {
             restore_parked(g, in, r, e, stream_of(g, in));
         } else {
@@ -1328,6 +1339,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             dalloc(&l.arg_idx, size_t(8) * g->sms);
             dalloc(&l.arg_cnt, 1);
             dalloc(&l.claim, DEC_CLAIM_MAX);
+            dalloc(&l.qkv_done, DEC_KV_HEADS_MAX);
             dalloc(&l.tile_ctr, 1);
             CK(cudaEventCreateWithFlags(&l.quota_ev, cudaEventDisableTiming));
         }
@@ -1450,7 +1462,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
                              l.arg_idx, l.arg_cnt, l.logits, l.bar, l.p_h, l.p_act, l.p_rs, l.p_q, l.p_attn,
-                             l.p_abuf, l.p_logits, l.p_tokens, l.tile_ctr, l.claim};
+                             l.p_abuf, l.p_logits, l.p_tokens, l.tile_ctr, l.claim, l.qkv_done};
         for (void* p : lane_ptrs)
             if (p) cudaFree(p);
         if (l.stream) cudaStreamDestroy(l.stream);
@@ -1496,6 +1508,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         if (s.d % 256 || s.ff % 256 || s.vocab % 128 || (s.qkv_rows() % 128))
             throw MeshError(MESH_ERR_CONFIG, "d_model/d_ff must be multiples of 256, vocab of 128");
         if (s.n_layers < 1 || s.n_layers * 4 + 1 > DEC_CLAIM_MAX) throw MeshError(MESH_ERR_CONFIG, "n_layers out of range");
+        if (s.n_kv > DEC_KV_HEADS_MAX) throw MeshError(MESH_ERR_CONFIG, "n_kv_heads out of range");
         if (s.max_seq < 2 || s.max_seq > DEC_BT_MAX * KV_BLOCK_TOKENS)
             throw MeshError(MESH_ERR_CONFIG, "max_seq_len out of range");
         ensure_scratch(g, s);
@@ -1976,15 +1989,28 @@ mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst,
         ReqState& sr = it->second;
         cudaEvent_t ready = record_new_event(stream_of(src, si));  // after every step that wrote the KV
         CK(cudaSetDevice(dst->cfg.device));
+        if (di.free_slots.empty()) {
+            cudaEventDestroy(ready);
+            throw MeshError(MESH_ERR_NOMEM, "migrate: destination request table full");
+        }
+        // destination blocks first: on failure nothing has changed on either side
+        std::vector<int> nb;
+        try {
+            while (nb.size() < sr.blocks.size()) nb.push_back(alloc_block(dst, di));
+        } catch (...) {
+            for (int b : nb) {
+                if (b < di.cap_blocks) di.free_blocks.insert(b);
+                di.live_blocks--;
+            }
+            cudaEventDestroy(ready);
+            throw;
+        }
         ReqState& dr = req_slot(di, request_id);
         cudaStream_t dst_st = stream_of(dst, di);
         dr.tokens = sr.tokens;
         dr.ctx = sr.ctx;
-        for (size_t i = 0; i < sr.blocks.size(); ++i) {
-            int b = alloc_block(dst, di);
-            dr.blocks.push_back(b);
-            write_bt_entry(di, dr.slot, int(i), b);
-        }
+        dr.blocks = std::move(nb);
+        for (size_t i = 0; i < dr.blocks.size(); ++i) write_bt_entry(di, dr.slot, int(i), dr.blocks[i]);
         CK(cudaStreamWaitEvent(dst_st, ready, 0));
         cudaEventDestroy(ready);
         // one copy kernel on the destination GPU: P2P loads of the source blocks over NVLink

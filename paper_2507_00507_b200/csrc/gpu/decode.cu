@@ -457,7 +457,7 @@ __device__ __forceinline__ void grid_sync(Ctx& c) {
     if (c.a->arrive && c.tid == 0 && c.nbar < 256) c.a->arrive[size_t(c.nbar) * c.G + c.cta] = gtimer();
     ++c.nbar;
     if (c.a->progress && c.tid == 0) c.a->progress[c.cta * 2] += 1;
-    if (c.tid == 0) grid_barrier(c.a->bar_count, c.a->bar_gen, unsigned(c.G));
+    if (c.tid == 0) grid_barrier_mono(c.a->bar_count, unsigned(c.nbar) * unsigned(c.G));
     csync();
     trace(c, 5);
 }
@@ -692,7 +692,16 @@ __device__ __forceinline__ void epilogue_group(Ctx& c, int kind, int layer, int 
                                          : warp_sum(c, ti);
         float v[4] = {sv.x, sv.y, sv.z, sv.w};
         switch (kind) {
-            case PH_QKV: epi_qkv(c, layer, tile, v, rs); break;
+            case PH_QKV:
+                epi_qkv(c, layer, tile, v, rs);
+                // publish the tile to the attention of its KV-head group (no grid barrier
+                // between QKV and attention): stores visible, then one count per tile
+                __threadfence();
+                __syncwarp();
+                if (c.lane == 0)
+                    asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.qkv_done + tile / qkv_group_tiles(a.s))
+                                 : "memory");
+                break;
             case PH_GU: epi_gu(c, tile, v, rs); break;
             case PH_O: epi_residual(c, tile, v, a.w.g_mlp + size_t(layer) * a.s.d, a.ssB); break;
             case PH_DOWN: {
@@ -1158,6 +1167,14 @@ __device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPla
         const AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0 + i);
         if (st.pair != cur_pair) {
             if (cur_pair >= 0) attn_flush<DH>(c, ap, cur_b, cur_kvh, cur_lo, cur_n, stt);
+            // this layer's q / current K,V of the group are written by the QKV phase's
+            // tiles of group kvh (any CTA): wait for the group's count, not for the grid
+            if (c.lane == 0) {
+                const int need = (layer + 1) * qkv_group_tiles(s);
+                while (int(ld_acquire_gpu(reinterpret_cast<const unsigned int*>(a.qkv_done + st.kvh))) < need) {
+                }
+            }
+            __syncwarp();
             cur_pair = st.pair;
             cur_b = st.b;
             cur_kvh = st.kvh;
@@ -1281,9 +1298,13 @@ __device__ __forceinline__ void run_argmax_combine(Ctx& c, float best_v[2], int 
                 a.last_tok[c.slot[b]] = bi;
             }
         }
-        if (c.tid == 0) atomicExch(a.arg_cnt, 0);
+        if (c.tid == 0) {
+            atomicExch(a.arg_cnt, 0);
+            atomicExch(a.bar_count, 0u);  // every CTA is past its last grid barrier
+        }
         // every CTA is past its last claim: rearm the dynamic phases' counters for the next step
         for (int i = c.tid; i < a.s.n_layers * 4 + 1; i += CONSUMER_THREADS) a.claim[i] = 0;
+        for (int i = c.tid; i < a.s.n_kv; i += CONSUMER_THREADS) a.qkv_done[i] = 0;
     }
 }
 
@@ -1382,8 +1403,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     grid_sync(c);
     for (int l = 0; l < a.s.n_layers; ++l) {
         run_gemv(c, PH_QKV, l, best_v, best_i);
-        grid_sync(c);
-        trace(c, 6);
+        trace(c, 6);  // no grid barrier: attention waits per KV-head group (qkv_done)
         if (!(a.skip & 1)) {
             if (a.s.dh == 64)
                 run_attention_t<64>(c, l, ap);

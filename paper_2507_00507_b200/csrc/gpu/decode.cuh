@@ -17,6 +17,7 @@ constexpr int DEC_MAXB = 8;         // batch columns of the mma (n = 8)
 constexpr int DEC_BT_MAX = 256;     // block-table entries per request -> contexts up to 4096 tokens
 constexpr int MAX_BT_UPDATES = 64;
 constexpr int DEC_CLAIM_MAX = 256;  // claim counters per lane: n_layers * 4 + 1 <= 256
+constexpr int DEC_KV_HEADS_MAX = 64;
 
 constexpr int DEC_SMEM_RING = DEC_NSTAGE * DEC_STAGE_BYTES;
 constexpr int DEC_SMEM_ACT = DEC_MAXB * (DEC_KSEG_MAX + 8) * 2;
@@ -61,6 +62,7 @@ struct DecodeArgs {
     int* arg_idx;      // [grid][8]
     int* arg_cnt;      // [1] (self-resetting)
     int* claim;        // [n_layers * 4 + 1] tile-claim counters of the dynamic GEMV phases (reset at step end)
+    int* qkv_done;     // [n_kv] QKV tiles finished per KV-head group, monotonic over the step's layers (reset at step end)
     float* logits;     // optional [8][vocab]
     int* tok_out;      // [8]
     unsigned int* bar_count;

@@ -66,23 +66,31 @@ struct QkvRow {
     int dim;
 };
 __host__ __device__ inline QkvRow qkv_row(const Shape& s, int prow) {
+    // Rows are grouped by KV head: group g = the GQA group's q heads, then k head
+    // g, then v head g (dh rows each), so the tiles of one group are contiguous
+    // and the decode attention of (request, kv head g) can start as soon as the
+    // group's tiles are done, without a grid-wide barrier after the QKV phase.
     int tiles_per_head = s.dh / 16;
     int tile = prow >> 4, r = prow & 15;
     int head_global = tile / tiles_per_head, j = tile % tiles_per_head;
+    const int gq = s.n_heads / s.n_kv, per_group = gq + 2;
+    const int grp = head_global / per_group, idx = head_global % per_group;
     QkvRow out;
-    if (head_global < s.n_heads) {
+    if (idx < gq) {
         out.section = 0;
-        out.head = head_global;
-    } else if (head_global < s.n_heads + s.n_kv) {
+        out.head = grp * gq + idx;
+    } else if (idx == gq) {
         out.section = 1;
-        out.head = head_global - s.n_heads;
+        out.head = grp;
     } else {
         out.section = 2;
-        out.head = head_global - s.n_heads - s.n_kv;
+        out.head = grp;
     }
     out.dim = (r < 8) ? (8 * j + r) : (8 * j + (r - 8) + s.dh / 2);
     return out;
 }
+// QKV tiles of KV-head group g: [g * qkv_group_tiles, (g + 1) * qkv_group_tiles)
+__host__ __device__ inline int qkv_group_tiles(const Shape& s) { return (s.n_heads / s.n_kv + 2) * (s.dh / 16); }
 // Gate/up: tile j holds gate rows [8j, 8j+8) in rows 0-7 and the matching up
 // rows in rows 8-15, so silu(gate) * up is formed in registers.
 __host__ __device__ inline void gu_row(int prow, int* is_up, int* row) {

@@ -93,11 +93,17 @@ __device__ __forceinline__ void seg_range(int K, int nseg, int s, int& c0, int& 
 }
 
 // ---- attention work plan (identical on producer and consumers) ----
-// Stages enumerate (request b, kv head, chunk s of RT = 2048/dh tokens) in
-// b-major order; stage = the K and V rows of those tokens for one layer, 8 KB.
+// Stages enumerate (kv head, request b, chunk s of RT = 2048/dh tokens) in
+// HEAD-major order; stage = the K and V rows of those tokens for one layer,
+// 8 KB. Head-major puts each CTA's contiguous range on one or a few KV heads,
+// so a CTA starts as soon as ITS heads' QKV tiles are done (the QKV tiles are
+// claimed in group order): the tail of the QKV phase overlaps attention. Pair
+// id of (b, kv head) = kvh * nb + b (consecutive in stage order).
 struct AttnPlan {
     int rt;             // tokens per stage
     int nst[DEC_MAXB];  // stages per (b, kv head)
+    int nb;             // requests
+    int hst;            // stages per kv head (all requests)
     int total;          // stages per layer
     int a0, a1;         // this CTA's contiguous range
 };
@@ -106,11 +112,13 @@ __device__ __forceinline__ int range_lo(int c, int total, int G) { return int(un
 __device__ __forceinline__ AttnPlan attn_plan(const Shape& s, int B, const int* pos, int cta, int G) {
     AttnPlan p;
     p.rt = 2048 / s.dh;
-    p.total = 0;
+    p.nb = B;
+    p.hst = 0;
     for (int b = 0; b < DEC_MAXB; ++b) {
         p.nst[b] = b < B ? (pos[b] + p.rt) / p.rt : 0;  // ceil((pos + 1) / rt)
-        p.total += s.n_kv * p.nst[b];
+        p.hst += p.nst[b];
     }
+    p.total = s.n_kv * p.hst;
     p.a0 = int(range_lo(cta, p.total, G));
     p.a1 = int(range_lo(cta + 1, p.total, G));
     return p;
@@ -119,20 +127,20 @@ struct AttnStage {
     int b, kvh, s, pair, pair_lo;  // pair_lo: global index of the pair's first stage
 };
 __device__ __forceinline__ AttnStage attn_stage_of(const AttnPlan& p, int n_kv, int i) {
+    (void)n_kv;
     AttnStage st;
+    st.kvh = i / p.hst;
+    const int r = i - st.kvh * p.hst;
     int base = 0;
-    for (int b = 0; b < DEC_MAXB; ++b) {
-        const int n = n_kv * p.nst[b];
-        if (i < base + n) {
-            const int r = i - base;
+    for (int b = 0; b < p.nb; ++b) {
+        if (r < base + p.nst[b]) {
             st.b = b;
-            st.kvh = r / p.nst[b];
-            st.s = r % p.nst[b];
-            st.pair = b * n_kv + st.kvh;
-            st.pair_lo = base + st.kvh * p.nst[b];
+            st.s = r - base;
+            st.pair = st.kvh * p.nb + b;
+            st.pair_lo = st.kvh * p.hst + base;
             return st;
         }
-        base += n;
+        base += p.nst[b];
     }
     st.b = st.kvh = st.s = st.pair = st.pair_lo = 0;
     return st;
@@ -282,16 +290,14 @@ struct Producer {
     }
     __device__ __forceinline__ void gemv_dynamic(int kind, int layer, int G) {
         const GemvPhase p = gemv_phase(a, kind, layer);
-        const int cl = claim_tiles(p.tiles, G), nch = p.K / DEC_CHUNK_COLS;
+        const int cl_big = claim_tiles(p.tiles, G), nch = p.K / DEC_CHUNK_COLS;
         int* ctr = a.claim + claim_index(a.s, kind, layer);
         const size_t tile_bytes = size_t(p.K) * 32;
-        // the next claim is requested one group ahead: its round trip hides behind this group's stages
-        int next = 0;
+        int cl = cl_big, next = 0;
         if (lane == 0) next = atomicAdd(ctr, cl);
         for (;;) {
             const int t0 = __shfl_sync(0xffu, next, 0);
             const int gn = max(0, min(cl, p.tiles - t0));
-            if (gn > 0 && lane == 0) next = atomicAdd(ctr, cl);
             // issue every pending stage first: the consumers may need them to
             // get to the descriptor slot this claim waits for
             flush();
@@ -308,6 +314,13 @@ struct Producer {
                 const uint8_t* t = p.base + size_t(t0 + ti) * tile_bytes;
                 for (int ch = 0; ch < nch; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, nullptr, -1);
             }
+            // Next claim once this group's stages are issued: a ring's depth of them is
+            // still to be consumed, which hides the round trip, and a CTA that streams
+            // slowly claims late. Guided sizes (remaining / 2G, at most cl_big, at
+            // least 1) end the phase on single tiles, so the tail imbalance across
+            // CTAs is about one tile.
+            cl = max(1, min(cl_big, (p.tiles - (t0 + gn)) / (2 * G)));
+            if (lane == 0) next = atomicAdd(ctr, cl);
         }
     }
     __device__ __forceinline__ void gemv(int kind, int layer, int& off, int cta, int G) {
@@ -383,19 +396,15 @@ struct Producer {
             const uint8_t* kb0 = nblk > 0 ? layer_base + size_t(btrow[k0]) * a.block_bytes + hoff : nullptr;
             const uint8_t* kb1 = nblk > 1 ? layer_base + size_t(btrow[k0 + 1]) * a.block_bytes + hoff : nullptr;
             push(kb0, kb1, nblk);
-            if (++sc == nst_b) {  // next (b, kv head)
+            if (++sc == nst_b) {  // next (kv head, b): requests inner
                 sc = 0;
-                if (++kvh == s.n_kv) {
-                    kvh = 0;
-                    do {
-                        ++b;
-                    } while (b < DEC_MAXB && ap.nst[b] == 0);
-                    if (b < DEC_MAXB) {
-                        nst_b = ap.nst[b];
-                        p = pos[b];
-                        btrow = sm.bt + b * DEC_BT_MAX;
-                    }
+                if (++b == ap.nb) {
+                    b = 0;
+                    ++kvh;
                 }
+                nst_b = ap.nst[b];
+                p = pos[b];
+                btrow = sm.bt + b * DEC_BT_MAX;
             }
         }
     }
@@ -439,6 +448,8 @@ struct Ctx {
     uint32_t nsh, nmask;  // ring depth = 1 << nsh (8 or 16)
     int off;          // round-robin offset of static phases (mirrors the producer)
     uint32_t dk;      // claim descriptors read (mirrors the producer)
+    uint64_t* actbar; // activation bulk-load mbarrier
+    uint32_t actph;   // its phase
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -471,27 +482,27 @@ __device__ __forceinline__ void release_stage(Ctx& c, uint32_t slot) {
     if (c.lane == 0) mbar_arrive(&c.sm.empty[slot]);
 }
 
-// Activation columns [k0, k1) of the 8 batch rows (bf16, global) into smem,
-// every thread's loads issued before its stores (up to 8 x 16 B in flight).
+// Activation columns [k0, k1) of the B batch rows (bf16, global) into smem
+// (row stride k1 - k0 + 8) with one bulk copy per row, all issued at once by
+// one thread on the activation mbarrier: the whole operand is one L2 round trip
+// plus its transfer (the per-thread 16-byte loads it replaces took ~5 us for a
+// 64 KB 7B operand under the phase's HBM load). Rows >= B are left as they are:
+// they only feed mma columns whose results are discarded. Called by every
+// consumer thread between csync()s.
 __device__ __forceinline__ void load_act(Ctx& c, const uint16_t* src, int ld, int k0, int k1) {
-    const int n = k1 - k0, stride = n + 8, vec_per_row = n / 8, total = DEC_MAXB * vec_per_row;
-    for (int base = 0; base < total; base += 8 * CONSUMER_THREADS) {
-        uint4 v[8];
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int i = base + k * CONSUMER_THREADS + c.tid;
-            const int b = i / vec_per_row, e = i % vec_per_row;
-            v[k] = (i < total && b < c.B) ? ldcg_u4(src + size_t(b) * ld + k0 + e * 8) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-            const int i = base + k * CONSUMER_THREADS + c.tid;
-            if (i < total) {
-                const int b = i / vec_per_row, e = i % vec_per_row;
-                *reinterpret_cast<uint4*>(c.sm.act + b * stride + e * 8) = v[k];
-            }
-        }
+    const int n = k1 - k0, stride = n + 8;
+    if (c.tid == 0) {
+        // the rows were written by other CTAs' generic stores (visible through the
+        // grid barrier's acquire) and the destination was read by generic loads:
+        // order both before the async-proxy copies
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+        mbar_arrive_expect_tx(c.actbar, uint32_t(c.B * n * 2));
+        for (int b = 0; b < c.B; ++b)
+            bulk_g2s(c.sm.act + b * stride, src + size_t(b) * ld + k0, uint32_t(n * 2), c.actbar);
     }
+    mbar_wait(c.actbar, c.actph & 1u);
+    ++c.actph;
 }
 
 // load_act + the RMSNorm scale rs[b] = 1/sqrt(mean(h_b^2) + eps) from the
@@ -926,11 +937,12 @@ __device__ __forceinline__ void attn_combine(const float* src, int W, int count,
 // batch of cp.async (a single L2 round trip) and combined from there.
 template <int DH>
 __device__ __forceinline__ void attn_arrive(Ctx& c, int b, int kvh, int pair_lo, int count, float* scratch) {
+    // pair id = kvh * B + b (head-major stage order)
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
     const int GQ = s.n_heads / s.n_kv;
     const int W = GQ * attn_hs<DH>();
-    const int pair = b * s.n_kv + kvh;
+    const int pair = kvh * c.B + b;
     __syncwarp();
     int last = 0;
     if (c.lane == 0) last = atom_add_acq_rel_gpu(a.acnt + pair, 1) == count - 1;
@@ -968,7 +980,7 @@ __device__ __forceinline__ void attn_flush(Ctx& c, const AttnPlan& ap, int b, in
     const int W = GQ * HS;
     const unsigned FULL = 0xffffffffu;
     const int g = c.lane >> 2, t = c.lane & 3;
-    const int pair = b * s.n_kv + kvh, k = pair - c.p0;
+    const int pair = kvh * c.B + b, k = pair - c.p0;
     int pre, r, rank, count;
     if (k < ATT_PT_MAX) {
         const AttnPair& e = c.pt[k];
@@ -1028,7 +1040,7 @@ __device__ __forceinline__ void attn_cta_combine(Ctx& c) {
         attn_combine<DH, false>(slots, W, e.n, GQ, c.lane, a.apart + size_t(e.lo_p + e.rank0) * W, nullptr);
         trace(c, 17);
         __syncwarp();  // the slots become the final-combine scratch
-        attn_arrive<DH>(c, pair / s.n_kv, pair % s.n_kv, e.lo_p, e.count, slots);
+        attn_arrive<DH>(c, pair % c.B, pair / c.B, e.lo_p, e.count, slots);
         trace(c, 18);
     }
 }
@@ -1314,6 +1326,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     __shared__ int slot_s[DEC_MAXB], pos_s[DEC_MAXB];
     __shared__ int dt0_s[4], dgn_s[4];
     __shared__ __align__(8) uint64_t dfull_s[4], dempty_s[4];
+    __shared__ __align__(8) uint64_t actbar_s;
     Smem sm = carve(smem_raw);
     sm.dt0 = dt0_s;
     sm.dgn = dgn_s;
@@ -1331,6 +1344,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
             mbar_init(&sm.dfull[i], 1);
             mbar_init(&sm.dempty[i], 1);
         }
+        mbar_init(&actbar_s, 1);
         fence_mbar_init();
     }
     if (threadIdx.x < DEC_MAXB) {
@@ -1365,6 +1379,8 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     c.q = 0;
     c.off = 0;
     c.dk = 0;
+    c.actbar = &actbar_s;
+    c.actph = 0;
     c.nsh = uint32_t(__ffs(a.nstage) - 1);
     c.nmask = uint32_t(a.nstage) - 1u;
     // attention plan + this CTA's pair table: identical for every layer of the step
@@ -1380,9 +1396,9 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
         c.np = attn_stage_of(ap, a.s.n_kv, ap.a1 - 1).pair - c.p0 + 1;
     }
     if (warp == 0 && lane < min(c.np, ATT_PT_MAX)) {
-        const int pair = c.p0 + lane, b = pair / a.s.n_kv, kvh = pair % a.s.n_kv;
-        int lo_p = kvh * ap.nst[b];
-        for (int bb = 0; bb < b; ++bb) lo_p += a.s.n_kv * ap.nst[bb];
+        const int pair = c.p0 + lane, b = pair % B, kvh = pair / B;
+        int lo_p = kvh * ap.hst;
+        for (int bb = 0; bb < b; ++bb) lo_p += ap.nst[bb];
         const int cap = a.s.dh == 64 ? attn_cap_pairs<64>(a.s) : attn_cap_pairs<128>(a.s);
         const PairSlot ps = pair_slot(ap, a.s.n_kv, pair, lo_p, lo_p + ap.nst[b], c.G, c.cta, 0, cap);
         AttnPair e;

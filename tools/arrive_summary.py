@@ -4,7 +4,9 @@ import numpy as np
 rows = [list(map(int, l.split())) for l in open(sys.argv[1]) if l.strip()]
 a = np.array([r for r in rows if any(r)], dtype=np.float64)
 a = a[:, :]
-names = ["embed"] + [f"L{l}.{p}" for l in range(200) for p in ["qkv", "attn", "o", "gu", "down"]]
+# barriers per layer: QKV -> attention has none (per-KV-head-group counters), so the
+# first barrier of a layer closes QKV + attention
+names = ["embed"] + [f"L{l}.{p}" for l in range(200) for p in ["qkv+attn", "o", "gu", "down"]]
 prev_release = a[0].max()
 tot = {}
 for i in range(1, a.shape[0]):

@@ -28,3 +28,7 @@ def test_two_rank_reduction_over_gloo():
     assert r["wall"] == 2.0          # max over ranks
     assert r["tokens"] == 300.0      # sum over ranks
     assert r["value"] == 150.0
+    # C5 fleet placement over the two nodes (cold starts on the node with the most
+    # free optimistic budget, cluster.cpp:325-365): both nodes host instances
+    f = r["fleet"]
+    assert f["gpu_nodes_used"] == 2 and f["gpu_instances_max"] >= 2 and f["total_requests"] > 0

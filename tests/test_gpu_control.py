@@ -68,3 +68,26 @@ def test_gpu_attached_run_keeps_every_decision(name, tmp_path, monkeypatch):
             evictions = sum(1 for line in fh if "evict" in line.lower())
         if evictions:
             assert m["gpu.swap_out_bytes"] > 0
+
+
+def test_fleet_two_nodes_one_device_wall_clock(tmp_path, monkeypatch):
+    """C5's fleet path on the one GPU a test box has: two GPU nodes driven as two
+    handles on device 0 (attach_gpu devices [0, 0]) from one host event loop, in
+    wall-clock mode (completions and emission times are CUDA events). Both nodes
+    receive instances through the control plane's placement, every request gets an
+    outcome, and the models-per-GPU accounting is filled in."""
+    import bench
+    monkeypatch.chdir(ROOT)
+    monkeypatch.setenv("MESH_GPU_LANES", "4")
+    cfg = bench.fleet_scenario(2, 1.0)
+    with control.Experiment(cfg) as exp:
+        exp.set("workload.window_s", 12.0)
+        exp.out_dir(str(tmp_path))
+        exp.attach_gpu([0, 0], 24 << 30, gpu.LIB_PATH)
+        exp.run()
+        m = {k: exp.metric(k) for k in ["gpu_nodes_used", "gpu_instances_max", "gpu_instances_avg", "total_requests",
+                                        "slo_compliant_rate", "wall_s", "gpu.steps", "gpu.decode_tokens"]}
+    assert m["total_requests"] > 0 and m["gpu.steps"] > 0 and m["gpu.decode_tokens"] > 0
+    assert m["gpu_nodes_used"] == 2 and m["gpu_instances_max"] >= 2
+    assert 12.0 <= m["wall_s"] < 60.0
+    assert 0.0 < m["slo_compliant_rate"] <= 1.0

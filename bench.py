@@ -61,10 +61,27 @@ MODELS = ["1b", "3b", "7b", "1b", "3b", "7b", "1b", "3b"]
 BATCH = 8
 LANES = int(os.environ.get("MESH_BENCH_LANES", "8"))  # one execution lane per co-located instance
 KV_POOL = 100 << 30
-E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "4,8,12").split(",")]
+E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "4,6,8").split(",")]
 WATERMARK = 20.0
 CPU_SAMPLE_S = 15.0     # bounded CPU baseline sample
 CPU_MAX_SEQ = 1160      # >= the longest I + O of the length set (1139)
+
+
+def profiler_region(on: bool) -> None:
+    """MESH_PROFILE_REGION=1: cudaProfilerStart/Stop around the timed region, so
+    `ncu --profile-from-start off` captures exactly the timed launches."""
+    if not os.environ.get("MESH_PROFILE_REGION"):
+        return
+    import ctypes
+    for name in ("libcudart.so", "libcudart.so.12", "/usr/local/cuda/lib64/libcudart.so"):
+        try:
+            rt = ctypes.CDLL(name)
+            break
+        except OSError:
+            continue
+    else:
+        return
+    (rt.cudaProfilerStart if on else rt.cudaProfilerStop)()
 
 
 def peaks():
@@ -523,7 +540,8 @@ def run_e2e_scale(device: int, scale: int):
                  "gpu.device_ms", "gpu.lane_busy_s", "slo_compliant_rate", "total_requests", "slo_compliant",
                  "slo_compliant_decode_tokens", "output_tokens", "gpu.kernel_launches", "gpu_instances_avg",
                  "gpu_instances_max", "gpu.instance_starts", "gpu.weight_cache_hits", "gpu.blocks_moved",
-                 "gpu.swap_out_bytes", "gpu.migrations", "evictions", "run_length_s"]
+                 "gpu.swap_out_bytes", "gpu.migrations", "evictions", "run_length_s", "gpu.dp_ms.step",
+                 "gpu.dp_ms.kv_resize", "gpu.dp_ms.instance_create", "gpu.host_ms.step_wait", "displacements"]
         m = {k: exp.metric(k) for k in names}
     m["scale"] = scale
     m["slo_tokens"] = m["slo_compliant_decode_tokens"] + m["slo_compliant"]  # + each compliant request's first token
@@ -641,7 +659,9 @@ def run_e2e(device: int, d: Dist, scales):
             "sweep": [{k: r[k] for k in ("scale", "total_requests", "slo_compliant_rate", "tokens_at_slo_per_s",
                                          "wall_s", "gpu_instances_avg", "gpu_instances_max", "gpu.steps",
                                          "gpu.instance_starts", "gpu.weight_cache_hits", "gpu.blocks_moved",
-                                         "gpu.swap_out_bytes", "evictions")} for r in runs],
+                                         "gpu.swap_out_bytes", "evictions", "gpu.dp_ms.step", "gpu.dp_ms.kv_resize",
+                                         "gpu.dp_ms.instance_create", "gpu.host_ms.step_wait", "gpu.lane_busy_s")}
+                      for r in runs],
             "trace": "scenarios/c3_b200/s{K}: acceptance overload generator's three phases (0.08, 0.28, "
                      "0.8 hot / 0.03 req/s per function) in a 30 s window, rates x K",
             "tables": "measured B200 tables + CostParams (admission); completions on CUDA events",
@@ -664,7 +684,9 @@ def run_ours(args, d: Dist):
         node.g.sync()
         node.g.timer_mark(0)
         node.mark0 = node.clock
+        profiler_region(True)
         launches = node.run(args.steps)
+        profiler_region(False)
         node.g.timer_mark(1)
         node.g.sync()
         dev_s = node.g.timer_elapsed(0, 1) / 1e3

@@ -15,6 +15,14 @@ from paper_2507_00507_b200 import control, gpu  # noqa: E402
 
 
 def main():
+    if os.environ.get("E2E_PRE_NODE"):  # reproduce bench.py: the value leg's node first, same process
+        node = bench.Colocated(0)
+        node.k = 0
+        node.fill()
+        node.run(len(bench.MODELS) * bench.BATCH)
+        node.run(int(os.environ["E2E_PRE_NODE"]))
+        node.g.sync()
+        node.g.close()
     k = int(sys.argv[1])
     out = sys.argv[2] if len(sys.argv) > 2 else os.path.join("gpurun_out", f"e2e_s{k}")
     os.makedirs(out, exist_ok=True)

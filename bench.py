@@ -73,15 +73,11 @@ def profiler_region(on: bool) -> None:
     if not os.environ.get("MESH_PROFILE_REGION"):
         return
     import ctypes
-    for name in ("libcudart.so", "libcudart.so.12", "/usr/local/cuda/lib64/libcudart.so"):
-        try:
-            rt = ctypes.CDLL(name)
-            break
-        except OSError:
-            continue
-    else:
+    try:  # driver API: acts on the context current on this thread (the data plane's primary context)
+        drv = ctypes.CDLL("libcuda.so.1")
+    except OSError:
         return
-    (rt.cudaProfilerStart if on else rt.cudaProfilerStop)()
+    (drv.cuProfilerStart if on else drv.cuProfilerStop)()
 
 
 def peaks():
@@ -719,9 +715,12 @@ def run_ours(args, d: Dist):
     sim = reference_simulator_sample(E2E_SCALES[0]) if d.ws == 1 else None
     traffic = None
     prof = os.path.join(ROOT, "profiles", "decode_traffic.json")
-    if os.path.exists(prof):
+    if os.path.exists(prof):  # ncu DRAM bytes per launch per model, weighted by this run's launch mix
         with open(prof) as fh:
-            traffic = json.load(fh).get("dram_bytes_per_launch")
+            per = json.load(fh).get("per_model", {})
+        n = sum(v["launches"] for v in node.per_model.values())
+        if per and n and all(m in per for m in node.per_model):
+            traffic = sum(v["launches"] * per[m]["dram_bytes"] for m, v in node.per_model.items()) / n
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": d.ws, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * wall_max / args.steps, "higher_is_better": True, "scaling": "weak",
@@ -742,6 +741,8 @@ def run_ours(args, d: Dist):
                    "parallelism": f"{d.ws} independent co-located nodes"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,
+                     "traffic_basis": "ncu dram__bytes_read+write per decode launch per model "
+                                      "(profiles/decode_traffic.json), weighted by this run's launch mix",
                      "kernel": "decode_kernel (persistent, TMA-ring), one launch per lane step",
                      "peak_source": peak_kind,
                      "algorithmic_bytes_per_launch": node.decode_bytes / max(1, node.decode_steps),

@@ -9,7 +9,8 @@ all drawing on the GPU's VMM KV pool.
 
   step    one instance step of the co-located schedule (the planned decode of
           that instance's batch of 8, or the prefill of a newly admitted
-          request), launched through the mesh_gpu C ABI; instances take turns.
+          request), launched through the mesh_gpu C ABI; every instance keeps up
+          to 4 steps queued on its own lane and is re-fed as its steps retire.
           Every admission and completion re-sizes the instance's KV target by
           the reference's rule (m_require + 20 % watermark, memory.cpp:19-36):
           KV grow (VMM map) and shrink (compaction kernel) run inside the timed
@@ -300,12 +301,12 @@ class Colocated:
             while len(inst["reqs"]) + len(inst["pending"]) < BATCH:
                 self.new_request(inst)
 
-    def plan(self, k):
-        """Step k of the schedule: instance k mod 8; a pending request is prefilled first."""
-        inst = self.insts[k % len(self.insts)]
+    def plan_of(self, inst):
+        """The instance's next step: a pending request is prefilled first (select_next's
+        prefill-first rule), else the decode of its batch."""
         if inst["pending"]:
-            return inst, "prefill", [inst["pending"][0]]
-        return inst, "decode", list(inst["reqs"])
+            return "prefill", [inst["pending"][0]]
+        return "decode", list(inst["reqs"])
 
     def launch(self, inst, kind, reqs):
         if kind == "prefill":
@@ -332,19 +333,52 @@ class Colocated:
             self.new_request(inst)
 
     def run(self, steps):
-        """Launch `steps` steps asynchronously (<= 32 outstanding), retire them in order."""
+        """Launch `steps` steps asynchronously. Every instance keeps up to DEPTH steps
+        queued on its own lane and gets its next step as soon as one of its steps
+        retires, so each lane runs at its own pace (a round-robin issue order would
+        hold fast lanes to the slowest lane's step time)."""
         from collections import deque
-        inflight = deque()
+        DEPTH = 4
+        q = [deque() for _ in self.insts]
         launches0 = self.g.stats()["kernel_launches"]
-        for _ in range(steps):
-            inst, kind, reqs = self.plan(self.k)
-            self.k += 1
-            inflight.append((self.launch(inst, kind, reqs), inst, kind, reqs))
+        issued = 0
+
+        def issue(i):
+            inst = self.insts[i]
+            kind, reqs = self.plan_of(inst)
+            q[i].append((self.launch(inst, kind, reqs), inst, kind, reqs))
             self.schedule_effects(inst, kind, reqs)
-            while len(inflight) > 32:
+
+        if os.environ.get("MESH_BENCH_ISSUE") == "rr":  # A/B: round-robin issue, in-order retire, <= 32 in flight
+            inflight = deque()
+            for k in range(steps):
+                inst = self.insts[k % len(self.insts)]
+                kind, reqs = self.plan_of(inst)
+                inflight.append((self.launch(inst, kind, reqs), inst, kind, reqs))
+                self.schedule_effects(inst, kind, reqs)
+                while len(inflight) > 32:
+                    self.retire(inflight.popleft())
+            while inflight:
                 self.retire(inflight.popleft())
-        while inflight:
-            self.retire(inflight.popleft())
+            return self.g.stats()["kernel_launches"] - launches0
+        while issued < steps:
+            # fill every lane's queue (fewest in flight first, then index)
+            for i in sorted(range(len(self.insts)), key=lambda j: (len(q[j]), j)):
+                if issued < steps and len(q[i]) < DEPTH:
+                    issue(i)
+                    issued += 1
+            # retire finished steps; if none finished, wait for the oldest queued one
+            progressed = False
+            for i in range(len(q)):
+                while q[i] and self.g.done(q[i][0][0]):
+                    self.retire(q[i].popleft())
+                    progressed = True
+            if not progressed and issued < steps:
+                i = min((j for j in range(len(q)) if q[j]), key=lambda j: q[j][0][0])
+                self.retire(q[i].popleft())
+        for i in range(len(q)):
+            while q[i]:
+                self.retire(q[i].popleft())
         return self.g.stats()["kernel_launches"] - launches0
 
     def retire(self, item):
@@ -355,7 +389,7 @@ class Colocated:
         if self.mark0 is not None and st["last_step_end_ms"] >= 0:
             emit = self.mark0 + st["last_step_end_ms"] / 1e3  # the step's end on the device timeline
         else:
-            emit = self.clock + st["last_step_ms"] / 1e3      # untimed warm-up: steps back to back
+            emit = self.clock + st["last_step_ms"] / 1e3      # no mark yet: steps back to back
         self.clock = max(self.clock, emit)
         if kind == "decode":
             s = inst["shape"]
@@ -669,6 +703,9 @@ def run_ours(args, d: Dist):
     hbm, peak_kind = peaks()
     node = Colocated(device)
     node.k = 0
+    node.g.sync()
+    node.g.timer_mark(0)  # emissions read off the device timeline from the first admission on
+    node.mark0 = 0.0
     node.fill()
     # initial admissions: every instance prefills its batch (untimed)
     node.run(len(MODELS) * BATCH)
@@ -728,7 +765,7 @@ def run_ours(args, d: Dist):
         "config": {"workload": "C3: 8 co-located Llama-shaped instances [1.1B, 3B, 7B, 1.1B, 3B, 7B, 1.1B, 3B] on "
                                "one B200, batch 8 each, shared VMM KV pool with watermark grow/shrink",
                    "models": MODELS, "batch_per_instance": BATCH, "step": "one instance step (decode of its batch "
-                   "or prefill of a newly admitted request), issued in turn; each instance on its own "
+                   "or prefill of a newly admitted request); every instance keeps <= 4 steps queued on its own "
                    f"execution lane ({LANES} lanes, SM quotas in proportion to streamed weight bytes), so "
                    "co-located instances step concurrently",
                    "lane_sm_quotas": quotas,

@@ -582,6 +582,23 @@ void rebalance_lanes(mesh_gpu* g) {
             q[size_t(biggest())]--;
             used--;
         }
+        // SMs left over by rounding down go to the busy lanes with the largest
+        // remainders (budget * w / wsum - quota), so every SM of the budget streams
+        while (used < budget && busy > 0) {
+            int best = -1;
+            double rem = -1e300;
+            for (int i = 0; i < n; ++i) {
+                const Lane& l = g->lanes[size_t(i)];
+                if (l.n_inst == 0) continue;
+                const double r = double(budget) * l.weight_bytes / wsum - double(q[size_t(i)]);
+                if (r > rem) {
+                    rem = r;
+                    best = i;
+                }
+            }
+            q[size_t(best)]++;
+            used++;
+        }
     }
     // No host wait: every lane whose quota grows makes its stream wait for the
     // work already queued on the lanes whose quota shrinks (an event recorded

@@ -62,7 +62,12 @@ MODELS = ["1b", "3b", "7b", "1b", "3b", "7b", "1b", "3b"]
 BATCH = 8
 LANES = int(os.environ.get("MESH_BENCH_LANES", "8"))  # one execution lane per co-located instance
 KV_POOL = 100 << 30
-E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "4,6,8").split(",")]
+KV_PREALLOC_GB = 96     # e2e: physical KV granules created when the data plane opens (not on the serving path)
+# e2e: 512 MiB physical KV granules. cuMemMap / cuMemSetAccess cost milliseconds per call once dozens
+# of instances hold mappings; at 80 instance starts 32 MiB granules spent 7.8 s of host time in them,
+# 512 MiB granules 2.4 s (tools/e2e_c3.py, MESH_GPU_KV_GRANULE_MB)
+KV_GRANULE_MB = 512
+E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "8,12,16").split(",")]
 WATERMARK = 20.0
 CPU_SAMPLE_S = 15.0     # bounded CPU baseline sample
 CPU_MAX_SEQ = 1160      # >= the longest I + O of the length set (1139)
@@ -561,6 +566,8 @@ def run_e2e_scale(device: int, scale: int):
 
     from paper_2507_00507_b200 import control, gpu
     os.environ["MESH_GPU_LANES"] = str(LANES)  # the data plane under the control plane: one lane per instance
+    os.environ.setdefault("MESH_GPU_KV_PREALLOC_GB", str(KV_PREALLOC_GB))  # physical KV granules created at open
+    os.environ.setdefault("MESH_GPU_KV_GRANULE_MB", str(KV_GRANULE_MB))
     cfg = os.path.join(C3_DIR, f"s{scale}", "config.json")
     with control.Experiment(cfg) as exp:
         exp.out_dir(tempfile.mkdtemp(prefix="mesh_e2e_"))
@@ -571,7 +578,8 @@ def run_e2e_scale(device: int, scale: int):
                  "slo_compliant_decode_tokens", "output_tokens", "gpu.kernel_launches", "gpu_instances_avg",
                  "gpu_instances_max", "gpu.instance_starts", "gpu.weight_cache_hits", "gpu.blocks_moved",
                  "gpu.swap_out_bytes", "gpu.migrations", "evictions", "run_length_s", "gpu.dp_ms.step",
-                 "gpu.dp_ms.kv_resize", "gpu.dp_ms.instance_create", "gpu.host_ms.step_wait", "displacements"]
+                 "gpu.dp_ms.kv_resize", "gpu.dp_ms.instance_create", "gpu.host_ms.step_wait", "displacements",
+                 "gpu_models_avg", "gpu_models_max"]
         m = {k: exp.metric(k) for k in names}
     m["scale"] = scale
     m["slo_tokens"] = m["slo_compliant_decode_tokens"] + m["slo_compliant"]  # + each compliant request's first token
@@ -628,6 +636,8 @@ def run_fleet_load(devices, load: int):
 
     from paper_2507_00507_b200 import control, gpu
     os.environ["MESH_GPU_LANES"] = str(LANES)
+    os.environ.setdefault("MESH_GPU_KV_PREALLOC_GB", str(KV_PREALLOC_GB))
+    os.environ.setdefault("MESH_GPU_KV_GRANULE_MB", str(KV_GRANULE_MB))
     n = len(devices)
     with control.Experiment(fleet_scenario(n, load * n)) as exp:
         exp.out_dir(tempfile.mkdtemp(prefix="mesh_fleet_out_"))
@@ -636,6 +646,7 @@ def run_fleet_load(devices, load: int):
         names = ["wall_s", "gpu.steps", "gpu.h2d_bytes", "gpu.d2h_bytes", "gpu.lane_busy_s", "slo_compliant_rate",
                  "total_requests", "slo_compliant", "slo_compliant_decode_tokens", "output_tokens",
                  "gpu_instances_avg", "gpu_instances_max", "gpu_nodes_used", "gpu_nodes_avg", "gpu.instance_starts",
+                 "gpu_models_avg", "gpu_models_max",
                  "gpu.migrations", "gpu.migrate_bytes", "gpu.swap_out_bytes", "displacements", "evictions"]
         m = {k: exp.metric(k) for k in names}
     m["load_per_gpu"] = load
@@ -658,6 +669,8 @@ def run_fleet(n: int):
             "capacity_load_per_gpu": head["load_per_gpu"] if ok else None,
             "slo_compliant_rate": head["slo_compliant_rate"], "wall_s": head["wall_s"],
             "models_per_gpu": {"time_avg": head["gpu_instances_avg"], "max": head["gpu_instances_max"],
+                               "distinct_models_time_avg": head["gpu_models_avg"],
+                               "distinct_models_max": head["gpu_models_max"],
                                "gpu_nodes_used": head["gpu_nodes_used"]},
             "sweep": [{k: r[k] for k in ("load_per_gpu", "total_requests", "slo_compliant_rate", "tokens_at_slo_per_s",
                                          "wall_s", "gpu_instances_avg", "gpu_instances_max", "gpu_nodes_used",
@@ -684,7 +697,10 @@ def run_e2e(device: int, d: Dist, scales):
             "capacity_scale": head["scale"] if ok else None,
             "capacity_rule": "highest load scale with wall-clock slo_compliant_rate >= 0.99",
             "slo_compliant_rate": head["slo_compliant_rate"], "wall_s": wall_max,
-            "models_per_gpu": {"time_avg": head["gpu_instances_avg"], "max": head["gpu_instances_max"]},
+            "models_per_gpu": {"time_avg": head["gpu_instances_avg"], "max": head["gpu_instances_max"],
+                               "distinct_models_time_avg": head["gpu_models_avg"],
+                               "distinct_models_max": head["gpu_models_max"],
+                               "note": "model instances resident per GPU (replicas of a model share its weights)"},
             "lane_busy_frac": head["gpu.lane_busy_s"] / (LANES * head["wall_s"]) if head["wall_s"] else None,
             "sweep": [{k: r[k] for k in ("scale", "total_requests", "slo_compliant_rate", "tokens_at_slo_per_s",
                                          "wall_s", "gpu_instances_avg", "gpu_instances_max", "gpu.steps",

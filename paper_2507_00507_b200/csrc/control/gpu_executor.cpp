@@ -105,6 +105,9 @@ GpuExecutor::GpuExecutor(const std::string& lib_path, std::vector<int> devices, 
         cfg.sm_quota = 0;
         cfg.kv_pool_bytes = pool_bytes_;
         cfg.prompt_seed = 1234;
+        if (const char* e = std::getenv("MESH_GPU_KV_GRANULE_MB")) cfg.kv_granule_bytes = std::atoll(e) << 20;
+        // pinned swap space pinned at open (evictions then never pin on the serving path)
+        if (const char* e = std::getenv("MESH_GPU_SWAP_POOL_MB")) cfg.swap_pool_mb = std::max(0, std::atoi(e));
         mesh_gpu* h = nullptr;
         if (api_->open(&cfg, &h) != MESH_OK) throw SimError("attach_gpu: mesh_gpu_open failed on device " + std::to_string(dev));
         handles_.push_back(h);

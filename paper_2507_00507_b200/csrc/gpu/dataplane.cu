@@ -1379,6 +1379,23 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->st.peer_devices = (int64_t)g->peers.size();
         // pinned swap space, pinned once up front (cudaHostAlloc of GBs takes ~0.1-1 s)
         if (cfg->swap_pool_mb > 0) host_pool().reserve(size_t(cfg->swap_pool_mb) << 20);
+        // MESH_GPU_KV_PREALLOC_GB: create that much of the KV pool's physical granules
+        // now. cuMemCreate costs ~1-4 ms per 32 MiB granule once dozens of instances
+        // hold mappings (C3 e2e, 80 instance starts: 10.8 s of host time); created
+        // up front, a grow on the serving path only maps.
+        if (const char* e = std::getenv("MESH_GPU_KV_PREALLOC_GB")) {
+            const long long want = std::min<long long>(g->pool.limit, (long long)(std::atof(e) * double(1LL << 30)));
+            CUmemAllocationProp pp = {};
+            pp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+            pp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+            pp.location.id = cfg->device;
+            for (long long have = 0; have + (long long)g->pool.gran <= want; have += (long long)g->pool.gran) {
+                CUmemGenericAllocationHandle h;
+                if (drv().create(&h, g->pool.gran, &pp, 0) != CUDA_SUCCESS) break;
+                g->pool.all.push_back(h);
+                g->pool.free_list.push_back(h);
+            }
+        }
         g->pool.device = cfg->device;
         CUmemAllocationProp prop2 = {};
         prop2.type = CU_MEM_ALLOCATION_TYPE_PINNED;

@@ -24,7 +24,9 @@ serving path rather than the arrival rate.
                 SLO compliance come from CUDA events, not from the tables; the
                 admission replay divides its pessimistic step costs by the
                 measured co-location speedup (instances step concurrently on
-                their SM quotas, tools/measure_colocation.py).
+                their SM quotas, tools/measure_colocation.py); replicas of a
+                model on the GPU share its weights (runtime.shared_weights:
+                the data plane keeps one weight set per model per GPU).
 
     python scenarios/make_scenarios.py
 """
@@ -82,7 +84,8 @@ def make_c3():
                          "window_s": C3_WINDOW, "sample_functions": 8},
             "slo": {"ttft_base_s": 2.0, "ttft_per_token_divisor": 512.0, "tpot_s": 0.25},
             "policy": {"kind": "mesh", "watermark_pct": 20.0, "keep_alive_s": 1.0},
-            "runtime": {"clock": "wall", "slots": 64, "colocation_speedup": C3_COLOCATION_SPEEDUP},
+            "runtime": {"clock": "wall", "slots": 64, "colocation_speedup": C3_COLOCATION_SPEEDUP,
+                        "shared_weights": True},
             "output": {"dir": os.path.relpath(os.path.join(d, "out"), ROOT), "event_log": False},
         }
         with open(os.path.join(d, "config.json"), "w") as fh:

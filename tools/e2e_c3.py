@@ -27,6 +27,8 @@ def main():
     out = sys.argv[2] if len(sys.argv) > 2 else os.path.join("gpurun_out", f"e2e_s{k}")
     os.makedirs(out, exist_ok=True)
     os.environ["MESH_GPU_LANES"] = str(bench.LANES)
+    os.environ.setdefault("MESH_GPU_KV_PREALLOC_GB", str(bench.KV_PREALLOC_GB))
+    os.environ.setdefault("MESH_GPU_KV_GRANULE_MB", str(bench.KV_GRANULE_MB))
     cfg = os.path.join(bench.C3_DIR, f"s{k}", "config.json")
     with control.Experiment(cfg) as exp:
         for kv in sys.argv[3:]:
@@ -40,7 +42,7 @@ def main():
                  "gpu.host_ms.step_issue", "gpu.host_ms.step_wait", "gpu.instance_starts", "gpu_instances_avg",
                  "gpu_instances_max", "gpu.kv_reclaims", "gpu.host_ms.vmm", "gpu.vmm_calls", "gpu.vmm_unmaps",
                  "gpu.dp_ms.instance_create", "gpu.dp_ms.instance_destroy", "gpu.dp_ms.kv_resize", "gpu.dp_ms.step",
-                 "gpu.weight_cache_hits", "gpu.migrations", "evictions"]
+                 "gpu.weight_cache_hits", "gpu.migrations", "evictions", "gpu_models_avg", "gpu_models_max"]
         m = {n: exp.metric(n) for n in names}
     rows = list(csv.DictReader(open(os.path.join(out, "requests.csv"))))
     by = {}

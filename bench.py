@@ -61,12 +61,16 @@ UNIT = "tokens/s"
 MODELS = ["1b", "3b", "7b", "1b", "3b", "7b", "1b", "3b"]
 BATCH = 8
 LANES = int(os.environ.get("MESH_BENCH_LANES", "8"))  # one execution lane per co-located instance
-KV_POOL = 100 << 30
-KV_PREALLOC_GB = 96     # e2e: physical KV granules created when the data plane opens (not on the serving path)
-# e2e: 512 MiB physical KV granules. cuMemMap / cuMemSetAccess cost milliseconds per call once dozens
+KV_POOL = 100 << 30     # value leg: KV pool per device
+# e2e / fleet: the control plane's KV budget (node mem 150 GB - the resident models' weights, ~97 GB)
+# plus each instance's physical rounding to whole granules (<= 256 MiB x ~66 instances); 53 GB of
+# weights + 116 GB of KV + lane scratch fit the B200's 179 GB
+E2E_KV_POOL = 116 << 30
+KV_PREALLOC_GB = 112    # e2e: physical KV granules created when the data plane opens (not on the serving path)
+# e2e: 256 MiB physical KV granules. cuMemMap / cuMemSetAccess cost milliseconds per call once dozens
 # of instances hold mappings; at 80 instance starts 32 MiB granules spent 7.8 s of host time in them,
-# 512 MiB granules 2.4 s (tools/e2e_c3.py, MESH_GPU_KV_GRANULE_MB)
-KV_GRANULE_MB = 512
+# 128 MiB 4.3 s, 512 MiB 2.4 s (tools/e2e_c3.py, MESH_GPU_KV_GRANULE_MB)
+KV_GRANULE_MB = 256
 E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "8,12,16").split(",")]
 WATERMARK = 20.0
 CPU_SAMPLE_S = 15.0     # bounded CPU baseline sample
@@ -571,7 +575,7 @@ def run_e2e_scale(device: int, scale: int):
     cfg = os.path.join(C3_DIR, f"s{scale}", "config.json")
     with control.Experiment(cfg) as exp:
         exp.out_dir(tempfile.mkdtemp(prefix="mesh_e2e_"))
-        exp.attach_gpu([device], KV_POOL, gpu.LIB_PATH)
+        exp.attach_gpu([device], E2E_KV_POOL, gpu.LIB_PATH)
         exp.run()
         names = ["wall_s", "gpu.steps", "gpu.decode_tokens", "gpu.prefill_tokens", "gpu.h2d_bytes", "gpu.d2h_bytes",
                  "gpu.device_ms", "gpu.lane_busy_s", "slo_compliant_rate", "total_requests", "slo_compliant",
@@ -641,7 +645,7 @@ def run_fleet_load(devices, load: int):
     n = len(devices)
     with control.Experiment(fleet_scenario(n, load * n)) as exp:
         exp.out_dir(tempfile.mkdtemp(prefix="mesh_fleet_out_"))
-        exp.attach_gpu(list(devices), KV_POOL, gpu.LIB_PATH)
+        exp.attach_gpu(list(devices), E2E_KV_POOL, gpu.LIB_PATH)
         exp.run()
         names = ["wall_s", "gpu.steps", "gpu.h2d_bytes", "gpu.d2h_bytes", "gpu.lane_busy_s", "slo_compliant_rate",
                  "total_requests", "slo_compliant", "slo_compliant_decode_tokens", "output_tokens",

@@ -35,7 +35,7 @@ def main():
             key, val = kv.split("=", 1)
             exp.set(key, json.loads(val) if val[:1] in "0123456789-[{tf" else val)
         exp.out_dir(out)
-        exp.attach_gpu([0], bench.KV_POOL, gpu.LIB_PATH)
+        exp.attach_gpu([0], bench.E2E_KV_POOL, gpu.LIB_PATH)
         exp.run()
         names = ["wall_s", "slo_compliant_rate", "total_requests", "gpu.steps", "gpu.lane_busy_s",
                  "gpu.host_ms.instance_create", "gpu.host_ms.instance_destroy", "gpu.host_ms.kv_resize",

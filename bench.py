@@ -596,7 +596,8 @@ FLEET_WINDOW = 30.0
 FLEET_LOADS = [int(x) for x in os.environ.get("MESH_BENCH_FLEET_LOADS", "1,2,3").split(",")]
 
 
-def fleet_scenario(n_nodes: int, k: float, seed: int = 4242) -> str:
+def fleet_scenario(n_nodes: int, k: float, seed: int = 4242, window: float = FLEET_WINDOW,
+                   mem_gb: float = 150.0) -> str:
     """C5 restated for the fleet e2e: 32 functions cycling [1b, 3b, 7b] on n_nodes GPU
     nodes (node i -> device i), the acceptance overload generator's three phases
     (proj/tests/acceptance_main.cpp:462-488: 0.08, 0.28, then 0.8 for 6 hot functions
@@ -610,10 +611,10 @@ def fleet_scenario(n_nodes: int, k: float, seed: int = 4242) -> str:
     for f in range(FLEET_FUNCS):
         fn = f"fn{f:02d}"
         for t0, t1, rate in ((0.0, 0.2, 0.08), (0.2, 0.6, 0.28), (0.6, 1.0, 0.8 if f < 6 else 0.03)):
-            t = t0 * FLEET_WINDOW
+            t = t0 * window
             while True:
                 t += rng.expovariate(rate * k)
-                if t >= t1 * FLEET_WINDOW:
+                if t >= t1 * window:
                     break
                 rows.append((t, fn))
     rows.sort()
@@ -623,10 +624,10 @@ def fleet_scenario(n_nodes: int, k: float, seed: int = 4242) -> str:
             fh.write(f"{t:.6f},{fn}\n")
     with open(os.path.join(C3_DIR, "s1", "config.json")) as fh:
         cfg = json.load(fh)
-    cfg["cluster"]["nodes"] = [{"class": "gpu", "count": n_nodes, "mem_gb": 150.0}]
+    cfg["cluster"]["nodes"] = [{"class": "gpu", "count": n_nodes, "mem_gb": mem_gb}]
     cfg["models"]["assignment"] = [["1b", "3b", "7b"][f % 3] for f in range(FLEET_FUNCS)]
-    cfg["workload"].update({"trace": os.path.join(d, "trace.csv"), "window_s": FLEET_WINDOW,
-                            "sample_functions": FLEET_FUNCS})
+    cfg["workload"].update({"trace": os.path.join(d, "trace.csv"), "window_s": window,
+                            "sample_functions": len({fn for _, fn in rows})})
     cfg["output"] = {"dir": os.path.join(d, "out"), "event_log": False}
     path = os.path.join(d, "config.json")
     with open(path, "w") as fh:
@@ -683,6 +684,37 @@ def run_fleet(n: int):
             "trace": "acceptance overload generator (32 functions, three phases) in a 30 s window, rates x "
                      "(per-GPU load x n GPUs)",
             "api": "llmmesh.h llm_experiment_run + llm_experiment_attach_gpu(devices 0..n-1), runtime.clock = wall"}
+
+
+def run_c4(device: int):
+    try:
+        return _run_c4(device)
+    except Exception as e:  # wall-clock decisions are timing-dependent: the reference's eviction
+        # ping-pong defect can end a C4 run; report it instead of failing the bench
+        return {"error": str(e)}
+
+
+def _run_c4(device: int):
+    """C4 beside the headline (scenarios/c4_b200: 7B + 13B under KV pressure, wall clock):
+    evictions swap running requests' KV to pinned host memory inside the timed region."""
+    import tempfile
+
+    from paper_2507_00507_b200 import control, gpu
+    os.environ["MESH_GPU_LANES"] = str(LANES)
+    os.environ.setdefault("MESH_GPU_SWAP_POOL_MB", "4096")
+    with control.Experiment(os.path.join(ROOT, "scenarios", "c4_b200", "config.json")) as exp:
+        exp.out_dir(tempfile.mkdtemp(prefix="mesh_c4_"))
+        exp.attach_gpu([device], 48 << 30, gpu.LIB_PATH)
+        exp.run()
+        names = ["wall_s", "slo_compliant_rate", "total_requests", "slo_compliant", "slo_compliant_decode_tokens",
+                 "evictions", "gpu.swap_out_bytes", "gpu.swap_in_bytes", "gpu.steps", "gpu.decode_tokens",
+                 "gpu_instances_avg",
+                 "gpu.blocks_moved"]
+        m = {k: exp.metric(k) for k in names}
+    m["tokens_at_slo_per_s"] = (m["slo_compliant_decode_tokens"] + m["slo_compliant"]) / m["wall_s"]
+    m["workload"] = ("C4: 7B + 13B functions on a 40 GB node (KV pressure, output estimator fixed low): "
+                     "ensure_kv_capacity evicts, the data plane swaps KV to pinned host memory and back")
+    return m
 
 
 def run_e2e(device: int, d: Dist, scales):
@@ -760,6 +792,7 @@ def run_ours(args, d: Dist):
         e2e = None
     elif d.ws == 1:
         e2e = run_e2e(device, d, E2E_SCALES)
+        e2e["c4"] = run_c4(device)
     else:
         # the fleet: rank 0 drives every device through the control plane's placement
         # (one host event loop, peer access between the devices); the other ranks wait

@@ -327,12 +327,13 @@ std::map<std::string, double> GpuExecutor::metrics() const {
     m["gpu.host_ms.kv_resize"] = host_ms_kv_;
     m["gpu.host_ms.step_issue"] = host_ms_step_;
     m["gpu.host_ms.step_wait"] = host_ms_wait_;
-    double swap = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0, vmm_calls = 0, vmm_ms = 0, reclaims = 0,
+    double swap = 0, swap_in = 0, mig = 0, moved = 0, launches = 0, h2d = 0, d2h = 0, vmm_calls = 0, vmm_ms = 0, reclaims = 0,
            wcache = 0, unmaps = 0, dp_create = 0, dp_destroy = 0, dp_kv = 0, dp_step = 0;
     for (mesh_gpu* h : handles_) {
         mesh_gpu_stats st{};
         api_->stats_get(h, &st);
         swap += static_cast<double>(st.swap_out_bytes);
+        swap_in += static_cast<double>(st.swap_in_bytes);
         mig += static_cast<double>(st.migrate_bytes);
         moved += static_cast<double>(st.blocks_moved);
         launches += static_cast<double>(st.kernel_launches);
@@ -359,6 +360,7 @@ std::map<std::string, double> GpuExecutor::metrics() const {
     m["gpu.host_ms.vmm"] = vmm_ms;
     m["gpu.kv_reclaims"] = reclaims;
     m["gpu.swap_out_bytes"] = swap;
+    m["gpu.swap_in_bytes"] = swap_in;
     m["gpu.migrate_bytes"] = mig;
     m["gpu.migrations"] = static_cast<double>(migrations_);
     m["gpu.migrate_fallbacks"] = static_cast<double>(migrate_fallbacks_);

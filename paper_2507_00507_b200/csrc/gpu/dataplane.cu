@@ -1619,6 +1619,20 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
                 e = cudaMallocAsync((void**)&in->wmem, total, st);
             }
             if (e != cudaSuccess) {
+                // then the KV pool's created-but-unmapped granules (MESH_GPU_KV_PREALLOC_GB):
+                // weights come first, the pool re-creates granules on demand
+                cudaGetLastError();
+                CK(cudaStreamSynchronize(g->side));
+                for (auto h : g->pool.free_list) {
+                    drv().release(h);
+                    g->pool.all.erase(std::find(g->pool.all.begin(), g->pool.all.end(), h));
+                }
+                g->pool.free_list.clear();
+                cudaMemPool_t mp;
+                if (cudaDeviceGetDefaultMemPool(&mp, g->cfg.device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
+                e = cudaMallocAsync((void**)&in->wmem, total, st);
+            }
+            if (e != cudaSuccess) {
                 cudaGetLastError();
                 give_back_bufs();
                 throw MeshError(MESH_ERR_NOMEM, "weights: cudaMallocAsync of " + std::to_string(total) + " bytes failed");

@@ -28,6 +28,14 @@ serving path rather than the arrival rate.
                 model on the GPU share its weights (runtime.shared_weights:
                 the data plane keeps one weight set per model per GPU).
 
+  c4_b200       BASELINE configs[3] (C4): 7B + 13B functions (two each) on one
+                B200 whose node memory (44 GB) is far below their KV demand, with the
+                output-length estimator fixed low (avg_output_seed 4, min_total_len
+                256; the pattern of proj/tests/test_cluster.cpp:289-325), so
+                ensure_kv_capacity evicts running requests (cluster.cpp:730-751) and
+                the data plane swaps their KV to pinned host memory and back. Hot /
+                cold Poisson arrivals for 30 s, measured tables, wall clock.
+
     python scenarios/make_scenarios.py
 """
 import json
@@ -59,6 +67,39 @@ def c3_rate(scale, window):
             return 0.28 * scale
         return (0.8 if fn in hot else 0.03) * scale
     return f
+
+
+def make_c4(d=None, hot=3.0, cold=1.0, mem_gb=44.0):
+    from paper_2507_00507_b200 import tables
+    d = d or os.path.join(HERE, "c4_b200")
+    os.makedirs(d, exist_ok=True)
+    lengths_csv(os.path.join(d, "lengths.csv"), 200, 58)
+    rate = lambda f, t, ph: hot if f in ("fn00", "fn01") else cold  # noqa: E731
+    n = poisson_trace(os.path.join(d, "trace.csv"), [f"fn{i:02d}" for i in range(4)], 30.0, rate, 58)
+    under = {"min_total_len": 256, "avg_output_seed": 4, "avg_output_fixed": True}
+    tpls = []
+    for t in ("7b", "13b"):
+        tt = dict(TEMPLATES[t])
+        tt.update(under)
+        tpls.append(tt)
+    cfg = {
+        "seed": 58,
+        "cluster": {"nodes": [{"class": "gpu", "count": 1, "mem_gb": mem_gb}]},
+        "models": {"templates": tpls, "assignment": ["7b", "13b"]},
+        "perf": {"overestimate_factor": 1.10, "max_len": 4096, "max_batch": 8,
+                 "tables": {f"{sc}:gpu": os.path.relpath(tables.measured_table_path(sc), ROOT) for sc in ("7b", "13b")},
+                 "gpu": tables.measured_cost_params()},
+        "workload": {"trace": os.path.relpath(os.path.join(d, "trace.csv"), ROOT),
+                     "lengths": os.path.relpath(os.path.join(d, "lengths.csv"), ROOT),
+                     "window_s": 30.0, "sample_functions": 4},
+        "slo": {"ttft_base_s": 2.0, "ttft_per_token_divisor": 512.0, "tpot_s": 0.25},
+        "policy": {"kind": "mesh", "watermark_pct": 20.0, "keep_alive_s": 1.0},
+        "runtime": {"clock": "wall", "slots": 64, "colocation_speedup": C3_COLOCATION_SPEEDUP, "shared_weights": True},
+        "output": {"dir": os.path.relpath(os.path.join(d, "out"), ROOT), "event_log": False},
+    }
+    with open(os.path.join(d, "config.json"), "w") as fh:
+        json.dump(cfg, fh, indent=2)
+    print("c4_b200:", n, "requests")
 
 
 def make_c3():
@@ -115,6 +156,7 @@ def main():
         json.dump(cfg, fh, indent=2)
     print("c2_saturated_b200: same trace, measured B200 tables")
     make_c3()
+    make_c4()
 
 
 if __name__ == "__main__":

@@ -79,9 +79,8 @@ def test_fleet_two_nodes_one_device_wall_clock(tmp_path, monkeypatch):
     import bench
     monkeypatch.chdir(ROOT)
     monkeypatch.setenv("MESH_GPU_LANES", "4")
-    cfg = bench.fleet_scenario(2, 1.0)
+    cfg = bench.fleet_scenario(2, 1.0, window=12.0, mem_gb=60.0)  # two 60 GB nodes share one B200
     with control.Experiment(cfg) as exp:
-        exp.set("workload.window_s", 12.0)
         exp.out_dir(str(tmp_path))
         exp.attach_gpu([0, 0], 24 << 30, gpu.LIB_PATH)
         exp.run()

@@ -707,7 +707,7 @@ def _run_c4(device: int):
         exp.attach_gpu([device], 48 << 30, gpu.LIB_PATH)
         exp.run()
         names = ["wall_s", "slo_compliant_rate", "total_requests", "slo_compliant", "slo_compliant_decode_tokens",
-                 "evictions", "gpu.swap_out_bytes", "gpu.swap_in_bytes", "gpu.steps", "gpu.decode_tokens",
+                 "evictions", "pingpong_drops", "gpu.swap_out_bytes", "gpu.swap_in_bytes", "gpu.steps", "gpu.decode_tokens",
                  "gpu_instances_avg",
                  "gpu.blocks_moved"]
         m = {k: exp.metric(k) for k in names}

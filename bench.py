@@ -712,7 +712,7 @@ def _run_c4(device: int):
                  "gpu.blocks_moved"]
         m = {k: exp.metric(k) for k in names}
     m["tokens_at_slo_per_s"] = (m["slo_compliant_decode_tokens"] + m["slo_compliant"]) / m["wall_s"]
-    m["workload"] = ("C4: 7B + 13B functions on a 40 GB node (KV pressure, output estimator fixed low): "
+    m["workload"] = ("C4: 7B + 13B functions on a 44 GB node (KV pressure, output estimator fixed low): "
                      "ensure_kv_capacity evicts, the data plane swaps KV to pinned host memory and back")
     return m
 

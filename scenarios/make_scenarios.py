@@ -69,7 +69,7 @@ def c3_rate(scale, window):
     return f
 
 
-def make_c4(d=None, hot=3.0, cold=1.0, mem_gb=44.0):
+def make_c4(d=None, hot=6.0, cold=1.0, mem_gb=44.0):
     from paper_2507_00507_b200 import tables
     d = d or os.path.join(HERE, "c4_b200")
     os.makedirs(d, exist_ok=True)

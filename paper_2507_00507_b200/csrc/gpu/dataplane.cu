@@ -1254,6 +1254,7 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     a.w = in.w;
     a.kv_base = reinterpret_cast<uint8_t*>(in.va);
     a.block_bytes = in.block_bytes;
+    a.kv_blocks = (long long)(in.va_size / size_t(in.block_bytes));
     a.bt_row = in.d_block_table + size_t(r.slot) * in.bt_stride;
     a.slot = r.slot;
     a.L = L;

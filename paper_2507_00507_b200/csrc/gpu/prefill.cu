@@ -11,6 +11,12 @@
 // add, silu(gate)*up. Attention is causal over the paged cache.
 #include "prefill.cuh"
 
+#include <string>
+#include <cstring>
+#include <cstdio>
+#include <chrono>
+#include <thread>
+
 #include <cuda.h>
 #include <math.h>
 #include <stdlib.h>
@@ -626,8 +632,340 @@ __global__ void __launch_bounds__(PA_THREADS) pf_attn(const __grid_constant__ Pr
     }
 }
 
+// ---------------------------------------------------------------------------
+// Causal attention on the 5th-gen tensor cores (tcgen05, TMEM accumulators).
+// Block = 128 queries of one head (the UMMA M); keys in 64-token chunks.
+//   warp 0      TMA producer: every 16-token KV block of the chunk is two (dh 64:
+//               one) 2 KB boxes per K and V, copied from the paged cache into the
+//               canonical SW128 layout (the cache's chunk swizzle by slot & 7 IS
+//               the 128-byte swizzle of an 8-row atom: the bytes land verbatim)
+//   warp 1      TMEM owner + single-thread MMA issuer:
+//                 S[j & 1] = Q . K_j^T   (M 128, N 64, K = dh; both K-major)
+//                 O       += P_j . V_j   (M 128, N dh, K 64; V read MN-major)
+//               S of chunk j+1 is issued before P_j is ready, so it overlaps the
+//               softmax of chunk j
+//   warps 2-5   softmax, one query row per thread straight from TMEM: causal
+//               mask, running max in the log2 domain with a lazy O rescale (only
+//               when the max grows by more than 2^8; numerator and denominator
+//               share the reference, so the result is exact), P -> shared memory
+//               as bf16 in the SW128 K-major layout, final O / l -> bf16
+// TMEM: O in columns [0, dh), the two S buffers at 128 and 192.
+constexpr int TA_QT = 128, TA_KC = 64, TA_THREADS = 192, TA_STAGES = 3;
+// MESH_PF_ATTN_DEBUG: bounded mbarrier waits that record (block, thread, barrier, chunk) in
+// host-mapped memory on a timeout and give up (results are then garbage), to locate a hang.
+__device__ int* g_ta_dbg = nullptr;
+__device__ __forceinline__ void ta_wait(uint64_t* bar, uint32_t parity, int id, int j) {
+    if (!g_ta_dbg) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    if ((threadIdx.x & 31) == 0) {  // heartbeat: (barrier, chunk) each warp is about to wait on
+        const int cta = blockIdx.y * gridDim.x + blockIdx.x;
+        if (cta < 150) reinterpret_cast<volatile int*>(g_ta_dbg)[512 + cta * 6 + (threadIdx.x >> 5)] = (id << 16) | j;
+    }
+    for (long long spin = 0; !mbar_try_wait(bar, parity); ++spin)
+        if (spin > (1ll << 40)) {
+            volatile int* d = g_ta_dbg;
+            const int slot = atomicAdd(const_cast<int*>(g_ta_dbg), 1) % 60;
+            d[1 + slot * 6 + 0] = blockIdx.x;
+            d[1 + slot * 6 + 1] = blockIdx.y;
+            d[1 + slot * 6 + 2] = threadIdx.x;
+            d[1 + slot * 6 + 3] = id;
+            d[1 + slot * 6 + 4] = j;
+            d[1 + slot * 6 + 5] = int(parity);
+            __threadfence_system();
+            return;
+        }
+}
+template <int DH>
+struct TaCfg {
+    static constexpr int HALVES = DH / 64;                // 128-byte K atoms per row
+    static constexpr int Q_HALF = TA_QT * 128;            // Q: [half][128 rows][128 B]
+    static constexpr int KV_HALF = TA_KC * 128;           // K or V: [half][64 keys][128 B]
+    static constexpr int K_BYTES = HALVES * KV_HALF;
+    static constexpr int STAGE = 2 * K_BYTES;             // K, then V
+    static constexpr int P_BYTES = TA_QT * 128;           // P: [128 queries][64 keys bf16]
+    static constexpr int Q_OFF = 0, ST_OFF = HALVES * Q_HALF, P_OFF = ST_OFF + TA_STAGES * STAGE;
+    static constexpr int BAR_OFF = P_OFF + P_BYTES;
+    static constexpr int SMEM = 1024 + BAR_OFF + 256;
+    static constexpr uint32_t TMEM_COLS = 256;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(TA_THREADS, 1)
+    pf_attn_tc(const __grid_constant__ PrefillArgs a, const __grid_constant__ CUtensorMap kvmap, int layer) {
+    using C = TaCfg<DH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+    uint64_t* kv_empty = kv_full + TA_STAGES;
+    uint64_t* s_full = kv_empty + TA_STAGES;  // [2]
+    uint64_t* s_empty = s_full + 2;           // [2]
+    uint64_t* p_full = s_empty + 2;
+    uint64_t* pv_done = p_full + 1;
+    uint64_t* q_ready = pv_done + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 1);
+
+    const Shape& s = a.s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nqt = (a.L + TA_QT - 1) / TA_QT;
+    const int qt = nqt - 1 - int(blockIdx.x);  // longest rows first
+    const int head = blockIdx.y, kvh = head / s.gq();
+    const int q0 = qt * TA_QT;
+    const int kmax = a.p0 + min(q0 + TA_QT, a.L) - 1;  // last key any query of the block sees
+    const int nchunks = kmax / TA_KC + 1;
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < TA_STAGES; ++i) {
+            mbar_init(kv_full + i, 1);
+            mbar_init(kv_empty + i, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(s_full + i, 1);
+            mbar_init(s_empty + i, 128);
+        }
+        mbar_init(p_full, 128);
+        mbar_init(pv_done, 1);
+        mbar_init(q_ready, 128);
+        fence_mbar_init();
+        prefetch_tmap(&kvmap);
+    }
+    if (warp == 1) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer
+            const int rK = ((layer * s.n_kv + kvh) * 2 + 0) * KV_BLOCK_TOKENS;
+            const int rV = ((layer * s.n_kv + kvh) * 2 + 1) * KV_BLOCK_TOKENS;
+            for (int j = 0; j < nchunks; ++j) {
+                const int st = j % TA_STAGES;
+                ta_wait(kv_empty + st, ((j / TA_STAGES) & 1) ^ 1, 1, j);
+                uint8_t* kb = sm + C::ST_OFF + st * C::STAGE;
+                mbar_arrive_expect_tx(kv_full + st, C::STAGE);
+#pragma unroll
+                for (int bi = 0; bi < TA_KC / KV_BLOCK_TOKENS; ++bi) {
+                    const int pos = j * TA_KC + bi * KV_BLOCK_TOKENS;
+                    // blocks past the last key: any mapped block (their rows are masked / zeroed)
+                    const int blk = a.bt_row[(pos <= kmax ? pos : 0) / KV_BLOCK_TOKENS];
+#pragma unroll
+                    for (int hh = 0; hh < C::HALVES; ++hh) {
+                        const int off = hh * C::KV_HALF + bi * KV_BLOCK_TOKENS * 128;
+                        tma_load_4d(kb + off, &kvmap, 0, hh, rK, blk, kv_full + st);
+                        tma_load_4d(kb + C::K_BYTES + off, &kvmap, 0, hh, rV, blk, kv_full + st);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer
+            constexpr uint32_t idesc_s = umma_idesc_bf16(TA_QT, TA_KC);
+            constexpr uint32_t idesc_o = umma_idesc_bf16(TA_QT, DH) | (1u << 16);  // B (V) MN-major
+            const uint32_t q_addr = smem_u32(sm + C::Q_OFF), p_addr = smem_u32(sm + C::P_OFF);
+            ta_wait(q_ready, 0, 2, 0);
+            tc_fence_after();
+            auto issue_s = [&](int j) {
+                const int st = j % TA_STAGES, sb = j & 1;
+                ta_wait(kv_full + st, (j / TA_STAGES) & 1, 3, j);
+                ta_wait(s_empty + sb, ((j >> 1) & 1) ^ 1, 4, j);
+                tc_fence_after();
+                const uint32_t k_addr = smem_u32(sm + C::ST_OFF + st * C::STAGE);
+#pragma unroll
+                for (int hh = 0; hh < C::HALVES; ++hh) {
+                    const uint64_t qd = umma_desc_sw128(q_addr + hh * C::Q_HALF);
+                    const uint64_t kd = umma_desc_sw128(k_addr + hh * C::KV_HALF);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)  // +32 B along the swizzled row per K = 16
+                        umma_bf16(tmem + 128u + uint32_t(sb * TA_KC), qd + 2 * k, kd + 2 * k, idesc_s, (hh | k) != 0);
+                }
+                umma_commit(s_full + sb);
+            };
+            issue_s(0);
+            for (int j = 0; j < nchunks; ++j) {
+                if (j + 1 < nchunks) issue_s(j + 1);
+                const int st = j % TA_STAGES;
+                ta_wait(p_full, j & 1, 5, j);
+                tc_fence_after();
+                const uint32_t v_addr = smem_u32(sm + C::ST_OFF + st * C::STAGE + C::K_BYTES);
+                const uint64_t pd = umma_desc_sw128(p_addr);
+#pragma unroll
+                for (int k = 0; k < TA_KC / 16; ++k)  // 16 keys = two 8-row groups = 2048 B of V
+                    umma_bf16(tmem, pd + 2 * k, umma_desc_sw128_mn(v_addr + k * 2048, C::KV_HALF), idesc_o,
+                              (j | k) != 0);
+                umma_commit(kv_empty + st);
+                umma_commit(pv_done);
+            }
+        }
+    } else {  // ---- softmax warps 2..5: thread = one query row (TMEM lane)
+        const int sub = warp & 3, row = sub * 32 + lane;
+        const uint32_t lane_addr = tmem + (uint32_t(sub * 32) << 16);
+        const int r = q0 + row;
+        {  // Q row -> canonical SW128 K-major (bf16, RoPE already applied)
+            const uint4* src = reinterpret_cast<const uint4*>(a.q + (size_t(r) * s.n_heads + head) * DH);
+#pragma unroll
+            for (int c = 0; c < DH / 8; ++c) {
+                const uint4 v = r < a.L ? src[c] : make_uint4(0, 0, 0, 0);
+                const int hh = c >> 3, cc = c & 7;
+                *reinterpret_cast<uint4*>(sm + C::Q_OFF + hh * C::Q_HALF + row * 128 + ((cc ^ (row & 7)) << 4)) = v;
+            }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(q_ready);
+        const int qpos = a.p0 + r;
+        const float sl2 = rsqrtf(float(DH)) * 1.4426950408889634f;
+        float mref = -INFINITY, l = 0.f;
+        for (int j = 0; j < nchunks; ++j) {
+            const int sb = j & 1, kbase = j * TA_KC;
+            ta_wait(s_full + sb, (j >> 1) & 1, 6, j);
+            tc_fence_after();
+            uint32_t sv[2][32];
+            tmem_ld32(lane_addr + 128u + uint32_t(sb * TA_KC), sv[0]);
+            tmem_ld32(lane_addr + 128u + uint32_t(sb * TA_KC + 32), sv[1]);
+            tc_fence_before();
+            mbar_arrive(s_empty + sb);
+            float p[64];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 64; ++k) {
+                const float v = __uint_as_float(sv[k >> 5][k & 31]);
+                p[k] = kbase + k <= qpos ? v * sl2 : -INFINITY;
+                mx = fmaxf(mx, p[k]);
+            }
+            if (j > 0) ta_wait(pv_done, (j - 1) & 1, 7, j);  // O stable, P buffer free
+            tc_fence_after();
+            // lazy rescale: only when a row's max grows by more than 2^8. tcgen05.ld / st are
+            // warp-collective, so the warp rescales if any of its rows must (others by 1)
+            const bool grow = mx > mref + 8.f;
+            const float corr = (grow && mref != -INFINITY) ? exp2f(mref - mx) : 1.f;
+            if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll 1
+                for (int c = 0; c < DH / 32; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32(lane_addr + uint32_t(c * 32), o);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+                    tmem_st32(lane_addr + uint32_t(c * 32), o);
+                }
+            }
+            l *= corr;
+            if (grow) mref = mx;
+            uint8_t* prow = sm + C::P_OFF + row * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                float e[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    e[i] = mref == -INFINITY ? 0.f : exp2f(p[c * 8 + i] - mref);
+                    l += e[i];
+                }
+                uint4 pk;
+                pk.x = pack_bf16x2(e[0], e[1]);
+                pk.y = pack_bf16x2(e[2], e[3]);
+                pk.z = pack_bf16x2(e[4], e[5]);
+                pk.w = pack_bf16x2(e[6], e[7]);
+                *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = pk;
+            }
+            if (j == nchunks - 1 && kmax < kbase + TA_KC - 1) {
+                // keys past the last one: P is 0 there, but 0 x NaN (unwritten cache rows)
+                // would still reach O through the MMA, so zero those V rows
+                uint8_t* vb = sm + C::ST_OFF + (j % TA_STAGES) * C::STAGE + C::K_BYTES;
+                const int k0 = kmax + 1 - kbase, n16 = (TA_KC - k0) * 8 * C::HALVES;
+                for (int i = row; i < n16; i += 128) {
+                    const int hh = i / ((TA_KC - k0) * 8), rem = i % ((TA_KC - k0) * 8);
+                    *reinterpret_cast<uint4*>(vb + hh * C::KV_HALF + (k0 + rem / 8) * 128 + (rem % 8) * 16) =
+                        make_uint4(0, 0, 0, 0);
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(p_full);
+        }
+        ta_wait(pv_done, (nchunks - 1) & 1, 8, nchunks);
+        tc_fence_after();
+        const float inv = 1.f / l;
+#pragma unroll 1
+        for (int c = 0; c < DH / 32; ++c) {
+            uint32_t o[32];
+            tmem_ld32(lane_addr + uint32_t(c * 32), o);
+            if (r < a.L) {
+                uint16_t* dst = a.attn + size_t(r) * s.d + head * DH + c * 32;
+#pragma unroll
+                for (int i = 0; i < 32; i += 8) {
+                    uint4 pk;
+                    pk.x = pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+                    pk.y = pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+                    pk.z = pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+                    pk.w = pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+                    *reinterpret_cast<uint4*>(dst + i) = pk;
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
+bool make_kvmap(CUtensorMap* m, const PrefillArgs& a);
+
+// MESH_PF_ATTN=mma selects the mma.sync kernel (kept as the A/B reference); default tcgen05.
+template <int DH>
+cudaError_t attn_tc_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
+    static bool cfg[MAX_DEVICES] = {};
+    const int dev = cur_device();
+    if (!cfg[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(pf_attn_tc<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             TaCfg<DH>::SMEM);
+        if (e != cudaSuccess) return e;
+        cfg[dev] = true;
+    }
+    CUtensorMap km;
+    if (!make_kvmap(&km, a)) return cudaErrorInvalidValue;
+    static int* dbg_host = nullptr;
+    if (getenv("MESH_PF_ATTN_DEBUG") && !dbg_host) {
+        int* dev = nullptr;
+        if (cudaHostAlloc((void**)&dbg_host, 16384, cudaHostAllocMapped) != cudaSuccess) return cudaErrorMemoryAllocation;
+        memset(dbg_host, 0, 16384);
+        cudaHostGetDevicePointer((void**)&dev, dbg_host, 0);
+        cudaMemcpyToSymbol(g_ta_dbg, &dev, sizeof(dev));
+        std::thread([] {  // watchdog: dump the heartbeats if the process is still here after 10 s
+            std::this_thread::sleep_for(std::chrono::seconds(10));
+            fprintf(stderr, "pf_attn_tc heartbeats (cta: warp0..5 = barrier<<16|chunk):\n");
+            for (int c = 0; c < 150; ++c) {
+                bool any = false;
+                for (int w = 0; w < 6; ++w) any |= dbg_host[512 + c * 6 + w] != 0;
+                if (!any) continue;
+                fprintf(stderr, "  cta %d:", c);
+                for (int w = 0; w < 6; ++w) fprintf(stderr, " %x", dbg_host[512 + c * 6 + w]);
+                fprintf(stderr, "\n");
+            }
+            fflush(stderr);
+        }).detach();
+        atexit([] {
+            const int n = dbg_host[0];
+            if (n) fprintf(stderr, "pf_attn_tc wait timeouts: %d\n", n);
+            for (int i = 0; i < n && i < 60; ++i)
+                fprintf(stderr, "  block (%d,%d) thread %d barrier %d chunk %d parity %d\n", dbg_host[1 + i * 6],
+                        dbg_host[2 + i * 6], dbg_host[3 + i * 6], dbg_host[4 + i * 6], dbg_host[5 + i * 6],
+                        dbg_host[6 + i * 6]);
+        });
+    }
+    dim3 grid((a.L + TA_QT - 1) / TA_QT, a.s.n_heads);
+    pf_attn_tc<DH><<<grid, TA_THREADS, TaCfg<DH>::SMEM, st>>>(a, km, layer);
+    return cudaGetLastError();
+}
+
 template <int DH>
 cudaError_t attn_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
+    static const bool use_mma = [] {
+        const char* e = getenv("MESH_PF_ATTN");
+        return e && std::string(e) == "mma";
+    }();
+    if (!use_mma) return attn_tc_launch<DH>(a, layer, st);
     static bool cfg[MAX_DEVICES] = {};
     const int dev = cur_device();
     if (!cfg[dev]) {
@@ -732,6 +1070,24 @@ bool make_wmap(CUtensorMap* m, const uint8_t* W, int N, int K) {
     cuuint32_t es[4] = {1, 1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<uint8_t*>(W), dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// The instance's KV region as a 4-D tensor {64 elements (128 B), halves of a row,
+// rows R = ((layer * n_kv + head) * 2 + k|v) * 16 + slot, blocks}: box {64, 1,
+// 16, 1} is one (block, layer, head, k|v) half: 16 rows x 128 B, the bytes of
+// an SW128 atom pair as the cache stores them.
+bool make_kvmap(CUtensorMap* m, const PrefillArgs& a) {
+    EncodeTiledFn enc = encode_tiled();
+    if (!enc) return false;
+    const Shape& s = a.s;
+    cuuint64_t dims[4] = {64, cuuint64_t(s.dh / 64), cuuint64_t(s.n_layers) * s.n_kv * 2 * KV_BLOCK_TOKENS,
+                          cuuint64_t(a.kv_blocks)};
+    cuuint64_t strides[3] = {128, cuuint64_t(s.dh) * 2, cuuint64_t(a.block_bytes)};
+    cuuint32_t box[4] = {64, 1, KV_BLOCK_TOKENS, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a.kv_base, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+               CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -11,6 +11,7 @@ struct PrefillArgs {
     Weights w;
     uint8_t* kv_base;
     long long block_bytes;
+    long long kv_blocks;  // blocks the instance's KV VA range can address (tensor-map extent)
     const int* bt_row;  // block table row of the request (device)
     int slot;
     int L;              // tokens in this pass

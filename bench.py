@@ -400,6 +400,9 @@ class Colocated:
         else:
             emit = self.clock + st["last_step_ms"] / 1e3      # no mark yet: steps back to back
         self.clock = max(self.clock, emit)
+        busy = self.lane_busy.setdefault(inst["id"], [0.0, 0])
+        busy[0] += st["last_step_ms"]
+        busy[1] += 1
         if kind == "decode":
             s = inst["shape"]
             ctx = sum(r["I"] + r["gen"] for r in reqs)
@@ -430,6 +433,7 @@ class Colocated:
         self.decode_bytes = self.decode_kernel_ms = 0.0
         self.decode_steps = self.prefill_steps = 0
         self.per_model = {}
+        self.lane_busy = {}  # instance -> [sum of its steps' device time (ms), steps]
         self.kv_grows = self.kv_shrinks = 0
 
 
@@ -828,6 +832,8 @@ def run_ours(args, d: Dist):
                    "decode_steps": node.decode_steps, "prefill_steps": node.prefill_steps,
                    "kv_grows": node.kv_grows, "kv_shrinks": node.kv_shrinks,
                    "kv_blocks_moved": g_stats["blocks_moved"],
+                   "lane_busy_frac": {str(i): round(v[0] / (1e3 * dev_s), 3) for i, v in sorted(node.lane_busy.items())},
+                   "lane_steps": {str(i): v[1] for i, v in sorted(node.lane_busy.items())},
                    "parallelism": f"{d.ws} independent co-located nodes"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,

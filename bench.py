@@ -118,10 +118,14 @@ class Dist:
                 torch.cuda.set_device(self.local)
             dist.init_process_group(backend=backend)
             self.dist, self.torch, self.backend = dist, torch, backend
+            # host-side barrier for the fleet leg: an NCCL barrier would leave a kernel spinning
+            # on every waiting rank's GPU -- the GPUs rank 0 is driving -- and a persistent decode
+            # grid needs all of its quota's SMs co-resident
+            self.cpu_pg = dist.new_group(backend="gloo") if backend == "nccl" else None
 
-    def barrier(self):
+    def barrier(self, host: bool = False):
         if self.ws > 1:
-            self.dist.barrier()
+            self.dist.barrier(group=self.cpu_pg if host else None)
 
     def reduce(self, x: float, op: str) -> float:
         if self.ws == 1:
@@ -134,6 +138,17 @@ class Dist:
     def close(self):
         if self.ws > 1:
             self.dist.destroy_process_group()
+
+
+class Solo:
+    """Dist stand-in for work one rank does alone (no collectives)."""
+    ws, rank = 1, 0
+
+    def barrier(self, host: bool = False):
+        pass
+
+    def reduce(self, x: float, op: str) -> float:
+        return x
 
 
 class Clocks:
@@ -800,9 +815,16 @@ def run_ours(args, d: Dist):
     else:
         # the fleet: rank 0 drives every device through the control plane's placement
         # (one host event loop, peer access between the devices); the other ranks wait
-        d.barrier()
-        e2e = run_fleet(d.ws) if d.rank == 0 else None
-        d.barrier()
+        d.barrier(host=True)
+        e2e = None
+        if d.rank == 0:
+            from paper_2507_00507_b200 import gpu
+            if gpu.lib().mesh_gpu_device_count() >= d.ws:
+                e2e = run_fleet(d.ws)
+            else:  # this rank sees only its own GPU (per-rank CUDA_VISIBLE_DEVICES): one node
+                e2e = run_e2e(device, Solo(), E2E_SCALES)
+                e2e["note"] = "fleet skipped: rank 0 sees fewer GPUs than ranks; single-node C3 e2e"
+        d.barrier(host=True)
     if d.rank != 0:
         return
     cpu = cpu_port_sample() if d.ws == 1 and not args.no_cpu else None

@@ -928,6 +928,264 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
     }
 }
 
+// Two query tiles per CTA, ping-ponged on the tensor core (FA4-style): query
+// tiles 2i and 2i+1 of one head share every K/V chunk (loaded once), and two
+// softmax warpgroups alternate with the MMA pipe -- while warpgroup A turns S_A
+// into P_A, the tensor core computes S_B / PV_B, and vice versa.
+//   warp 0: TMA producer; warp 1: MMA issuer (+ TMEM owner);
+//   warps 2-5: softmax of tile A, warps 6-9: softmax of tile B.
+// TMEM (512 columns): O_A [0, dh), O_B [128, 128 + dh), S_A [256, 320), S_B [384, 448).
+constexpr int T2_THREADS = 320;
+template <int DH>
+struct Ta2Cfg {
+    static constexpr int HALVES = DH / 64;
+    static constexpr int Q_HALF = TA_QT * 128;
+    static constexpr int Q_TILE = HALVES * Q_HALF;        // one tile's Q
+    static constexpr int KV_HALF = TA_KC * 128;
+    static constexpr int K_BYTES = HALVES * KV_HALF;
+    static constexpr int STAGE = 2 * K_BYTES;
+    static constexpr int P_TILE = TA_QT * 128;
+    static constexpr int Q_OFF = 0, ST_OFF = 2 * Q_TILE, P_OFF = ST_OFF + TA_STAGES * STAGE;
+    static constexpr int BAR_OFF = P_OFF + 2 * P_TILE;
+    static constexpr int SMEM = 1024 + BAR_OFF + 256;
+    static constexpr uint32_t TMEM_COLS = 512;
+};
+
+template <int DH>
+__global__ void __launch_bounds__(T2_THREADS, 1)
+    pf_attn_tc2(const __grid_constant__ PrefillArgs a, const __grid_constant__ CUtensorMap kvmap, int layer) {
+    using C = Ta2Cfg<DH>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
+    uint64_t* kv_empty = kv_full + TA_STAGES;
+    uint64_t* s_full = kv_empty + TA_STAGES;  // [tile]
+    uint64_t* s_empty = s_full + 2;           // [tile]
+    uint64_t* p_full = s_empty + 2;           // [tile]
+    uint64_t* pv_done = p_full + 2;           // [tile]
+    uint64_t* q_ready = pv_done + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 1);
+
+    const Shape& s = a.s;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nqt = (a.L + TA_QT - 1) / TA_QT, npair = (nqt + 1) / 2;
+    const int qp = npair - 1 - int(blockIdx.x);  // longest rows first
+    const int head = blockIdx.y, kvh = head / s.gq();
+    // tile t covers queries [q0[t], q0[t] + 128); tile B may not exist (odd tile count)
+    int q0[2], nch[2];
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+        q0[t] = (2 * qp + t) * TA_QT;
+        nch[t] = q0[t] < a.L ? (a.p0 + min(q0[t] + TA_QT, a.L) - 1) / TA_KC + 1 : 0;
+    }
+    const int nchunks = max(nch[0], nch[1]);
+    const int kmax = a.p0 + min(q0[nch[1] ? 1 : 0] + TA_QT, a.L) - 1;  // last key any query of the CTA sees
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < TA_STAGES; ++i) {
+            mbar_init(kv_full + i, 1);
+            mbar_init(kv_empty + i, 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(s_full + t, 1);
+            mbar_init(s_empty + t, 128);
+            mbar_init(p_full + t, 128);
+            mbar_init(pv_done + t, 1);
+        }
+        mbar_init(q_ready, 256);
+        fence_mbar_init();
+        prefetch_tmap(&kvmap);
+    }
+    if (warp == 1) tmem_alloc(smem_u32(tmem_slot), C::TMEM_COLS);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- TMA producer (one K/V stream for both tiles)
+            const int rK = ((layer * s.n_kv + kvh) * 2 + 0) * KV_BLOCK_TOKENS;
+            const int rV = ((layer * s.n_kv + kvh) * 2 + 1) * KV_BLOCK_TOKENS;
+            for (int j = 0; j < nchunks; ++j) {
+                const int st = j % TA_STAGES;
+                ta_wait(kv_empty + st, ((j / TA_STAGES) & 1) ^ 1, 1, j);
+                uint8_t* kb = sm + C::ST_OFF + st * C::STAGE;
+                mbar_arrive_expect_tx(kv_full + st, C::STAGE);
+#pragma unroll
+                for (int bi = 0; bi < TA_KC / KV_BLOCK_TOKENS; ++bi) {
+                    const int pos = j * TA_KC + bi * KV_BLOCK_TOKENS;
+                    const int blk = a.bt_row[(pos <= kmax ? pos : 0) / KV_BLOCK_TOKENS];
+#pragma unroll
+                    for (int hh = 0; hh < C::HALVES; ++hh) {
+                        const int off = hh * C::KV_HALF + bi * KV_BLOCK_TOKENS * 128;
+                        tma_load_4d(kb + off, &kvmap, 0, hh, rK, blk, kv_full + st);
+                        tma_load_4d(kb + C::K_BYTES + off, &kvmap, 0, hh, rV, blk, kv_full + st);
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // ---- MMA issuer: S_A(j), S_B(j), PV_A(j), S_A(j+1), PV_B(j), S_B(j+1), ...
+            constexpr uint32_t idesc_s = umma_idesc_bf16(TA_QT, TA_KC);
+            constexpr uint32_t idesc_o = umma_idesc_bf16(TA_QT, DH) | (1u << 16);  // B (V) MN-major
+            ta_wait(q_ready, 0, 2, 0);
+            tc_fence_after();
+            auto issue_s = [&](int t, int j) {
+                const int st = j % TA_STAGES;
+                ta_wait(kv_full + st, (j / TA_STAGES) & 1, 3, j);
+                ta_wait(s_empty + t, (j & 1) ^ 1, 4, j);
+                tc_fence_after();
+                const uint32_t k_addr = smem_u32(sm + C::ST_OFF + st * C::STAGE);
+                const uint32_t q_addr = smem_u32(sm + C::Q_OFF + t * C::Q_TILE);
+#pragma unroll
+                for (int hh = 0; hh < C::HALVES; ++hh) {
+                    const uint64_t qd = umma_desc_sw128(q_addr + hh * C::Q_HALF);
+                    const uint64_t kd = umma_desc_sw128(k_addr + hh * C::KV_HALF);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        umma_bf16(tmem + 256u + uint32_t(t * 128), qd + 2 * k, kd + 2 * k, idesc_s, (hh | k) != 0);
+                }
+                umma_commit(s_full + t);
+            };
+            auto issue_pv = [&](int t, int j) {
+                const int st = j % TA_STAGES;
+                ta_wait(p_full + t, j & 1, 5, j);
+                tc_fence_after();
+                const uint32_t v_addr = smem_u32(sm + C::ST_OFF + st * C::STAGE + C::K_BYTES);
+                const uint64_t pd = umma_desc_sw128(smem_u32(sm + C::P_OFF + t * C::P_TILE));
+#pragma unroll
+                for (int k = 0; k < TA_KC / 16; ++k)
+                    umma_bf16(tmem + uint32_t(t * 128), pd + 2 * k, umma_desc_sw128_mn(v_addr + k * 2048, C::KV_HALF),
+                              idesc_o, (j | k) != 0);
+                umma_commit(pv_done + t);
+            };
+            for (int t = 0; t < 2; ++t)
+                if (nch[t] > 0) issue_s(t, 0);
+            for (int j = 0; j < nchunks; ++j) {
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (j >= nch[t]) continue;
+                    issue_pv(t, j);
+                    if (j + 1 < nch[t]) issue_s(t, j + 1);
+                }
+                umma_commit(kv_empty + (j % TA_STAGES));  // both tiles' MMAs of chunk j read the stage
+            }
+        }
+    } else {  // ---- softmax warpgroups: tile t = (warp - 2) / 4, one query row per thread
+        const int t = (warp - 2) >> 2, sub = warp & 3, row = sub * 32 + lane;
+        const uint32_t lane_addr = tmem + (uint32_t(sub * 32) << 16);
+        const uint32_t o_col = uint32_t(t * 128), s_col = 256u + uint32_t(t * 128);
+        const int r = q0[t] + row;
+        {
+            const uint4* src = reinterpret_cast<const uint4*>(a.q + (size_t(r) * s.n_heads + head) * DH);
+#pragma unroll
+            for (int c = 0; c < DH / 8; ++c) {
+                const uint4 v = r < a.L ? src[c] : make_uint4(0, 0, 0, 0);
+                const int hh = c >> 3, cc = c & 7;
+                *reinterpret_cast<uint4*>(sm + C::Q_OFF + t * C::Q_TILE + hh * C::Q_HALF + row * 128 +
+                                          ((cc ^ (row & 7)) << 4)) = v;
+            }
+        }
+        fence_proxy_async_smem();
+        mbar_arrive(q_ready);
+        const int qpos = a.p0 + r, n_t = nch[t];
+        const float sl2 = rsqrtf(float(DH)) * 1.4426950408889634f;
+        float mref = -INFINITY, l = 0.f;
+        for (int j = 0; j < n_t; ++j) {
+            const int kbase = j * TA_KC;
+            ta_wait(s_full + t, j & 1, 6, j);
+            tc_fence_after();
+            uint32_t sv[2][32];
+            tmem_ld32(lane_addr + s_col, sv[0]);
+            tmem_ld32(lane_addr + s_col + 32u, sv[1]);
+            tc_fence_before();
+            mbar_arrive(s_empty + t);
+            float p[64];
+            float mx = -INFINITY;
+#pragma unroll
+            for (int k = 0; k < 64; ++k) {
+                const float v = __uint_as_float(sv[k >> 5][k & 31]);
+                p[k] = kbase + k <= qpos ? v * sl2 : -INFINITY;
+                mx = fmaxf(mx, p[k]);
+            }
+            if (j > 0) ta_wait(pv_done + t, (j - 1) & 1, 7, j);  // O_t stable, P_t free
+            tc_fence_after();
+            const bool grow = mx > mref + 8.f;
+            const float corr = (grow && mref != -INFINITY) ? exp2f(mref - mx) : 1.f;
+            if (__any_sync(0xffffffffu, corr != 1.f)) {
+#pragma unroll 1
+                for (int c = 0; c < DH / 32; ++c) {
+                    uint32_t o[32];
+                    tmem_ld32(lane_addr + o_col + uint32_t(c * 32), o);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * corr);
+                    tmem_st32(lane_addr + o_col + uint32_t(c * 32), o);
+                }
+            }
+            l *= corr;
+            if (grow) mref = mx;
+            uint8_t* prow = sm + C::P_OFF + t * C::P_TILE + row * 128;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+                float e[8];
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    e[i] = mref == -INFINITY ? 0.f : exp2f(p[c * 8 + i] - mref);
+                    l += e[i];
+                }
+                uint4 pk;
+                pk.x = pack_bf16x2(e[0], e[1]);
+                pk.y = pack_bf16x2(e[2], e[3]);
+                pk.z = pack_bf16x2(e[4], e[5]);
+                pk.w = pack_bf16x2(e[6], e[7]);
+                *reinterpret_cast<uint4*>(prow + ((c ^ (row & 7)) << 4)) = pk;
+            }
+            // keys past the CTA's last key in its last chunk: zero those V rows (0 x NaN of
+            // unwritten cache rows would reach O). Only the tile that alone processes the
+            // last chunk does it: with two full tiles, tile A's range ends a chunk earlier.
+            if (j == nchunks - 1 && kmax < kbase + TA_KC - 1 && (t == 1 || nch[1] < nchunks)) {
+                uint8_t* vb = sm + C::ST_OFF + (j % TA_STAGES) * C::STAGE + C::K_BYTES;
+                const int k0 = kmax + 1 - kbase, n16 = (TA_KC - k0) * 8 * C::HALVES;
+                for (int i = row; i < n16; i += 128) {
+                    const int hh = i / ((TA_KC - k0) * 8), rem = i % ((TA_KC - k0) * 8);
+                    *reinterpret_cast<uint4*>(vb + hh * C::KV_HALF + (k0 + rem / 8) * 128 + (rem % 8) * 16) =
+                        make_uint4(0, 0, 0, 0);
+                }
+            }
+            fence_proxy_async_smem();
+            tc_fence_before();
+            mbar_arrive(p_full + t);
+        }
+        if (n_t > 0) {
+            ta_wait(pv_done + t, (n_t - 1) & 1, 8, n_t);
+            tc_fence_after();
+            const float inv = 1.f / l;
+#pragma unroll 1
+            for (int c = 0; c < DH / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(lane_addr + o_col + uint32_t(c * 32), o);
+                if (r < a.L) {
+                    uint16_t* dst = a.attn + size_t(r) * s.d + head * DH + c * 32;
+#pragma unroll
+                    for (int i = 0; i < 32; i += 8) {
+                        uint4 pk;
+                        pk.x = pack_bf16x2(__uint_as_float(o[i]) * inv, __uint_as_float(o[i + 1]) * inv);
+                        pk.y = pack_bf16x2(__uint_as_float(o[i + 2]) * inv, __uint_as_float(o[i + 3]) * inv);
+                        pk.z = pack_bf16x2(__uint_as_float(o[i + 4]) * inv, __uint_as_float(o[i + 5]) * inv);
+                        pk.w = pack_bf16x2(__uint_as_float(o[i + 6]) * inv, __uint_as_float(o[i + 7]) * inv);
+                        *reinterpret_cast<uint4*>(dst + i) = pk;
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc(tmem, C::TMEM_COLS);
+    }
+}
+
 bool make_kvmap(CUtensorMap* m, const PrefillArgs& a);
 
 // MESH_PF_ATTN=mma selects the mma.sync kernel (kept as the A/B reference); default tcgen05.
@@ -978,12 +1236,36 @@ cudaError_t attn_tc_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
 }
 
 template <int DH>
+cudaError_t attn_tc2_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
+    static bool cfg[MAX_DEVICES] = {};
+    const int dev = cur_device();
+    if (!cfg[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(pf_attn_tc2<DH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Ta2Cfg<DH>::SMEM);
+        if (e != cudaSuccess) return e;
+        cfg[dev] = true;
+    }
+    CUtensorMap km;
+    if (!make_kvmap(&km, a)) return cudaErrorInvalidValue;
+    const int nqt = (a.L + TA_QT - 1) / TA_QT;
+    dim3 grid((nqt + 1) / 2, a.s.n_heads);
+    pf_attn_tc2<DH><<<grid, T2_THREADS, Ta2Cfg<DH>::SMEM, st>>>(a, km, layer);
+    return cudaGetLastError();
+}
+
+// MESH_PF_ATTN: "tc2" (default) two query tiles per CTA ping-ponged, "tc" one tile per CTA,
+// "mma" the mma.sync kernel. tc2 needs p0 == 0 whenever L > 128 (a fresh prefill; a resume
+// feeds one token), which is how the data plane issues prefills.
+template <int DH>
 cudaError_t attn_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
-    static const bool use_mma = [] {
+    static const int mode = [] {
         const char* e = getenv("MESH_PF_ATTN");
-        return e && std::string(e) == "mma";
+        if (e && std::string(e) == "mma") return 0;
+        if (e && std::string(e) == "tc") return 1;
+        return 2;
     }();
-    if (!use_mma) return attn_tc_launch<DH>(a, layer, st);
+    if (mode == 2 && (a.p0 == 0 || a.L <= TA_QT)) return attn_tc2_launch<DH>(a, layer, st);
+    if (mode >= 1) return attn_tc_launch<DH>(a, layer, st);
     static bool cfg[MAX_DEVICES] = {};
     const int dev = cur_device();
     if (!cfg[dev]) {

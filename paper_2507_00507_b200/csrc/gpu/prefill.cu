@@ -12,6 +12,7 @@
 #include "prefill.cuh"
 
 #include <string>
+#include <vector>
 #include <cstring>
 #include <cstdio>
 #include <chrono>
@@ -672,6 +673,19 @@ constexpr int TA_QT = 128, TA_KC = 64, TA_THREADS = 192, TA_STAGES = 3;
 // MESH_PF_ATTN_DEBUG: bounded mbarrier waits that record (block, thread, barrier, chunk) in
 // host-mapped memory on a timeout and give up (results are then garbage), to locate a hang.
 __device__ int* g_ta_dbg = nullptr;
+__device__ __forceinline__ float ex2_approx(float x) {  // MUFU.EX2 without the denormal range fix-up
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ unsigned long long* g_ta_trace = nullptr;  // MESH_PF_ATTN_TRACE: CTA (0, 0) event timeline
+__device__ __forceinline__ void ta_trace(int id, int j) {
+    // plain stores into device memory at [id][j] (no atomics, no host round trips)
+    if (!g_ta_trace || blockIdx.x != 0 || blockIdx.y != 0 || j >= 1024) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_ta_trace[id * 1024 + j] = t;
+}
 __device__ __forceinline__ void ta_wait(uint64_t* bar, uint32_t parity, int id, int j) {
     if (!g_ta_dbg) {
         mbar_wait(bar, parity);
@@ -934,7 +948,9 @@ __global__ void __launch_bounds__(TA_THREADS, 1)
 // into P_A, the tensor core computes S_B / PV_B, and vice versa.
 //   warp 0: TMA producer; warp 1: MMA issuer (+ TMEM owner);
 //   warps 2-5: softmax of tile A, warps 6-9: softmax of tile B.
-// TMEM (512 columns): O_A [0, dh), O_B [128, 128 + dh), S_A [256, 320), S_B [384, 448).
+// S is double-buffered per tile so the issuer runs S_t(j+1) ahead of PV_t(j): a
+// warpgroup's next scores are ready the moment it finishes P_t(j).
+// TMEM (512 columns): O_A [0, dh), O_B [128, 128 + dh), S_t buffer b at 256 + 128 t + 64 b.
 constexpr int T2_THREADS = 320;
 template <int DH>
 struct Ta2Cfg {
@@ -959,9 +975,9 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
     uint8_t* sm = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
     uint64_t* kv_full = reinterpret_cast<uint64_t*>(sm + C::BAR_OFF);
     uint64_t* kv_empty = kv_full + TA_STAGES;
-    uint64_t* s_full = kv_empty + TA_STAGES;  // [tile]
-    uint64_t* s_empty = s_full + 2;           // [tile]
-    uint64_t* p_full = s_empty + 2;           // [tile]
+    uint64_t* s_full = kv_empty + TA_STAGES;  // [tile][buffer]
+    uint64_t* s_empty = s_full + 4;           // [tile][buffer]
+    uint64_t* p_full = s_empty + 4;           // [tile]
     uint64_t* pv_done = p_full + 2;           // [tile]
     uint64_t* q_ready = pv_done + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_ready + 1);
@@ -985,9 +1001,11 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
             mbar_init(kv_full + i, 1);
             mbar_init(kv_empty + i, 1);
         }
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t < 4; ++t) {
             mbar_init(s_full + t, 1);
             mbar_init(s_empty + t, 128);
+        }
+        for (int t = 0; t < 2; ++t) {
             mbar_init(p_full + t, 128);
             mbar_init(pv_done + t, 1);
         }
@@ -1009,6 +1027,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
                 const int st = j % TA_STAGES;
                 ta_wait(kv_empty + st, ((j / TA_STAGES) & 1) ^ 1, 1, j);
                 uint8_t* kb = sm + C::ST_OFF + st * C::STAGE;
+                ta_trace(10, j);
                 mbar_arrive_expect_tx(kv_full + st, C::STAGE);
 #pragma unroll
                 for (int bi = 0; bi < TA_KC / KV_BLOCK_TOKENS; ++bi) {
@@ -1024,7 +1043,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ---- MMA issuer: S_A(j), S_B(j), PV_A(j), S_A(j+1), PV_B(j), S_B(j+1), ...
+        if (lane == 0) {  // ---- MMA issuer: S_A(0), S_B(0), then per chunk S_A(j+1), PV_A(j), S_B(j+1), PV_B(j)
             constexpr uint32_t idesc_s = umma_idesc_bf16(TA_QT, TA_KC);
             constexpr uint32_t idesc_o = umma_idesc_bf16(TA_QT, DH) | (1u << 16);  // B (V) MN-major
             ta_wait(q_ready, 0, 2, 0);
@@ -1032,7 +1051,7 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
             auto issue_s = [&](int t, int j) {
                 const int st = j % TA_STAGES;
                 ta_wait(kv_full + st, (j / TA_STAGES) & 1, 3, j);
-                ta_wait(s_empty + t, (j & 1) ^ 1, 4, j);
+                ta_wait(s_empty + 2 * t + (j & 1), ((j >> 1) & 1) ^ 1, 4, j);
                 tc_fence_after();
                 const uint32_t k_addr = smem_u32(sm + C::ST_OFF + st * C::STAGE);
                 const uint32_t q_addr = smem_u32(sm + C::Q_OFF + t * C::Q_TILE);
@@ -1042,13 +1061,16 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
                     const uint64_t kd = umma_desc_sw128(k_addr + hh * C::KV_HALF);
 #pragma unroll
                     for (int k = 0; k < 4; ++k)
-                        umma_bf16(tmem + 256u + uint32_t(t * 128), qd + 2 * k, kd + 2 * k, idesc_s, (hh | k) != 0);
+                        umma_bf16(tmem + 256u + uint32_t(t * 128 + (j & 1) * 64), qd + 2 * k, kd + 2 * k, idesc_s,
+                                  (hh | k) != 0);
                 }
-                umma_commit(s_full + t);
+                umma_commit(s_full + 2 * t + (j & 1));
+                ta_trace(30 + t, j);
             };
             auto issue_pv = [&](int t, int j) {
                 const int st = j % TA_STAGES;
                 ta_wait(p_full + t, j & 1, 5, j);
+                ta_trace(20 + t, j);
                 tc_fence_after();
                 const uint32_t v_addr = smem_u32(sm + C::ST_OFF + st * C::STAGE + C::K_BYTES);
                 const uint64_t pd = umma_desc_sw128(smem_u32(sm + C::P_OFF + t * C::P_TILE));
@@ -1064,8 +1086,8 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
 #pragma unroll
                 for (int t = 0; t < 2; ++t) {
                     if (j >= nch[t]) continue;
-                    issue_pv(t, j);
                     if (j + 1 < nch[t]) issue_s(t, j + 1);
+                    issue_pv(t, j);
                 }
                 umma_commit(kv_empty + (j % TA_STAGES));  // both tiles' MMAs of chunk j read the stage
             }
@@ -1092,22 +1114,33 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
         float mref = -INFINITY, l = 0.f;
         for (int j = 0; j < n_t; ++j) {
             const int kbase = j * TA_KC;
-            ta_wait(s_full + t, j & 1, 6, j);
+            ta_wait(s_full + 2 * t + (j & 1), (j >> 1) & 1, 6, j);
+            if (lane == 0 && sub == 2) ta_trace(40 + t, j);
             tc_fence_after();
             uint32_t sv[2][32];
-            tmem_ld32(lane_addr + s_col, sv[0]);
-            tmem_ld32(lane_addr + s_col + 32u, sv[1]);
+            tmem_ld32(lane_addr + s_col + uint32_t((j & 1) * 64), sv[0]);
+            tmem_ld32(lane_addr + s_col + uint32_t((j & 1) * 64) + 32u, sv[1]);
             tc_fence_before();
-            mbar_arrive(s_empty + t);
+            mbar_arrive(s_empty + 2 * t + (j & 1));
+            // raw scores; the causal mask only in chunks that cross some row's diagonal
             float p[64];
             float mx = -INFINITY;
+            if (__any_sync(0xffffffffu, kbase + TA_KC - 1 > qpos)) {
 #pragma unroll
-            for (int k = 0; k < 64; ++k) {
-                const float v = __uint_as_float(sv[k >> 5][k & 31]);
-                p[k] = kbase + k <= qpos ? v * sl2 : -INFINITY;
-                mx = fmaxf(mx, p[k]);
+                for (int k = 0; k < 64; ++k) {
+                    p[k] = kbase + k <= qpos ? __uint_as_float(sv[k >> 5][k & 31]) : -INFINITY;
+                    mx = fmaxf(mx, p[k]);
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < 64; ++k) {
+                    p[k] = __uint_as_float(sv[k >> 5][k & 31]);
+                    mx = fmaxf(mx, p[k]);
+                }
             }
+            mx *= sl2;  // log2 domain
             if (j > 0) ta_wait(pv_done + t, (j - 1) & 1, 7, j);  // O_t stable, P_t free
+            if (lane == 0 && sub == 2) ta_trace(60 + t, j);
             tc_fence_after();
             const bool grow = mx > mref + 8.f;
             const float corr = (grow && mref != -INFINITY) ? exp2f(mref - mx) : 1.f;
@@ -1123,13 +1156,15 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
             }
             l *= corr;
             if (grow) mref = mx;
+            if (lane == 0 && sub == 2) ta_trace(70 + t, j);
             uint8_t* prow = sm + C::P_OFF + t * C::P_TILE + row * 128;
+            const float moff = mref == -INFINITY ? 0.f : -mref;  // fully masked rows: ex2(-inf) = 0
 #pragma unroll
             for (int c = 0; c < 8; ++c) {
                 float e[8];
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {
-                    e[i] = mref == -INFINITY ? 0.f : exp2f(p[c * 8 + i] - mref);
+                    e[i] = ex2_approx(fmaf(p[c * 8 + i], sl2, moff));
                     l += e[i];
                 }
                 uint4 pk;
@@ -1151,8 +1186,10 @@ __global__ void __launch_bounds__(T2_THREADS, 1)
                         make_uint4(0, 0, 0, 0);
                 }
             }
+            if (lane == 0 && sub == 2) ta_trace(80 + t, j);
             fence_proxy_async_smem();
             tc_fence_before();
+            if (lane == 0 && sub == 2) ta_trace(50 + t, j);
             mbar_arrive(p_full + t);
         }
         if (n_t > 0) {
@@ -1247,9 +1284,31 @@ cudaError_t attn_tc2_launch(const PrefillArgs& a, int layer, cudaStream_t st) {
     }
     CUtensorMap km;
     if (!make_kvmap(&km, a)) return cudaErrorInvalidValue;
+    static int trace_state = getenv("MESH_PF_ATTN_TRACE") ? 1 : 0;  // 1: trace the next launch
+    unsigned long long* tr_dev = nullptr;
+    if (trace_state == 1) {
+        if (cudaMalloc((void**)&tr_dev, 8 * 96 * 1024) != cudaSuccess) return cudaErrorMemoryAllocation;
+        cudaMemsetAsync(tr_dev, 0, 8 * 96 * 1024, st);
+        cudaMemcpyToSymbolAsync(g_ta_trace, &tr_dev, sizeof(tr_dev), 0, cudaMemcpyHostToDevice, st);
+    }
     const int nqt = (a.L + TA_QT - 1) / TA_QT;
     dim3 grid((nqt + 1) / 2, a.s.n_heads);
     pf_attn_tc2<DH><<<grid, T2_THREADS, Ta2Cfg<DH>::SMEM, st>>>(a, km, layer);
+    if (trace_state == 1) {  // dump CTA (0, 0)'s timeline of this launch, then stop tracing
+        trace_state = 2;
+        std::vector<unsigned long long> h(96 * 1024);
+        cudaStreamSynchronize(st);
+        cudaMemcpy(h.data(), tr_dev, 8 * 96 * 1024, cudaMemcpyDeviceToHost);
+        unsigned long long* null_ptr = nullptr;
+        cudaMemcpyToSymbol(g_ta_trace, &null_ptr, sizeof(null_ptr));
+        cudaFree(tr_dev);
+        if (FILE* f = fopen(getenv("MESH_PF_ATTN_TRACE"), "w")) {
+            for (int id = 0; id < 96; ++id)
+                for (int j = 0; j < 1024; ++j)
+                    if (h[id * 1024 + j]) fprintf(f, "%llu %d %d\n", h[id * 1024 + j], id, j);
+            fclose(f);
+        }
+    }
     return cudaGetLastError();
 }
 

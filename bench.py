@@ -279,7 +279,10 @@ class Colocated:
         import random
 
         from paper_2507_00507_b200.gpu import SHAPES, MeshGpu
-        self.g = MeshGpu(device, kv_pool_bytes=KV_POOL, prompt_seed=seed, lanes=LANES)
+        # the whole KV arena backed at open: no VMM driver call (each drains the device) while serving
+        os.environ.setdefault("MESH_GPU_KV_PREALLOC_GB", str(KV_POOL >> 30))
+        self.g = MeshGpu(device, kv_pool_bytes=KV_POOL, prompt_seed=seed, lanes=LANES,
+                         kv_granule_bytes=KV_GRANULE_MB << 20)
         self.shapes = [SHAPES[m] for m in MODELS]
         self.rng = random.Random(seed)
         self.lengths = load_lengths()
@@ -398,8 +401,9 @@ class Colocated:
                     self.retire(q[i].popleft())
                     progressed = True
             if not progressed and issued < steps:
-                i = min((j for j in range(len(q)) if q[j]), key=lambda j: q[j][0][0])
-                self.retire(q[i].popleft())
+                # wait for ANY lane's head step (blocking on one ticket would let the other
+                # lanes run dry behind a long prefill)
+                time.sleep(5e-5)
         for i in range(len(q)):
             while q[i]:
                 self.retire(q[i].popleft())
@@ -432,6 +436,7 @@ class Colocated:
             pm["launches"] += 1
         else:
             self.prefill_steps += 1
+            self.prefill_ms += st["last_step_ms"]
         for r in reqs:
             deadline = r["arrival"] + max(2.0, r["I"] / 512.0) + 0.25 * r["gen"]
             if emit > deadline + 1e-9:
@@ -447,6 +452,7 @@ class Colocated:
         self.tokens_ok = self.tokens_all = self.completed = self.violations = 0
         self.decode_bytes = self.decode_kernel_ms = 0.0
         self.decode_steps = self.prefill_steps = 0
+        self.prefill_ms = 0.0
         self.per_model = {}
         self.lane_busy = {}  # instance -> [sum of its steps' device time (ms), steps]
         self.kv_grows = self.kv_shrinks = 0
@@ -769,6 +775,33 @@ def run_e2e(device: int, d: Dist, scales):
             "api": "llmmesh.h llm_experiment_run + llm_experiment_attach_gpu, runtime.clock = wall"}
 
 
+class HostProfile:
+    """MESH_BENCH_HOSTPROF=1: host seconds spent in each MeshGpu call of the timed loop
+    (stderr), to tell host-issue gaps from device time."""
+
+    def __init__(self, node):
+        self.acc = {}
+        g = node.g
+        for name in ("step_async", "wait", "done", "stats", "kv_resize", "request_free"):
+            f = getattr(g, name)
+
+            def wrap(*a, _f=f, _n=name, **k):
+                t0 = time.perf_counter()
+                try:
+                    return _f(*a, **k)
+                finally:
+                    e = self.acc.setdefault(_n, [0.0, 0])
+                    e[0] += time.perf_counter() - t0
+                    e[1] += 1
+            setattr(g, name, wrap)
+
+    def report(self, wall):
+        tot = sum(v[0] for v in self.acc.values())
+        print(json.dumps({"host_wall_s": round(wall, 3), "in_calls_s": round(tot, 3),
+                          "calls": {k: [round(v[0], 4), v[1], round(1e6 * v[0] / max(1, v[1]), 1)]
+                                    for k, v in sorted(self.acc.items())}}), file=sys.stderr)
+
+
 def run_ours(args, d: Dist):
     device = d.local
     hbm, peak_kind = peaks()
@@ -789,7 +822,12 @@ def run_ours(args, d: Dist):
         node.g.timer_mark(0)
         node.mark0 = node.clock
         profiler_region(True)
+        hp = HostProfile(node) if os.environ.get("MESH_BENCH_HOSTPROF") else None
+        w0 = time.perf_counter()
         launches = node.run(args.steps)
+        host_wall = time.perf_counter() - w0
+        if hp:
+            hp.report(host_wall)
         profiler_region(False)
         node.g.timer_mark(1)
         node.g.sync()
@@ -856,6 +894,7 @@ def run_ours(args, d: Dist):
                    "kv_blocks_moved": g_stats["blocks_moved"],
                    "lane_busy_frac": {str(i): round(v[0] / (1e3 * dev_s), 3) for i, v in sorted(node.lane_busy.items())},
                    "lane_steps": {str(i): v[1] for i, v in sorted(node.lane_busy.items())},
+                   "prefill_step_ms_avg": round(node.prefill_ms / max(1, node.prefill_steps), 2),
                    "parallelism": f"{d.ws} independent co-located nodes"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                      "frac": achieved / hbm if hbm else None, "traffic": traffic,

@@ -56,9 +56,10 @@ typedef struct mesh_model_shape {
 typedef struct mesh_gpu_cfg {
     int32_t device;         /* CUDA ordinal */
     int32_t sm_quota;       /* CTAs of the persistent decode kernel; 0 = all SMs */
-    int64_t kv_pool_bytes;  /* physical HBM the KV pool may map (VMM granules) */
+    int64_t kv_pool_bytes;  /* physical HBM of the KV arena (granule slots, backed on first use or at
+                               open with MESH_GPU_KV_PREALLOC_GB) */
     uint64_t prompt_seed;   /* synthetic prompt ids: hash(seed, request, position) */
-    int64_t kv_granule_bytes; /* physical chunk per cuMemCreate/cuMemMap, multiple of 2 MiB; 0 = 32 MiB */
+    int64_t kv_granule_bytes; /* arena slot (one cuMemCreate/cuMemMap), multiple of 2 MiB; 0 = 32 MiB */
     int32_t lanes;          /* concurrent execution lanes (stream + scratch + an even share of the SM
                                quota); instances bind to the lane with the fewest weight bytes and
                                co-located instances on different lanes step concurrently.
@@ -77,7 +78,7 @@ typedef struct mesh_step_plan {
 } mesh_step_plan;
 
 typedef struct mesh_gpu_stats {
-    int64_t kv_mapped_bytes;      /* physical bytes currently mapped for KV (all instances) */
+    int64_t kv_mapped_bytes;      /* KV arena bytes assigned to instances (capacity + lazy slack) */
     int64_t kv_pool_bytes;        /* configured physical limit */
     int64_t blocks_moved;         /* compaction block copies */
     int64_t bytes_moved;          /* compaction bytes (read + write counted once) */
@@ -90,7 +91,7 @@ typedef struct mesh_gpu_stats {
     int64_t kv_granule_bytes;     /* physical chunk size of the KV pool */
     int64_t vmm_calls;            /* cuMemMap / cuMemUnmap / cuMemSetAccess calls */
     double vmm_ms;                /* host time inside them */
-    int64_t kv_reclaims;          /* lazy-shrink slack reclaims (each drains the streams once) */
+    int64_t kv_reclaims;          /* lazy-shrink slack reclaims (stream-ordered, no host wait) */
     double last_step_end_ms;      /* end of the last waited step on the device timeline of timer
                                      mark 0 (all lanes), -1 before the mark */
     int64_t weight_cache_hits;    /* instance creates that shared a live or cached weight set of the
@@ -114,12 +115,17 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
                                      uint64_t weight_seed);
 mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id);
 
-/* Physically applies a KV ScaleOp at issue time: grow maps
- * granules (one access grant per grow), shrink compacts live blocks below the
- * new high-water mark with a batched block-copy kernel. Shrinks release lazily:
- * the tail granules stay mapped (no host/device sync) until another grow would
- * exceed the pool limit, which drains the streams once and unmaps every
- * instance's slack. `from` must equal the instance's current target. */
+/* Physically applies a KV ScaleOp at issue time. Every instance's
+ * KV lives in one device-wide arena of granule slots; a grow assigns extents of
+ * free slots (>= 32 whole blocks each) to the instance, a shrink compacts live
+ * blocks below the new high-water mark with a batched block-copy kernel and
+ * keeps the extents above it (lazy) until another instance's grow finds no free
+ * run and takes them back. Neither path calls the VMM driver or waits on the
+ * host: a reassigned slot's new owner waits on an event of the previous owner's
+ * queued work. Only a slot's first use maps memory (cuMemMap drains the whole
+ * device), so MESH_GPU_KV_PREALLOC_GB backs the arena at open. Block ids
+ * (request_info) are the instance's logical ids; the device sees arena ids.
+ * `from` must equal the instance's current target. */
 mesh_status mesh_gpu_kv_resize(mesh_gpu* g, int64_t instance_id, int64_t from_bytes, int64_t to_bytes);
 
 mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan* plan, int64_t* ticket);

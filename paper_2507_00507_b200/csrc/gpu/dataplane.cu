@@ -190,18 +190,17 @@ struct Granule {
     CUmemGenericAllocationHandle h;
 };
 
+// Physical KV memory: granules created with cuMemCreate, mapped once into the
+// KV arena (below) and never unmapped on the serving path.
 struct PhysPool {
     int device = 0;
     size_t gran = 2u << 20;
     long long limit = 0;
-    long long mapped = 0;  // granules in use x gran
-    std::vector<CUmemGenericAllocationHandle> free_list;
+    long long mapped = 0;  // bytes of arena slots assigned to instances (capacity + lazy slack)
+    std::vector<CUmemGenericAllocationHandle> free_list;  // created, not mapped
     std::vector<CUmemGenericAllocationHandle> all;
 
     CUmemGenericAllocationHandle take() {
-        if (mapped + (long long)gran > limit)
-            throw MeshError(MESH_ERR_NOMEM, "KV pool exhausted (limit " + std::to_string(limit) + " bytes)");
-        mapped += gran;
         if (!free_list.empty()) {
             auto h = free_list.back();
             free_list.pop_back();
@@ -213,17 +212,11 @@ struct PhysPool {
         prop.location.id = device;
         CUmemGenericAllocationHandle h;
         CUresult r = drv().create(&h, gran, &prop, 0);
-        if (r != CUDA_SUCCESS) {
-            mapped -= gran;
-            throw MeshError(MESH_ERR_NOMEM, "cuMemCreate failed: " + std::to_string(int(r)));
-        }
+        if (r != CUDA_SUCCESS) throw MeshError(MESH_ERR_NOMEM, "cuMemCreate failed: " + std::to_string(int(r)));
         all.push_back(h);
         return h;
     }
-    void give(CUmemGenericAllocationHandle h) {
-        mapped -= gran;
-        free_list.push_back(h);
-    }
+    void give(CUmemGenericAllocationHandle h) { free_list.push_back(h); }
 };
 
 struct ReqState {
@@ -340,10 +333,16 @@ struct Instance {
     uint64_t shape_key = 0;
     uint8_t* wmem = nullptr;
     Weights w{};
-    // KV region
-    CUdeviceptr va = 0;
-    size_t va_size = 0;
-    std::vector<CUmemGenericAllocationHandle> granules;  // mapped, in VA order
+    // KV region: extents of the device's KV arena. Block ids the control plane and
+    // the policy see are logical (0 .. cap-1, the oracle's ids); the device sees
+    // physical ids (block p at arena base + p * block_bytes), translated per extent.
+    struct Extent {
+        int s0, k;  // arena slots [s0, s0 + k)
+        int p0, L;  // physical blocks [p0, p0 + L): the whole blocks inside those slots
+    };
+    std::vector<Extent> ext;      // in logical order
+    std::vector<int> ext_first;   // logical id of each extent's first block
+    int ext_slots = 1;            // slots per extent (>= 32 blocks per extent)
     long long block_bytes = 0;
     long long target = 0;  // accounted KV bytes (control plane target)
     int cap_blocks = 0;
@@ -430,6 +429,7 @@ struct mesh_gpu {
     bool check = false;              // MESH_GPU_CHECK: synchronous per-step validation (debug)
     bool poison = false;             // MESH_GPU_POISON: NaN-fill newly mapped KV granules (debug)
     bool prefill_quota = false;      // MESH_PREFILL_QUOTA: cap prefill GEMM grids at the lane quota
+    int prefill_min_ctas = 0;        // MESH_PREFILL_CTAS=n: cap at max(lane quota, n) instead
     PhysPool pool;
     std::map<int64_t, std::unique_ptr<Instance>> insts;
     std::vector<Lane> lanes;         // concurrent execution lanes (>= 1)
@@ -469,20 +469,28 @@ struct mesh_gpu {
         uint64_t tick;      // last release, for LRU eviction of idle sets
     };
     std::map<uint64_t, WeightSet> wsets;  // by shape key
-    // Per-instance buffers of unloaded instances, recycled by the next create:
-    // the KV VA range WITH its mapped granules (an instance start then maps
-    // nothing until it outgrows them; no cuMemMap / cuMemUnmap, each of which
-    // costs host time and a TLB shoot-down, on the keep-alive churn path), the
-    // block table and the last-token array. Every range has the same size
-    // (va_size), so any range serves any model.
+    // Per-instance buffers of unloaded instances (block table, last tokens),
+    // recycled by the next create: no cudaMalloc / cudaFree on the churn path.
     struct InstBufs {
-        CUdeviceptr va;
         int* d_block_table;  // [MAX_SLOTS][DEC_BT_MAX]
         int* d_last_tok;
-        std::vector<CUmemGenericAllocationHandle> granules;  // mapped at va, in order
     };
     std::vector<InstBufs> ibufs;  // free per-instance buffers
-    size_t va_size = 0;           // KV VA range per instance: the pool limit + the largest tail slack
+    // The KV arena: ONE virtual range for every instance's KV, carved into
+    // granule-sized slots. A slot is backed (cuMemCreate + cuMemMap) the first
+    // time it is needed, or at open (MESH_GPU_KV_PREALLOC_GB), and then stays
+    // mapped: growing, shrinking, reclaiming and recycling KV between instances
+    // is host bookkeeping plus a stream wait on the previous owner's last work.
+    // cuMemMap / cuMemUnmap wait for the whole device to drain, so none of them
+    // runs on the serving path once the arena is backed.
+    struct KvArena {
+        CUdeviceptr base = 0;
+        int nslots = 0;
+        std::vector<CUmemGenericAllocationHandle> h;  // 0: not backed yet
+        std::vector<int64_t> owner;                    // -1: free
+        std::vector<cudaEvent_t> ev;                   // free slot: after its last owner's queued work
+        size_t bytes(size_t gran) const { return size_t(nslots) * gran; }
+    } arena;
     size_t wcache_cap = size_t(32) << 30;  // MESH_GPU_WCACHE_GB: bytes of idle weight sets kept
     uint64_t wtick = 0;
     // devices that may map this device's KV (peer access over NVLink): every KV
@@ -743,12 +751,6 @@ int blocks_for_target(const Instance& in, long long target) {
     return int(blocks) + DEC_MAXB;  // one partial tail block per resident request
 }
 
-size_t granules_for(const mesh_gpu* g, long long bytes) {
-    return size_t((bytes + (long long)g->pool.gran - 1) / (long long)g->pool.gran);
-}
-
-// Unmaps an instance's granules from the top of its VA range down to `keep`.
-// The caller guarantees no queued work touches the tail (streams drained).
 struct VmmTimer {  // host time of VMM driver calls -> stats
     mesh_gpu* g;
     std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
@@ -778,65 +780,53 @@ void evict_weights(mesh_gpu* g, size_t cap) {
     }
 }
 
-void unmap_tail(mesh_gpu* g, Instance& in, size_t keep) {
-    Driver& d = drv();
-    VmmTimer vt(g);
-    while (in.granules.size() > keep) {
-        size_t off = (in.granules.size() - 1) * g->pool.gran;
-        CU(d.unmap(in.va + off, g->pool.gran), "cuMemUnmap");
-        g->st.vmm_calls++;
-        g->st.vmm_unmaps++;
-        g->pool.give(in.granules.back());
-        in.granules.pop_back();
-    }
-}
+// ---- the KV arena
+int kv_capacity(const Instance& in) { return in.ext.empty() ? 0 : in.ext_first.back() + in.ext.back().L; }
 
-// Shrinks are lazy: a shrink compacts the live blocks below the new capacity
-// but leaves the tail granules mapped, so a later grow of the same instance
-// costs nothing and a shrink never stalls the host on the device. Granules go
-// back to the pool only when another grow needs them: one drain of the streams,
-// then every instance's slack above its capacity is unmapped.
-void unmap_idle(mesh_gpu* g, mesh_gpu::InstBufs& b, size_t keep) {
-    Driver& d = drv();
-    VmmTimer vt(g);
-    while (b.granules.size() > keep) {
-        CU(d.unmap(b.va + (b.granules.size() - 1) * g->pool.gran, g->pool.gran), "cuMemUnmap");
-        g->st.vmm_calls++;
-        g->st.vmm_unmaps++;
-        g->pool.give(b.granules.back());
-        b.granules.pop_back();
-    }
+// physical id (arena-relative) of the instance's logical block b
+int phys_of(const Instance& in, int b) {
+    const size_t i = size_t(std::upper_bound(in.ext_first.begin(), in.ext_first.end(), b) - in.ext_first.begin()) - 1;
+    return in.ext[i].p0 + (b - in.ext_first[i]);
 }
-
-void reclaim_slack(mesh_gpu* g, long long need) {
-    // granules parked in recycled ranges first: nothing runs on them, no drain
-    for (auto& b : g->ibufs) {
-        if (g->pool.mapped + need <= g->pool.limit) return;
-        unmap_idle(g, b, 0);
-    }
-    if (g->pool.mapped + need <= g->pool.limit) return;
-    g->st.kv_reclaims++;
-    sync_all(g);
-    for (auto& [id, ip] : g->insts) unmap_tail(g, *ip, granules_for(g, (long long)ip->cap_blocks * ip->block_bytes));
+std::vector<int> phys_list(const Instance& in, const std::vector<int>& ids) {
+    std::vector<int> p(ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) p[i] = phys_of(in, ids[i]);
+    return p;
 }
+uint8_t* arena_ptr(const mesh_gpu* g) { return reinterpret_cast<uint8_t*>(g->arena.base); }
 
-// Grow-only: maps granules until `bytes` of the instance's VA range are backed.
-void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
+// Backs slots [s0, s0 + n) that have no physical memory yet: the only cuMemMap
+// calls (first use of a slot; the device drains once per call batch). Access is
+// granted to this device and every NVLink peer (a migration's copy kernel runs on
+// the destination GPU and loads the source's blocks directly).
+void back_slots(mesh_gpu* g, int s0, int n) {
     const size_t gran = g->pool.gran;
-    const size_t want = granules_for(g, (long long)bytes), first = in.granules.size();
-    if (want <= first) return;
-    if (want * gran > in.va_size) throw MeshError(MESH_ERR_NOMEM, "instance KV VA range exhausted");
-    if (g->pool.mapped + (long long)((want - first) * gran) > g->pool.limit)
-        reclaim_slack(g, (long long)((want - first) * gran));
     Driver& d = drv();
     VmmTimer vt(g);
-    while (in.granules.size() < want) {
-        const size_t off = in.granules.size() * gran;
+    std::vector<CUmemAccessDesc> acc(1 + g->peers.size());
+    for (size_t i = 0; i < acc.size(); ++i) {
+        acc[i] = {};
+        acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+        acc[i].location.id = i == 0 ? g->cfg.device : g->peers[i - 1];
+        acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    }
+    int run = -1;  // first slot of the current run of newly mapped slots
+    auto grant = [&](int end) {
+        if (run < 0) return;
+        CU(d.set_access(g->arena.base + size_t(run) * gran, size_t(end - run) * gran, acc.data(), acc.size()),
+           "cuMemSetAccess");
+        g->st.vmm_calls++;
+        run = -1;
+    };
+    for (int sl = s0; sl < s0 + n; ++sl) {
+        if (g->arena.h[size_t(sl)]) {
+            grant(sl);
+            continue;
+        }
         CUmemGenericAllocationHandle h;
         try {
             h = g->pool.take();
         } catch (const MeshError&) {
-            if (g->pool.mapped + (long long)gran > g->pool.limit) throw;  // the pool's limit, not HBM
             // HBM is short: idle weight sets go first (stream-ordered frees, then
             // hand the freed memory back from the allocator's pool), then retry
             evict_weights(g, 0);
@@ -845,41 +835,126 @@ void map_to(mesh_gpu* g, Instance& in, size_t bytes) {
             if (cudaDeviceGetDefaultMemPool(&mp, g->cfg.device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
             h = g->pool.take();
         }
-        CUresult r = d.map(in.va + off, gran, 0, h, 0);
+        CUresult r = d.map(g->arena.base + size_t(sl) * gran, gran, 0, h, 0);
         if (r != CUDA_SUCCESS) {
             g->pool.give(h);
+            grant(sl);
             throw MeshError(MESH_ERR_RUNTIME, "cuMemMap failed: " + std::to_string(int(r)));
         }
-        in.granules.push_back(h);
+        g->arena.h[size_t(sl)] = h;
         g->st.vmm_calls++;
+        if (run < 0) run = sl;
     }
-    // one access grant for the whole newly mapped range: this device, and every
-    // peer that can reach it over NVLink (a migration's copy kernel runs on the
-    // destination GPU and loads these blocks directly)
-    std::vector<CUmemAccessDesc> acc(1 + g->peers.size());
-    for (size_t i = 0; i < acc.size(); ++i) {
-        acc[i] = {};
-        acc[i].location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-        acc[i].location.id = i == 0 ? g->cfg.device : g->peers[i - 1];
-        acc[i].flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+    grant(s0 + n);
+}
+
+// Returns the instance's last extent to the arena. Its slots stay mapped; the
+// next owner's streams wait for `ev` (the owner's queued work at release), so no
+// host wait. ev == nullptr: the owner's work is known to be finished.
+void release_extent(mesh_gpu* g, Instance& in, cudaStream_t owner_stream) {
+    const Instance::Extent e = in.ext.back();
+    for (int sl = e.s0; sl < e.s0 + e.k; ++sl) {
+        g->arena.owner[size_t(sl)] = -1;
+        if (owner_stream) g->arena.ev[size_t(sl)] = record_new_event(owner_stream);
     }
-    CU(d.set_access(in.va + first * gran, (want - first) * gran, acc.data(), acc.size()), "cuMemSetAccess");
-    g->st.vmm_calls++;
-    // debug (MESH_GPU_POISON): recycled KV memory may hold any bit pattern; fill
-    // new granules with bf16 NaN so reads of unwritten KV cannot go unnoticed
-    if (g->poison)
-        CK(cudaMemsetAsync(reinterpret_cast<void*>(in.va + first * gran), 0xff, (want - first) * gran,
-                           stream_of(g, in)));
+    g->pool.mapped -= (long long)e.k * (long long)g->pool.gran;
+    in.ext.pop_back();
+    in.ext_first.pop_back();
+}
+
+// Shrinks are lazy: a shrink compacts the live blocks below the new capacity but
+// keeps the extents above it, so a later grow of the same instance costs nothing.
+// Another instance's grow that finds no free run takes them back here.
+bool reclaim_slack(mesh_gpu* g, const Instance* growing) {
+    bool any = false;
+    for (auto& [id, ip] : g->insts) {
+        Instance& in = *ip;
+        if (&in == growing) continue;  // its capacity is being raised right now
+        while (!in.ext.empty() && in.ext_first.back() >= in.cap_blocks) {
+            release_extent(g, in, stream_of(g, in));
+            any = true;
+        }
+    }
+    if (any) g->st.kv_reclaims++;
+    return any;
+}
+
+int find_run(const mesh_gpu* g, int k) {
+    int n = 0;
+    for (int sl = 0; sl < g->arena.nslots; ++sl) {
+        n = g->arena.owner[size_t(sl)] < 0 ? n + 1 : 0;
+        if (n == k) return sl - k + 1;
+    }
+    return -1;
+}
+
+// Grows the instance's extents until they hold `blocks` logical blocks.
+void assign_to(mesh_gpu* g, Instance& in, int blocks) {
+    const size_t gran = g->pool.gran;
+    const long long bb = in.block_bytes;
+    while (kv_capacity(in) < blocks) {
+        const int k = in.ext_slots;
+        int s0 = find_run(g, k);
+        if (s0 < 0 && reclaim_slack(g, &in)) s0 = find_run(g, k);
+        if (s0 < 0)
+            throw MeshError(MESH_ERR_NOMEM, "KV pool exhausted (limit " + std::to_string(g->pool.limit) + " bytes)");
+        back_slots(g, s0, k);
+        cudaStream_t st = stream_of(g, in);
+        for (int sl = s0; sl < s0 + k; ++sl) {
+            g->arena.owner[size_t(sl)] = in.id;
+            cudaEvent_t& ev = g->arena.ev[size_t(sl)];
+            if (ev) {  // the previous owner's queued work on these slots comes first
+                CK(cudaStreamWaitEvent(st, ev, 0));
+                CK(cudaStreamWaitEvent(g->side_in, ev, 0));
+                cudaEventDestroy(ev);
+                ev = nullptr;
+            }
+        }
+        g->pool.mapped += (long long)k * (long long)gran;
+        const long long lo = (long long)s0 * (long long)gran, hi = lo + (long long)k * (long long)gran;
+        Instance::Extent e{s0, k, int((lo + bb - 1) / bb), 0};
+        e.L = int(hi / bb) - e.p0;
+        in.ext_first.push_back(kv_capacity(in));
+        in.ext.push_back(e);
+        // debug (MESH_GPU_POISON): recycled KV memory may hold any bit pattern; fill
+        // newly assigned slots with bf16 NaN so reads of unwritten KV cannot go unnoticed
+        if (g->poison) CK(cudaMemsetAsync(arena_ptr(g) + lo, 0xff, size_t(hi - lo), st));
+    }
+}
+
+// Gives the physical memory of every backed, unassigned slot back to the driver
+// (weights need HBM). cuMemUnmap drains the device: not a serving-path call.
+void release_free_slots(mesh_gpu* g) {
+    Driver& d = drv();
+    VmmTimer vt(g);
+    sync_all(g);
+    for (int sl = 0; sl < g->arena.nslots; ++sl) {
+        if (g->arena.owner[size_t(sl)] >= 0 || !g->arena.h[size_t(sl)]) continue;
+        if (g->arena.ev[size_t(sl)]) {
+            cudaEventDestroy(g->arena.ev[size_t(sl)]);
+            g->arena.ev[size_t(sl)] = nullptr;
+        }
+        CU(d.unmap(g->arena.base + size_t(sl) * g->pool.gran, g->pool.gran), "cuMemUnmap");
+        g->st.vmm_calls++;
+        g->st.vmm_unmaps++;
+        g->pool.give(g->arena.h[size_t(sl)]);
+        g->arena.h[size_t(sl)] = 0;
+    }
+    for (auto h : g->pool.free_list) {
+        drv().release(h);
+        g->pool.all.erase(std::find(g->pool.all.begin(), g->pool.all.end(), h));
+    }
+    g->pool.free_list.clear();
 }
 
 void write_bt_entry(Instance& in, int slot, int idx, int block) {
-    in.h_block_table[size_t(slot) * in.bt_stride + idx] = block;
+    in.h_block_table[size_t(slot) * in.bt_stride + idx] = phys_of(in, block);
 }
 
 void resize_kv(mesh_gpu* g, Instance& in, long long to) {
     int new_cap = blocks_for_target(in, to);
     if (new_cap >= in.cap_blocks) {
-        map_to(g, in, size_t(new_cap) * in.block_bytes);
+        assign_to(g, in, new_cap);
         for (int b = in.cap_blocks; b < new_cap; ++b) in.free_blocks.insert(b);
         in.cap_blocks = new_cap;
         in.target = to;
@@ -909,15 +984,15 @@ void resize_kv(mesh_gpu* g, Instance& in, long long to) {
     if (!from.empty()) {
         // one batched copy kernel per 256 moves, block lists passed by value (no pair buffer, no host wait)
         cudaStream_t st = stream_of(g, in);
-        uint8_t* base = reinterpret_cast<uint8_t*>(in.va);
-        launch_blocks_copy(base, base, in.block_bytes, from.data(), to_ids.data(), int(from.size()), st);
+        const std::vector<int> pf = phys_list(in, from), pt = phys_list(in, to_ids);
+        launch_blocks_copy(arena_ptr(g), arena_ptr(g), in.block_bytes, pf.data(), pt.data(), int(pf.size()), st);
         CK(cudaMemcpyAsync(in.d_block_table, in.h_block_table.data(), in.h_block_table.size() * sizeof(int),
                            cudaMemcpyHostToDevice, st));
         CK(cudaEventRecord(in.last_ev, st));
         g->st.blocks_moved += (long long)from.size();
         g->st.bytes_moved += 2LL * (long long)from.size() * in.block_bytes;
     }
-    // the tail stays mapped (lazy shrink, see reclaim_slack); queued work may still read it
+    // the extents above the new capacity stay assigned (lazy shrink, see reclaim_slack)
     in.free_blocks = low_free;
     in.cap_blocks = new_cap;
     in.target = to;
@@ -931,7 +1006,7 @@ int alloc_block(mesh_gpu* g, Instance& in) {
     if (in.free_blocks.empty()) {
         // physical overcommit beyond the accounted target (rounding slack exhausted)
         int b = in.cap_blocks;
-        map_to(g, in, size_t(b + 1) * in.block_bytes);
+        assign_to(g, in, b + 1);
         in.cap_blocks = b + 1;
         in.live_blocks++;
         return b;
@@ -1042,7 +1117,7 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     DecodeArgs a{};
     a.s = in.s;
     a.w = in.w;
-    a.kv_base = reinterpret_cast<uint8_t*>(in.va);
+    a.kv_base = arena_ptr(g);
     a.block_bytes = in.block_bytes;
     a.block_table = in.d_block_table;
     a.bt_stride = in.bt_stride;
@@ -1096,7 +1171,7 @@ void build_decode_desc(mesh_gpu* g, Instance& in, const int64_t* rids, int n, St
             if (d.n_upd >= MAX_BT_UPDATES) throw MeshError(MESH_ERR_RUNTIME, "too many block-table updates");
             d.upd[d.n_upd][0] = r.slot;
             d.upd[d.n_upd][1] = int(r.blocks.size()) - 1;
-            d.upd[d.n_upd][2] = b;
+            d.upd[d.n_upd][2] = phys_of(in, b);
             d.n_upd++;
         }
     }
@@ -1157,8 +1232,8 @@ void restore_parked(mesh_gpu* g, Instance& in, ReqState& r, SwapEntry& e, cudaSt
         write_bt_entry(in, r.slot, i, b);
     }
     CK(cudaStreamWaitEvent(st, e.done, 0));
-    launch_blocks_copy(reinterpret_cast<uint8_t*>(in.va), host_pool().ptr(e.chunk, e.off), in.block_bytes, nullptr,
-                       r.blocks.data(), nblk, st);
+    const std::vector<int> pb = phys_list(in, r.blocks);
+    launch_blocks_copy(arena_ptr(g), host_pool().ptr(e.chunk, e.off), in.block_bytes, nullptr, pb.data(), nblk, st);
     cudaEvent_t ev = record_new_event(st);
     if (st != stream_of(g, in)) {
         CK(cudaStreamWaitEvent(stream_of(g, in), ev, 0));
@@ -1252,9 +1327,9 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     PrefillArgs a{};
     a.s = in.s;
     a.w = in.w;
-    a.kv_base = reinterpret_cast<uint8_t*>(in.va);
+    a.kv_base = arena_ptr(g);
     a.block_bytes = in.block_bytes;
-    a.kv_blocks = (long long)(in.va_size / size_t(in.block_bytes));
+    a.kv_blocks = (long long)(g->arena.bytes(g->pool.gran) / size_t(in.block_bytes));
     a.bt_row = in.d_block_table + size_t(r.slot) * in.bt_stride;
     a.slot = r.slot;
     a.L = L;
@@ -1270,7 +1345,7 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     // Prefill GEMMs keep no grid barrier, so they may take every SM (their CTAs
     // queue behind other lanes' decode grids and finish); a lane's quota bounds
     // its persistent decode grid only. Measured: +5 % C2 tokens/s, -8 % e2e wall.
-    a.max_ctas = g->prefill_quota ? ln.ctas : 0;
+    a.max_ctas = g->prefill_quota ? std::max(ln.ctas, g->prefill_min_ctas) : 0;
     a.tile_ctr = ln.tile_ctr;
     a.last_tok = in.d_last_tok;
     a.tok_out = g->d_tok + t.ring * 8;
@@ -1365,7 +1440,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         CK(cudaStreamCreateWithFlags(&g->side_in, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&g->lane_join, cudaEventDisableTiming));
         // peers: devices that can load this device's memory over NVLink get read/write
-        // access to every KV granule (map_to); this device may load theirs
+        // access to every KV granule (back_slots); this device may load theirs
         for (int d = 0; d < n; ++d) {
             if (d == cfg->device) continue;
             int can = 0;
@@ -1380,23 +1455,6 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->st.peer_devices = (int64_t)g->peers.size();
         // pinned swap space, pinned once up front (cudaHostAlloc of GBs takes ~0.1-1 s)
         if (cfg->swap_pool_mb > 0) host_pool().reserve(size_t(cfg->swap_pool_mb) << 20);
-        // MESH_GPU_KV_PREALLOC_GB: create that much of the KV pool's physical granules
-        // now. cuMemCreate costs ~1-4 ms per 32 MiB granule once dozens of instances
-        // hold mappings (C3 e2e, 80 instance starts: 10.8 s of host time); created
-        // up front, a grow on the serving path only maps.
-        if (const char* e = std::getenv("MESH_GPU_KV_PREALLOC_GB")) {
-            const long long want = std::min<long long>(g->pool.limit, (long long)(std::atof(e) * double(1LL << 30)));
-            CUmemAllocationProp pp = {};
-            pp.type = CU_MEM_ALLOCATION_TYPE_PINNED;
-            pp.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
-            pp.location.id = cfg->device;
-            for (long long have = 0; have + (long long)g->pool.gran <= want; have += (long long)g->pool.gran) {
-                CUmemGenericAllocationHandle h;
-                if (drv().create(&h, g->pool.gran, &pp, 0) != CUDA_SUCCESS) break;
-                g->pool.all.push_back(h);
-                g->pool.free_list.push_back(h);
-            }
-        }
         g->pool.device = cfg->device;
         CUmemAllocationProp prop2 = {};
         prop2.type = CU_MEM_ALLOCATION_TYPE_PINNED;
@@ -1412,7 +1470,20 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->pool.gran = want;
         g->st.kv_granule_bytes = (long long)want;
         g->pool.limit = cfg->kv_pool_bytes > 0 ? cfg->kv_pool_bytes : (long long)(prop.totalGlobalMem / 2);
-        g->va_size = ((size_t(g->pool.limit) + (size_t(256) << 20)) / g->pool.gran + 1) * g->pool.gran;
+        // the KV arena: one VA range of limit / granule slots for every instance
+        g->arena.nslots = int(std::max<long long>(1, g->pool.limit / (long long)g->pool.gran));
+        CU(drv().addr_reserve(&g->arena.base, g->arena.bytes(g->pool.gran), g->pool.gran, 0, 0), "cuMemAddressReserve");
+        g->arena.h.assign(size_t(g->arena.nslots), 0);
+        g->arena.owner.assign(size_t(g->arena.nslots), -1);
+        g->arena.ev.assign(size_t(g->arena.nslots), nullptr);
+        // MESH_GPU_KV_PREALLOC_GB: back that much of the arena now (cuMemCreate +
+        // cuMemMap, ~1-4 ms per granule and a device drain per map batch), so the
+        // serving path never calls the VMM driver
+        if (const char* e = std::getenv("MESH_GPU_KV_PREALLOC_GB")) {
+            const long long want = std::min<long long>(g->pool.limit, (long long)(std::atof(e) * double(1LL << 30)));
+            const int n = int(std::min<long long>(g->arena.nslots, want / (long long)g->pool.gran));
+            if (n > 0) back_slots(g.get(), 0, n);
+        }
         CK(cudaHostAlloc((void**)&g->h_desc, sizeof(StepDesc) * RING, cudaHostAllocDefault));
         CK(cudaMalloc((void**)&g->d_desc, sizeof(StepDesc) * RING));
         CK(cudaHostAlloc((void**)&g->h_tok, sizeof(int) * 8 * RING, cudaHostAllocDefault));
@@ -1424,6 +1495,10 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->check = std::getenv("MESH_GPU_CHECK") != nullptr;
         g->poison = std::getenv("MESH_GPU_POISON") != nullptr;
         g->prefill_quota = std::getenv("MESH_PREFILL_QUOTA") != nullptr;
+        if (const char* e = std::getenv("MESH_PREFILL_CTAS")) {
+            g->prefill_quota = true;
+            g->prefill_min_ctas = std::atoi(e);
+        }
         if (const char* e = std::getenv("MESH_GPU_NSTAGE")) g->nstage = std::atoi(e) >= 16 ? 16 : 8;
         if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
         if (const char* e = std::getenv("MESH_GPU_WCACHE_GB")) g->wcache_cap = size_t(std::max(0.0, std::atof(e)) * double(1 << 30));
@@ -1470,11 +1545,6 @@ void mesh_gpu_close(mesh_gpu* g) {
     }
     for (auto& [id, in] : g->insts) {
         for (PendingFree& pf : in->pending_free) cudaEventDestroy(pf.ev);
-        try {
-            unmap_tail(g, *in, 0);
-        } catch (...) {
-        }
-        if (in->va) drv().addr_free(in->va, in->va_size);
         if (in->last_ev) cudaEventDestroy(in->last_ev);
         cudaFree(in->d_block_table);
         cudaFree(in->d_last_tok);
@@ -1485,14 +1555,14 @@ void mesh_gpu_close(mesh_gpu* g) {
     }
     cudaStreamSynchronize(g->side);
     for (auto& b : g->ibufs) {
-        try {
-            unmap_idle(g, b, 0);
-        } catch (...) {
-        }
-        drv().addr_free(b.va, g->va_size);
         cudaFree(b.d_block_table);
         cudaFree(b.d_last_tok);
     }
+    for (int sl = 0; sl < g->arena.nslots; ++sl) {
+        if (g->arena.ev[size_t(sl)]) cudaEventDestroy(g->arena.ev[size_t(sl)]);
+        if (g->arena.h[size_t(sl)]) drv().unmap(g->arena.base + size_t(sl) * g->pool.gran, g->pool.gran);
+    }
+    if (g->arena.base) drv().addr_free(g->arena.base, g->arena.bytes(g->pool.gran));
     for (auto h : g->pool.all) drv().release(h);
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
@@ -1568,41 +1638,26 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         size_t norms = (2 * L + 1) * s.d * 4, rope = size_t(s.max_seq) * (s.dh / 2) * 8;
         size_t total = L * (qkv + o + gu + dn) + lm + emb + norms + rope + 4096;
         in->block_bytes = (long long)KV_BLOCK_TOKENS * s.kv_bytes_per_token();
-        size_t gran = g->pool.gran;
-        in->va_size = g->va_size;
-        if (size_t(in->block_bytes) * (DEC_MAXB + 2) > in->va_size - size_t(g->pool.limit))
-            throw MeshError(MESH_ERR_CONFIG, "KV block too large for the VA slack");
+        // extents of >= 32 whole blocks: at most one block per extent lost to alignment
+        in->ext_slots = int(std::max<long long>(1, (32 * in->block_bytes + (long long)g->pool.gran - 1) /
+                                                       (long long)g->pool.gran));
+        if (in->ext_slots > g->arena.nslots) throw MeshError(MESH_ERR_CONFIG, "KV block too large for the pool");
         in->bt_stride = (s.max_seq + KV_BLOCK_TOKENS - 1) / KV_BLOCK_TOKENS;
         in->h_block_table.assign(size_t(MAX_SLOTS) * in->bt_stride, 0);
-        // per-instance buffers first: recycle the free range that still has the most
-        // granules mapped (else allocate); on any later failure they go back
-        bool recycled = false;
+        // per-instance buffers first (recycled, else allocated); on any later failure they go back
         if (!g->ibufs.empty()) {
-            size_t bi = 0;
-            for (size_t i = 1; i < g->ibufs.size(); ++i)
-                if (g->ibufs[i].granules.size() > g->ibufs[bi].granules.size()) bi = i;
-            mesh_gpu::InstBufs& bb = g->ibufs[bi];
-            in->va = bb.va;
-            in->d_block_table = bb.d_block_table;
-            in->d_last_tok = bb.d_last_tok;
-            in->granules = std::move(bb.granules);
-            g->ibufs.erase(g->ibufs.begin() + long(bi));
-            recycled = true;
-        }
-        if (!recycled) {
-            // KV region: reserve the whole pool's worth of VA
-            CU(drv().addr_reserve(&in->va, in->va_size, gran, 0, 0), "cuMemAddressReserve");
-            if (cudaMalloc((void**)&in->d_block_table, sizeof(int) * size_t(MAX_SLOTS) * DEC_BT_MAX) != cudaSuccess ||
-                cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS) != cudaSuccess) {
-                cudaGetLastError();
-                if (in->d_block_table) cudaFree(in->d_block_table);
-                drv().addr_free(in->va, in->va_size);
-                throw MeshError(MESH_ERR_NOMEM, "instance buffers: cudaMalloc failed");
-            }
+            in->d_block_table = g->ibufs.back().d_block_table;
+            in->d_last_tok = g->ibufs.back().d_last_tok;
+            g->ibufs.pop_back();
+        } else if (cudaMalloc((void**)&in->d_block_table, sizeof(int) * size_t(MAX_SLOTS) * DEC_BT_MAX) != cudaSuccess ||
+                   cudaMalloc((void**)&in->d_last_tok, sizeof(int) * MAX_SLOTS) != cudaSuccess) {
+            cudaGetLastError();
+            if (in->d_block_table) cudaFree(in->d_block_table);
+            throw MeshError(MESH_ERR_NOMEM, "instance buffers: cudaMalloc failed");
         }
         Instance* ip = in.get();
         auto give_back_bufs = [g, ip] {
-            g->ibufs.push_back({ip->va, ip->d_block_table, ip->d_last_tok, std::move(ip->granules)});
+            g->ibufs.push_back({ip->d_block_table, ip->d_last_tok});
         };
         // weights: share a live or idle set of the same model, else allocate
         // (stream-ordered, so a later free never serialises the device) and
@@ -1620,15 +1675,10 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
                 e = cudaMallocAsync((void**)&in->wmem, total, st);
             }
             if (e != cudaSuccess) {
-                // then the KV pool's created-but-unmapped granules (MESH_GPU_KV_PREALLOC_GB):
-                // weights come first, the pool re-creates granules on demand
+                // then the KV arena's backed but unassigned slots: weights come first,
+                // the arena re-backs slots on demand (the rare path that unmaps)
                 cudaGetLastError();
-                CK(cudaStreamSynchronize(g->side));
-                for (auto h : g->pool.free_list) {
-                    drv().release(h);
-                    g->pool.all.erase(std::find(g->pool.all.begin(), g->pool.all.end(), h));
-                }
-                g->pool.free_list.clear();
+                release_free_slots(g);
                 cudaMemPool_t mp;
                 if (cudaDeviceGetDefaultMemPool(&mp, g->cfg.device) == cudaSuccess) cudaMemPoolTrimTo(mp, 0);
                 e = cudaMallocAsync((void**)&in->wmem, total, st);
@@ -1721,7 +1771,8 @@ mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id) {
         lane_of(g, in).n_inst--;
         // release the weight set (kept while idle, for a reload) and recycle the
         // per-instance buffers: no cudaFree, which would serialise the device
-        g->ibufs.push_back({in.va, in.d_block_table, in.d_last_tok, std::move(in.granules)});
+        while (!in.ext.empty()) release_extent(g, in, nullptr);  // its work finished above
+        g->ibufs.push_back({in.d_block_table, in.d_last_tok});
         auto wit = g->wsets.find(in.shape_key);
         if (wit != g->wsets.end()) {
             wit->second.refs--;
@@ -1767,8 +1818,8 @@ std::string debug_request_state(mesh_gpu* g, Instance& in, int64_t rid) {
                   cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < r.blocks.size(); ++i) {
         m += " " + std::to_string(r.blocks[i]);
-        if (dev[i] != r.blocks[i]) m += "(dev " + std::to_string(dev[i]) + ")";
-        if (in.h_block_table[size_t(r.slot) * in.bt_stride + i] != r.blocks[i]) m += "(mirror!)";
+        if (dev[i] != phys_of(in, r.blocks[i])) m += "(dev " + std::to_string(dev[i]) + ")";
+        if (in.h_block_table[size_t(r.slot) * in.bt_stride + i] != phys_of(in, r.blocks[i])) m += "(mirror!)";
         if (in.free_blocks.count(r.blocks[i])) m += "(FREE!)";
         for (auto& [o, os] : in.reqs)
             if (o != rid && std::find(os.blocks.begin(), os.blocks.end(), r.blocks[i]) != os.blocks.end())
@@ -1779,8 +1830,7 @@ std::string debug_request_state(mesh_gpu* g, Instance& in, int64_t rid) {
     int bad_pos = -1, bad_layer = -1, nbad = 0;
     for (int p = 0; p < r.ctx; ++p) {
         if (p % KV_BLOCK_TOKENS == 0)
-            CK(cudaMemcpy(blk.data(), reinterpret_cast<uint8_t*>(in.va) + size_t(r.blocks[p / KV_BLOCK_TOKENS]) *
-                                                                           in.block_bytes,
+            CK(cudaMemcpy(blk.data(), arena_ptr(g) + size_t(phys_of(in, r.blocks[p / KV_BLOCK_TOKENS])) * in.block_bytes,
                           in.block_bytes, cudaMemcpyDeviceToHost));
         for (int l = 0; l < in.s.n_layers; ++l)
             for (int kv = 0; kv < 2; ++kv)
@@ -1944,8 +1994,9 @@ mesh_status mesh_gpu_swap_out(mesh_gpu* g, int64_t instance_id, int64_t request_
             cudaEvent_t ready = record_new_event(stream_of(g, in));
             CK(cudaStreamWaitEvent(g->side, ready, 0));
             cudaEventDestroy(ready);
-            launch_blocks_copy(host_pool().ptr(ci, off), reinterpret_cast<uint8_t*>(in.va), in.block_bytes,
-                               r.blocks.data(), nullptr, int(r.blocks.size()), g->side);
+            const std::vector<int> pb = phys_list(in, r.blocks);
+            launch_blocks_copy(host_pool().ptr(ci, off), arena_ptr(g), in.block_bytes, pb.data(), nullptr,
+                               int(pb.size()), g->side);
             e.done = record_new_event(g->side);
             pf.ev = record_new_event(g->side);
             pf.blocks = r.blocks;
@@ -2063,8 +2114,8 @@ mesh_status mesh_gpu_migrate(mesh_gpu* src, int64_t src_instance, mesh_gpu* dst,
         CK(cudaStreamWaitEvent(dst_st, ready, 0));
         cudaEventDestroy(ready);
         // one copy kernel on the destination GPU: P2P loads of the source blocks over NVLink
-        launch_blocks_copy(reinterpret_cast<uint8_t*>(di.va), reinterpret_cast<const uint8_t*>(si.va), di.block_bytes,
-                           sr.blocks.data(), dr.blocks.data(), int(sr.blocks.size()), dst_st);
+        const std::vector<int> ps = phys_list(si, sr.blocks), pd = phys_list(di, dr.blocks);
+        launch_blocks_copy(arena_ptr(dst), arena_ptr(src), di.block_bytes, ps.data(), pd.data(), int(ps.size()), dst_st);
         const int last = sr.tokens.empty() ? 0 : sr.tokens.back();
         set_int<<<1, 1, 0, dst_st>>>(di.d_last_tok + dr.slot, last);
         CK(cudaGetLastError());
@@ -2147,7 +2198,11 @@ mesh_status mesh_gpu_instance_kv(mesh_gpu* g, int64_t instance_id, int64_t* targ
     return guarded(g, [&] {
         Instance& in = inst_of(g, instance_id);
         if (target_bytes) *target_bytes = in.target;
-        if (mapped_bytes) *mapped_bytes = (int64_t)in.granules.size() * (int64_t)g->pool.gran;
+        if (mapped_bytes) {
+            int64_t n = 0;
+            for (const Instance::Extent& e : in.ext) n += e.k;
+            *mapped_bytes = n * (int64_t)g->pool.gran;
+        }
         if (capacity_blocks) *capacity_blocks = in.cap_blocks;
         if (live_blocks) *live_blocks = in.live_blocks;
     });

@@ -66,12 +66,12 @@ KV_POOL = 100 << 30     # value leg: KV pool per device
 # plus each instance's physical rounding to whole granules (<= 256 MiB x ~66 instances); 53 GB of
 # weights + 116 GB of KV + lane scratch fit the B200's 179 GB
 E2E_KV_POOL = 116 << 30
-KV_PREALLOC_GB = 112    # e2e: physical KV granules created when the data plane opens (not on the serving path)
+KV_PREALLOC_GB = 96     # e2e: KV arena backed at open (params of the 8 resident models + this fit HBM with scratch)
 # e2e: 256 MiB physical KV granules. cuMemMap / cuMemSetAccess cost milliseconds per call once dozens
 # of instances hold mappings; at 80 instance starts 32 MiB granules spent 7.8 s of host time in them,
 # 128 MiB 4.3 s, 512 MiB 2.4 s (tools/e2e_c3.py, MESH_GPU_KV_GRANULE_MB)
 KV_GRANULE_MB = 256
-E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "8,12,16").split(",")]
+E2E_SCALES = [int(x) for x in os.environ.get("MESH_BENCH_E2E_SCALES", "10,12,14,16").split(",")]
 WATERMARK = 20.0
 CPU_SAMPLE_S = 15.0     # bounded CPU baseline sample
 CPU_MAX_SEQ = 1160      # >= the longest I + O of the length set (1139)
@@ -280,9 +280,14 @@ class Colocated:
 
         from paper_2507_00507_b200.gpu import SHAPES, MeshGpu
         # the whole KV arena backed at open: no VMM driver call (each drains the device) while serving
-        os.environ.setdefault("MESH_GPU_KV_PREALLOC_GB", str(KV_POOL >> 30))
-        self.g = MeshGpu(device, kv_pool_bytes=KV_POOL, prompt_seed=seed, lanes=LANES,
-                         kv_granule_bytes=KV_GRANULE_MB << 20)
+        prev = os.environ.get("MESH_GPU_KV_PREALLOC_GB")
+        os.environ["MESH_GPU_KV_PREALLOC_GB"] = prev or str(KV_POOL >> 30)
+        try:
+            self.g = MeshGpu(device, kv_pool_bytes=KV_POOL, prompt_seed=seed, lanes=LANES,
+                             kv_granule_bytes=KV_GRANULE_MB << 20)
+        finally:
+            if prev is None:
+                del os.environ["MESH_GPU_KV_PREALLOC_GB"]
         self.shapes = [SHAPES[m] for m in MODELS]
         self.rng = random.Random(seed)
         self.lengths = load_lengths()

@@ -114,6 +114,11 @@ const char* mesh_gpu_last_error(const mesh_gpu* g);
 mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mesh_model_shape* shape,
                                      uint64_t weight_seed);
 mesh_status mesh_gpu_instance_destroy(mesh_gpu* g, int64_t instance_id);
+/* Optional, before serving: sizes the lanes' scratch for the largest of `n`
+ * shapes and grows the weight allocator's pool by the weight sets of all `n`
+ * (one entry per distinct model), so no later instance_create resizes scratch
+ * (a device-wide sync) or maps allocator memory (a device drain). */
+mesh_status mesh_gpu_reserve(mesh_gpu* g, const mesh_model_shape* shapes, int32_t n);
 
 /* Physically applies a KV ScaleOp at issue time. Every instance's
  * KV lives in one device-wide arena of granule slots; a grow assigns extents of

@@ -39,6 +39,7 @@ struct GpuExecutor::Api {
     decltype(&mesh_gpu_step_done) step_done;
     decltype(&mesh_gpu_timer_mark) timer_mark;
     decltype(&mesh_gpu_migrate) migrate;
+    decltype(&mesh_gpu_reserve) reserve;
 };
 
 namespace {
@@ -97,6 +98,7 @@ GpuExecutor::GpuExecutor(const std::string& lib_path, std::vector<int> devices, 
     BIND(step_done, "mesh_gpu_step_done");
     BIND(timer_mark, "mesh_gpu_timer_mark");
     BIND(migrate, "mesh_gpu_migrate");
+    BIND(reserve, "mesh_gpu_reserve");
 #undef BIND
     if (const char* e = std::getenv("MESH_MIGRATE")) migrate_ = std::atoi(e) != 0;
     for (int dev : devices_) {
@@ -129,12 +131,28 @@ mesh_gpu* GpuExecutor::handle_for_node(NodeId node) {
     return handles_[static_cast<std::size_t>(node) % handles_.size()];
 }
 
+namespace {
+mesh_model_shape c_shape(const LlamaShape& L, int max_seq) {
+    return mesh_model_shape{L.n_layers, L.d_model, L.n_heads, L.n_kv_heads, L.d_head, L.d_ff, L.vocab, L.tied,
+                            std::min(L.max_seq_len, max_seq), L.rope_theta, L.rms_eps};
+}
+}  // namespace
+
+// Every model's weight set and scratch reserved on every device before the clock
+// starts: instance starts on the serving path then neither resize scratch (a
+// device-wide sync) nor grow the weight allocator's pool (a device drain).
+void GpuExecutor::prepare(const Cluster& c) {
+    HostTimer ht(host_ms_create_);
+    std::vector<mesh_model_shape> shapes;
+    for (const auto& [id, m] : c.models()) shapes.push_back(c_shape(llama_shape_for(m.spec.size_class), m.spec.max_seq_len));
+    if (shapes.empty()) return;
+    for (mesh_gpu* h : handles_) check(h, api_->reserve(h, shapes.data(), int32_t(shapes.size())), "reserve");
+}
+
 void GpuExecutor::instance_start(const Cluster&, const Instance& inst) {
     HostTimer ht(host_ms_create_);
     ++instance_starts_;
-    const LlamaShape& L = llama_shape_for(inst.model->size_class);
-    mesh_model_shape s{L.n_layers, L.d_model, L.n_heads, L.n_kv_heads, L.d_head, L.d_ff, L.vocab, L.tied,
-                       std::min(L.max_seq_len, inst.model->max_seq_len), L.rope_theta, L.rms_eps};
+    const mesh_model_shape s = c_shape(llama_shape_for(inst.model->size_class), inst.model->max_seq_len);
     mesh_gpu* h = handle_for_node(inst.node_id);
     inst_dev_[inst.id] = static_cast<int>(static_cast<std::size_t>(inst.node_id) % handles_.size());
     check(h, api_->instance_create(h, inst.id, &s, weight_seed(inst.model->model_id)), "instance_create");

@@ -26,6 +26,7 @@ public:
     GpuExecutor(const std::string& lib_path, std::vector<int> devices, long long kv_pool_bytes);
     ~GpuExecutor() override;
 
+    void prepare(const Cluster&) override;
     void instance_start(const Cluster&, const Instance&) override;
     void kv_issue(const Cluster&, const Instance&, const ScaleOp&) override;
     void iteration_start(const Cluster&, const Node&, const Instance&, const IterationPlan&) override;

@@ -1388,6 +1388,44 @@ mesh_status guarded(mesh_gpu* g, F&& body, double* host_ms = nullptr) {
     }
 }
 
+// The data plane's shape of a C-ABI model shape (validated: throws MESH_ERR_CONFIG).
+Shape shape_of(const mesh_model_shape& m) {
+    const mesh_model_shape* sh = &m;
+    Shape s{};
+    s.n_layers = sh->n_layers;
+    s.d = sh->d_model;
+    s.n_heads = sh->n_heads;
+    s.n_kv = sh->n_kv_heads;
+    s.dh = sh->d_head;
+    s.ff = sh->d_ff;
+    s.vocab = sh->vocab;
+    s.tied = sh->tied_embeddings;
+    s.max_seq = sh->max_seq_len;
+    s.rope_theta = sh->rope_theta > 0 ? sh->rope_theta : 10000.f;
+    s.eps = sh->rms_eps > 0 ? sh->rms_eps : 1e-5f;
+    if (s.dh != 64 && s.dh != 128) throw MeshError(MESH_ERR_CONFIG, "d_head must be 64 or 128");
+    if (s.n_heads % s.n_kv != 0 || s.gq() * s.dh > 512)
+        throw MeshError(MESH_ERR_CONFIG, "GQA group x d_head must be <= 512 (decode smem budget)");
+    if (s.n_heads * s.dh != s.d) throw MeshError(MESH_ERR_CONFIG, "n_heads * d_head must equal d_model");
+    if (s.d % 256 || s.ff % 256 || s.vocab % 128 || (s.qkv_rows() % 128))
+        throw MeshError(MESH_ERR_CONFIG, "d_model/d_ff must be multiples of 256, vocab of 128");
+    if (s.n_layers < 1 || s.n_layers * 4 + 1 > DEC_CLAIM_MAX) throw MeshError(MESH_ERR_CONFIG, "n_layers out of range");
+    if (s.n_kv > DEC_KV_HEADS_MAX) throw MeshError(MESH_ERR_CONFIG, "n_kv_heads out of range");
+    if (s.max_seq < 2 || s.max_seq > DEC_BT_MAX * KV_BLOCK_TOKENS)
+        throw MeshError(MESH_ERR_CONFIG, "max_seq_len out of range");
+    return s;
+}
+
+// Bytes of one weight set (tiled GEMM operands, embeddings, gains, RoPE table).
+size_t weight_set_bytes(const Shape& s) {
+    const size_t L = s.n_layers;
+    const size_t qkv = size_t(s.qkv_rows()) * s.d * 2, o = size_t(s.d) * s.n_heads * s.dh * 2,
+                 gu = size_t(2 * s.ff) * s.d * 2, dn = size_t(s.d) * s.ff * 2, lm = size_t(s.vocab) * s.d * 2,
+                 emb = size_t(s.vocab) * s.d * 2;
+    const size_t norms = (2 * L + 1) * s.d * 4, rope = size_t(s.max_seq) * (s.dh / 2) * 8;
+    return L * (qkv + o + gu + dn) + lm + emb + norms + rope + 4096;
+}
+
 }  // namespace
 
 extern "C" {
@@ -1476,6 +1514,16 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         g->arena.h.assign(size_t(g->arena.nslots), 0);
         g->arena.owner.assign(size_t(g->arena.nslots), -1);
         g->arena.ev.assign(size_t(g->arena.nslots), nullptr);
+        // weight sets come from the stream-ordered allocator's pool: keep freed memory
+        // in the pool (default threshold 0 hands it back to the driver at every
+        // synchronisation, and re-growing it maps memory, which drains the device)
+        {
+            cudaMemPool_t mp;
+            if (cudaDeviceGetDefaultMemPool(&mp, cfg->device) == cudaSuccess) {
+                uint64_t thr = UINT64_MAX;
+                cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr);
+            }
+        }
         // MESH_GPU_KV_PREALLOC_GB: back that much of the arena now (cuMemCreate +
         // cuMemMap, ~1-4 ms per granule and a device drain per map batch), so the
         // serving path never calls the VMM driver
@@ -1594,29 +1642,11 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
     if (!g || !sh) return MESH_ERR_ARG;
     return guarded(g, [&] {
         if (g->insts.count(instance_id)) throw MeshError(MESH_ERR_ARG, "duplicate instance id");
-        Shape s{};
-        s.n_layers = sh->n_layers;
-        s.d = sh->d_model;
-        s.n_heads = sh->n_heads;
-        s.n_kv = sh->n_kv_heads;
-        s.dh = sh->d_head;
-        s.ff = sh->d_ff;
-        s.vocab = sh->vocab;
-        s.tied = sh->tied_embeddings;
-        s.max_seq = sh->max_seq_len;
-        s.rope_theta = sh->rope_theta > 0 ? sh->rope_theta : 10000.f;
-        s.eps = sh->rms_eps > 0 ? sh->rms_eps : 1e-5f;
-        if (s.dh != 64 && s.dh != 128) throw MeshError(MESH_ERR_CONFIG, "d_head must be 64 or 128");
-        if (s.n_heads % s.n_kv != 0 || s.gq() * s.dh > 512)
-            throw MeshError(MESH_ERR_CONFIG, "GQA group x d_head must be <= 512 (decode smem budget)");
-        if (s.n_heads * s.dh != s.d) throw MeshError(MESH_ERR_CONFIG, "n_heads * d_head must equal d_model");
-        if (s.d % 256 || s.ff % 256 || s.vocab % 128 || (s.qkv_rows() % 128))
-            throw MeshError(MESH_ERR_CONFIG, "d_model/d_ff must be multiples of 256, vocab of 128");
-        if (s.n_layers < 1 || s.n_layers * 4 + 1 > DEC_CLAIM_MAX) throw MeshError(MESH_ERR_CONFIG, "n_layers out of range");
-        if (s.n_kv > DEC_KV_HEADS_MAX) throw MeshError(MESH_ERR_CONFIG, "n_kv_heads out of range");
-        if (s.max_seq < 2 || s.max_seq > DEC_BT_MAX * KV_BLOCK_TOKENS)
-            throw MeshError(MESH_ERR_CONFIG, "max_seq_len out of range");
+        const Shape s = shape_of(*sh);
+        static const bool ctrace = std::getenv("MESH_GPU_CREATE_TRACE") != nullptr;
+        const auto c0 = std::chrono::steady_clock::now();
         ensure_scratch(g, s);
+        const auto c1 = std::chrono::steady_clock::now();
         auto in = std::make_unique<Instance>();
         in->id = instance_id;
         // bind to an empty lane if there is one, else to the lane with the fewest
@@ -1636,7 +1666,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
                gu = size_t(2 * s.ff) * s.d * 2, dn = size_t(s.d) * s.ff * 2, lm = size_t(s.vocab) * s.d * 2,
                emb = size_t(s.vocab) * s.d * 2;
         size_t norms = (2 * L + 1) * s.d * 4, rope = size_t(s.max_seq) * (s.dh / 2) * 8;
-        size_t total = L * (qkv + o + gu + dn) + lm + emb + norms + rope + 4096;
+        const size_t total = weight_set_bytes(s);
         in->block_bytes = (long long)KV_BLOCK_TOKENS * s.kv_bytes_per_token();
         // extents of >= 32 whole blocks: at most one block per extent lost to alignment
         in->ext_slots = int(std::max<long long>(1, (32 * in->block_bytes + (long long)g->pool.gran - 1) /
@@ -1690,6 +1720,7 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
             }
             fresh = true;
         }
+        const auto c2 = std::chrono::steady_clock::now();
         uint8_t* p = in->wmem;
         auto take = [&](size_t n) {
             uint8_t* r = p;
@@ -1753,6 +1784,33 @@ mesh_status mesh_gpu_instance_create(mesh_gpu* g, int64_t instance_id, const mes
         g->lanes[best].n_inst++;
         g->insts.emplace(instance_id, std::move(in));
         rebalance_lanes(g);
+        if (ctrace) {
+            auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+            const auto c3 = std::chrono::steady_clock::now();
+            fprintf(stderr, "instance_create %lld: scratch %.2f ms, weights alloc %.2f ms (%s), rest %.2f ms\n",
+                    (long long)instance_id, ms(c0, c1), ms(c1, c2), fresh ? "fresh" : "shared", ms(c2, c3));
+        }
+    }, &g->st.host_ms_create);
+}
+
+mesh_status mesh_gpu_reserve(mesh_gpu* g, const mesh_model_shape* shapes, int32_t n) {
+    if (!g || (n > 0 && !shapes) || n < 0) return MESH_ERR_ARG;
+    return guarded(g, [&] {
+        size_t wbytes = 0;
+        for (int i = 0; i < n; ++i) {
+            const Shape s = shape_of(shapes[i]);
+            ensure_scratch(g, s);
+            wbytes += (weight_set_bytes(s) + 255) & ~size_t(255);
+        }
+        if (wbytes == 0) return;
+        // grow the allocator pool now (freed memory stays in it: release threshold max)
+        void* p = nullptr;
+        if (cudaMallocAsync(&p, wbytes, g->side) != cudaSuccess) {
+            cudaGetLastError();
+            return;  // best effort: creates allocate on demand
+        }
+        CK(cudaFreeAsync(p, g->side));
+        CK(cudaStreamSynchronize(g->side));
     }, &g->st.host_ms_create);
 }
 

@@ -50,7 +50,7 @@ sys.path.insert(0, ROOT)
 from make_ctrl_golden import TEMPLATES, const_rate, lengths_csv, poisson_trace  # noqa: E402
 
 C3_MODELS = ["1b", "3b", "7b", "1b", "3b", "7b", "1b", "3b"]
-C3_SCALES = [1, 2, 4, 6, 8, 12, 16]
+C3_SCALES = (1, 2, 4, 6, 8, 10, 12, 14, 16)
 C3_WINDOW = 30.0
 # runtime.colocation_speedup: measured by tools/measure_colocation.py (profiles/colocation_r02.json):
 # the C3 node's step sequence takes 4.51 s on one lane and 2.70 s on eight concurrent lanes

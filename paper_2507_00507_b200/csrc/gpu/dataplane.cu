@@ -413,6 +413,8 @@ struct Lane {
     double weight_bytes = 0;  // bound instances (placement balance, SM quota)
     int n_inst = 0;
     int* tile_ctr = nullptr;  // prefill GEMM dynamic tile counter
+    float* sk_ws = nullptr;   // prefill split-K partials
+    int* sk_cnt = nullptr;    // prefill split-K arrival counters
     cudaEvent_t quota_ev = nullptr;  // tail of the lane's queue when its quota last shrank
 };
 
@@ -1347,6 +1349,8 @@ void launch_prefill_step(mesh_gpu* g, Instance& in, const mesh_step_plan& p, Tic
     // its persistent decode grid only. Measured: +5 % C2 tokens/s, -8 % e2e wall.
     a.max_ctas = g->prefill_quota ? std::max(ln.ctas, g->prefill_min_ctas) : 0;
     a.tile_ctr = ln.tile_ctr;
+    a.sk_ws = ln.sk_ws;
+    a.sk_cnt = ln.sk_cnt;
     a.last_tok = in.d_last_tok;
     a.tok_out = g->d_tok + t.ring * 8;
     CK(cudaEventRecord(t.start, ln.stream));
@@ -1472,6 +1476,8 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             dalloc(&l.claim, DEC_CLAIM_MAX);
             dalloc(&l.qkv_done, DEC_KV_HEADS_MAX);
             dalloc(&l.tile_ctr, 1);
+            dalloc(&l.sk_ws, size_t(2) * g->sms * 128 * 256);
+            dalloc(&l.sk_cnt, SK_TILES_MAX);
             CK(cudaEventCreateWithFlags(&l.quota_ev, cudaEventDisableTiming));
         }
         CK(cudaStreamCreateWithFlags(&g->side, cudaStreamNonBlocking));
@@ -1615,7 +1621,7 @@ void mesh_gpu_close(mesh_gpu* g) {
     for (Lane& l : g->lanes) {
         void* lane_ptrs[] = {l.h, l.act, l.attn, l.abuf, l.q, l.ssA, l.ssB, l.apart, l.acnt, l.arg_val,
                              l.arg_idx, l.arg_cnt, l.logits, l.bar, l.p_h, l.p_act, l.p_rs, l.p_q, l.p_attn,
-                             l.p_abuf, l.p_logits, l.p_tokens, l.tile_ctr, l.claim, l.qkv_done};
+                             l.p_abuf, l.p_logits, l.p_tokens, l.tile_ctr, l.sk_ws, l.sk_cnt, l.claim, l.qkv_done};
         for (void* p : lane_ptrs)
             if (p) cudaFree(p);
         if (l.stream) cudaStreamDestroy(l.stream);
@@ -1970,6 +1976,12 @@ mesh_status mesh_gpu_step(mesh_gpu* g, int64_t instance_id, const mesh_step_plan
             }
         }
         *ticket = g->next_ticket++;
+        static FILE* slog = std::getenv("MESH_GPU_STEP_LOG") ? std::fopen(std::getenv("MESH_GPU_STEP_LOG"), "w") : nullptr;
+        if (slog)  // diagnostics: host time, instance, model (weight set), lane, decode batch (0: prefill)
+            std::fprintf(slog, "%.1f %lld %llu %d %d\n",
+                         std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now().time_since_epoch()).count(),
+                         (long long)instance_id, (unsigned long long)(in.shape_key % 100000), in.lane,
+                         t.prefill ? 0 : plan->n_decode);
         g->tickets.emplace(*ticket, std::move(t));
     }, &g->st.host_ms_step);
 }

@@ -266,7 +266,7 @@ __device__ __forceinline__ void tc_epilogue(const PrefillArgs& a, int row, int l
 template <int KIND, int BN, int CS>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     pf_gemm_tc(const __grid_constant__ PrefillArgs a, const __grid_constant__ CUtensorMap wmap,
-               const __grid_constant__ CUtensorMap xmap, int N, int K, int Lrows, int layer) {
+               const __grid_constant__ CUtensorMap xmap, int N, int K, int Lrows, int layer, int splits) {
     using C = TcCfg<BN>;
     constexpr int B_PART = C::B_STAGE / CS;      // token rows this CTA fetches for the whole cluster
     constexpr uint16_t MASK = (1u << CS) - 1u;
@@ -288,6 +288,16 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     const int cluster = blockIdx.x / CS, nclusters = gridDim.x / CS;
     // a cluster owns CS consecutive weight tiles and one token tile
     const int nN = (Lrows + BN - 1) / BN, ntiles = (N / TC_BM / CS) * nN, nk = K / TC_BK;
+    // Split-K (CS == 1, tiles < SMs): work unit u = (tile u / splits, K range u % splits).
+    // Every unit of a split tile writes its fp32 partial to the lane's workspace; the
+    // last to arrive sums the partials in split order (deterministic) and runs the
+    // fused epilogue. No unit waits for another (no co-residency assumption).
+    const int nunits = ntiles * splits;
+    auto krange = [&](int u, int& k0, int& k1) {
+        const int sp = u % splits;
+        k0 = (nk * sp) / splits;
+        k1 = (nk * (sp + 1)) / splits;
+    };
     if (warp == 0 && lane == 0) {
         for (int s = 0; s < C::STAGES; ++s) {
             mbar_init(full + s, 1);
@@ -322,11 +332,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const int sl = i & 3;
             mbar_wait(qempty + sl, ((i >> 2) & 1) ^ 1);
             const int t = atomicAdd(a.tile_ctr, 1);
-            // ntiles + gridDim.x draws in all; the last one resets the counter for the next launch
-            if (t == ntiles + int(gridDim.x) - 1) *reinterpret_cast<volatile int*>(a.tile_ctr) = 0;
-            qid[sl] = t < ntiles ? t : -1;
+            // nunits + gridDim.x draws in all; the last one resets the counter for the next launch
+            if (t == nunits + int(gridDim.x) - 1) *reinterpret_cast<volatile int*>(a.tile_ctr) = 0;
+            qid[sl] = t < nunits ? t : -1;
             mbar_arrive(qfull + sl);
-            return t < ntiles ? t : -1;
+            return t < nunits ? t : -1;
         }
     };
     // whole_warp: every lane reads the slot, then lane 0 releases it; else one thread does both
@@ -348,10 +358,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             for (int i = 0;; ++i) {
-                const int t = draw(i, cluster + i * nclusters);
-                if (t < 0) break;
+                const int u = draw(i, cluster + i * nclusters);
+                if (u < 0) break;
+                const int t = u / splits;
                 const int mt = (t / nN) * CS + rank, nt = t % nN;
-                for (int kb = 0; kb < nk; ++kb) {
+                int k0, k1;
+                krange(u, k0, k1);
+                for (int kb = k0; kb < k1; ++kb) {
                     mbar_wait(empty + stage, phase ^ 1);
                     mbar_arrive_expect_tx(full + stage, TC_A_STAGE + C::B_STAGE);
                     // eight pre-swizzled 16x64 blocks, one TMA instruction
@@ -375,18 +388,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             int stage = 0, acc = 0;
             uint32_t phase = 0, aphase = 0;
             for (int i = 0;; ++i) {
-                if (take(i, cluster + i * nclusters, false) < 0) break;
+                const int u = take(i, cluster + i * nclusters, false);
+                if (u < 0) break;
+                int k0, k1;
+                krange(u, k0, k1);
                 mbar_wait(tempty + acc, aphase ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + uint32_t(acc * BN);
-                for (int kb = 0; kb < nk; ++kb) {
+                for (int kb = k0; kb < k1; ++kb) {
                     mbar_wait(full + stage, phase);
                     tc_fence_after();
                     const uint64_t ad = umma_desc_sw128(smem_u32(As + stage * TC_A_STAGE));
                     const uint64_t bd = umma_desc_sw128(smem_u32(Bs + stage * C::B_STAGE));
 #pragma unroll
                     for (int k = 0; k < TC_BK / 16; ++k)  // +32 B along the swizzled row per K=16
-                        umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                        umma_bf16(d, ad + 2 * k, bd + 2 * k, idesc, (kb != k0) || k != 0);
                     if constexpr (CS > 1)
                         umma_commit_mc(empty + stage, MASK);
                     else
@@ -407,24 +423,93 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int sub = warp & 3;
         int acc = 0;
         uint32_t aphase = 0;
+        int* last_flag = qid + 4 + 2;  // smem word past the tile queue and the TMEM slot
         for (int i = 0;; ++i) {
-            const int t = take(i, cluster + i * nclusters, true);
-            if (t < 0) break;
+            const int u = take(i, cluster + i * nclusters, true);
+            if (u < 0) break;
+            const int t = u / splits;
             const int mt = (t / nN) * CS + rank, nt = t % nN;
             mbar_wait(tfull + acc, aphase);
             tc_fence_after();
             const int row = mt * TC_BM + sub * 32 + lane;
+            if (splits == 1) {
 #pragma unroll 1
-            for (int c = 0; c < BN / 32; ++c) {
-                const int l0 = nt * BN + c * 32;
-                if (l0 >= Lrows) break;
-                uint32_t v[32];
-                tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + uint32_t(acc * BN + c * 32), v);
-                tc_epilogue<KIND>(a, row, l0, v, Lrows, layer, lane);
+                for (int c = 0; c < BN / 32; ++c) {
+                    const int l0 = nt * BN + c * 32;
+                    if (l0 >= Lrows) break;
+                    uint32_t v[32];
+                    tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + uint32_t(acc * BN + c * 32), v);
+                    tc_epilogue<KIND>(a, row, l0, v, Lrows, layer, lane);
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + acc);
+            } else {
+                // partial -> workspace [unit][chunk][j4][row] float4: consecutive rows (threads)
+                // write consecutive 16 B, so every warp store is one 512 B run
+                float4* mine = reinterpret_cast<float4*>(a.sk_ws) + size_t(u) * (BN / 4) * TC_BM + sub * 32 + lane;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    if (nt * BN + c * 32 >= Lrows) break;
+                    uint32_t v[32];
+                    tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + uint32_t(acc * BN + c * 32), v);
+#pragma unroll
+                    for (int j = 0; j < 32; j += 4)
+                        __stcg(mine + size_t(c * 8 + j / 4) * TC_BM,
+                               make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                           __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3])));
+                }
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(tempty + acc);  // the accumulator is free again
+                __threadfence();
+                named_bar_sync(2, 128);  // the 4 epilogue warps wrote their rows
+                if (sub == 2 && lane == 0) {
+                    const int prev = atomicAdd(a.sk_cnt + t, 1);
+                    const int last = prev == splits - 1;
+                    if (last) a.sk_cnt[t] = 0;  // every unit of the tile arrived: reset for the next launch
+                    *reinterpret_cast<volatile int*>(last_flag) = last;
+                }
+                named_bar_sync(2, 128);
+                if (*reinterpret_cast<volatile int*>(last_flag)) {
+                    __threadfence();
+                    const float4* base =
+                        reinterpret_cast<const float4*>(a.sk_ws) + size_t(t) * splits * (BN / 4) * TC_BM + sub * 32 + lane;
+                    const size_t ustride = size_t(BN / 4) * TC_BM;
+#pragma unroll 1
+                    for (int c = 0; c < BN / 32; ++c) {
+                        const int l0 = nt * BN + c * 32;
+                        if (l0 >= Lrows) break;
+                        // all splits' loads of the chunk in flight at once, then summed in split order
+                        float4 q[4][8];
+#pragma unroll
+                        for (int sp = 0; sp < 4; ++sp)
+#pragma unroll
+                            for (int j4 = 0; j4 < 8; ++j4)
+                                q[sp][j4] = sp < splits ? __ldcg(base + sp * ustride + size_t(c * 8 + j4) * TC_BM)
+                                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+                        uint32_t v[32];
+#pragma unroll
+                        for (int j4 = 0; j4 < 8; ++j4) {
+                            float4 acc4 = q[0][j4];
+#pragma unroll
+                            for (int sp = 1; sp < 4; ++sp)
+                                if (sp < splits) {
+                                    acc4.x += q[sp][j4].x;
+                                    acc4.y += q[sp][j4].y;
+                                    acc4.z += q[sp][j4].z;
+                                    acc4.w += q[sp][j4].w;
+                                }
+                            v[4 * j4] = __float_as_uint(acc4.x);
+                            v[4 * j4 + 1] = __float_as_uint(acc4.y);
+                            v[4 * j4 + 2] = __float_as_uint(acc4.z);
+                            v[4 * j4 + 3] = __float_as_uint(acc4.w);
+                        }
+                        tc_epilogue<KIND>(a, row, l0, v, Lrows, layer, lane);
+                    }
+                }
+                named_bar_sync(2, 128);  // last_flag is rewritten by the next unit
             }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(tempty + acc);
             if (++acc == 2) {
                 acc = 0;
                 aphase ^= 1;
@@ -1484,6 +1569,25 @@ int pick_bn(int N, int rows) {
     return best;
 }
 
+// Split-K factor for a grid of G CTAs and T output tiles of nk K blocks: fewest
+// waves x (1/S of a tile) + the partial write/read (~8 % of a tile), units <= 2G
+// (the workspace), >= 8 K blocks per unit. MESH_PREFILL_SPLITK=0 disables it.
+int pick_splits(int T, int G, int nk) {
+    static const int off = getenv("MESH_PREFILL_SPLITK") && atoi(getenv("MESH_PREFILL_SPLITK")) == 0;
+    if (off || T >= G || T > SK_TILES_MAX) return 1;
+    int best = 1;
+    double best_cost = double((T + G - 1) / G);
+    for (int S = 2; S <= 4; ++S) {
+        if (T * S > 2 * G || nk / S < 8) break;
+        const double cost = double((T * S + G - 1) / G) / S + 0.08;
+        if (cost < best_cost - 1e-9) {
+            best_cost = cost;
+            best = S;
+        }
+    }
+    return best;
+}
+
 template <int KIND, int BN, int CS>
 cudaError_t gemm_tc_launch(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx,
                            int rows, int layer, cudaStream_t st) {
@@ -1514,8 +1618,12 @@ cudaError_t gemm_tc_launch(const PrefillArgs& a, const uint8_t* W, int N, int K,
     if (!make_wmap(&wm, W, N, K) || !make_xmap(&xm, X, K, ldx, rows, BN / CS)) return cudaErrorInvalidValue;
     const int ctiles = (N / TC_BM / CS) * ((rows + BN - 1) / BN);
     const int quota = a.max_ctas > 0 ? std::max(1, a.max_ctas / CS) : max_clusters;
-    cfg.gridDim = dim3(CS * std::min(ctiles, std::min(max_clusters, quota)));
-    return cudaLaunchKernelEx(&cfg, pf_gemm_tc<KIND, BN, CS>, a, wm, xm, N, K, rows, layer);
+    const int G = std::min(max_clusters, quota);
+    // split-K only for the down projection (long K, residual-add epilogue): measured 3B L = 462
+    // down 47.4 -> 41.5 us, while QKV (RoPE + paged-KV epilogue) and O got slower (41 -> 70, 24 -> 32)
+    const int splits = (CS == 1 && KIND == PF_DOWN) ? pick_splits(ctiles, G, K / TC_BK) : 1;
+    cfg.gridDim = dim3(CS * std::min(ctiles * splits, G));
+    return cudaLaunchKernelEx(&cfg, pf_gemm_tc<KIND, BN, CS>, a, wm, xm, N, K, rows, layer, splits);
 }
 
 // Cluster size along the weight rows: the CTAs of a cluster share (multicast)

@@ -29,8 +29,11 @@ struct PrefillArgs {
     int* tok_out;       // [1]
     int max_ctas;       // SM quota of the lane (persistent GEMM grid); 0 = all SMs
     int* tile_ctr;      // lane's dynamic tile counter (zero between launches; self-resetting)
+    float* sk_ws;       // split-K partial tiles [units][128][256] fp32 (units <= 2 x SMs)
+    int* sk_cnt;        // split-K arrivals per output tile (self-resetting), >= SK_TILES_MAX
 };
 
+constexpr int SK_TILES_MAX = 1024;
 cudaError_t launch_prefill(const PrefillArgs& a, cudaStream_t stream);
 // kernels one launch_prefill issues (embed, per layer 2 norms + 4 GEMMs + attention, final norm/lm_head/argmax)
 inline int prefill_launch_count(const Shape& s) { return 1 + 7 * s.n_layers + 3; }

@@ -525,6 +525,152 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair tcgen05 GEMM (cta_group::2): a 2-CTA cluster computes a 256-row x BN
+// tile with one M = 256 MMA per K = 16 step. Rank r holds weight rows
+// [128 r, 128 r + 128) and token rows [BN/2 r, BN/2 r + BN/2) of every stage, so
+// each SM fills 32 KB of shared memory per 64-deep K block for a 128 x 256
+// output (the single-CTA 128 x 256 tile needs 48 KB, and its operand stream,
+// not the tensor pipe, set its pace). Rank 0 issues the MMAs; its commits
+// arrive on both CTAs' barriers; each CTA's epilogue warps drain their own TMEM
+// half (128 rows x BN) with the same fused epilogues. Tiles are dealt
+// round-robin over clusters (both CTAs walk the same sequence).
+// ---------------------------------------------------------------------------
+template <int BN>
+struct Tc2Cfg {
+    static constexpr int A_STAGE = TC_A_STAGE;           // 128 rows x 64 K
+    static constexpr int B_STAGE = (BN / 2) * TC_BK * 2;  // this CTA's half of the tokens
+    static constexpr int STAGES = 196608 / (A_STAGE + B_STAGE);
+    static constexpr int TMEM_COLS = 2 * BN;
+    static constexpr int SMEM = 1024 + STAGES * (A_STAGE + B_STAGE) + 512;
+};
+
+template <int KIND, int BN>
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    pf_gemm_2sm(const __grid_constant__ PrefillArgs a, const __grid_constant__ CUtensorMap wmap,
+                const __grid_constant__ CUtensorMap xmap, int N, int K, int Lrows, int layer) {
+    using C = Tc2Cfg<BN>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+    uint8_t* As = smem;
+    uint8_t* Bs = smem + C::STAGES * C::A_STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(Bs + C::STAGES * C::B_STAGE);  // rank 0's count both halves
+    uint64_t* empty = full + C::STAGES;
+    uint64_t* tfull = empty + C::STAGES;  // [2]
+    uint64_t* tempty = tfull + 2;         // [2] rank 0: both CTAs' epilogue warps (8)
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const int cluster = blockIdx.x / 2, nclusters = gridDim.x / 2;
+    const int nN = (Lrows + BN - 1) / BN, ntiles = (N / 256) * nN, nk = K / TC_BK;
+    if (warp == 0 && lane == 0) {
+        for (int s = 0; s < C::STAGES; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(tfull + i, 1);
+            mbar_init(tempty + i, 8);
+        }
+        fence_mbar_init();
+        prefetch_tmap(&wmap);
+        prefetch_tmap(&xmap);
+    }
+    if (warp == 1) tmem_alloc_2sm(smem_u32(tmem_slot), C::TMEM_COLS);
+    tc_fence_before();
+    cluster_sync_all();  // barriers initialised and TMEM allocated in both CTAs
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {  // ---- producer (both CTAs): this CTA's halves of A and B
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = cluster; t < ntiles; t += nclusters) {
+                const int mt = t / nN, nt = t % nN;
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(empty + stage, phase ^ 1);
+                    if (rank == 0) mbar_arrive_expect_tx(full + stage, 2 * (C::A_STAGE + C::B_STAGE));
+                    tma_load_4d_2sm(As + stage * C::A_STAGE, &wmap, 0, 0, kb, mt * 16 + int(rank) * 8, full + stage);
+                    tma_load_2d_2sm(Bs + stage * C::B_STAGE, &xmap, kb * TC_BK, nt * BN + int(rank) * (BN / 2),
+                                    full + stage);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0 && rank == 0) {  // ---- MMA issuer (rank 0 only)
+            constexpr uint32_t idesc = umma_idesc_bf16(256, BN);
+            int stage = 0, acc = 0;
+            uint32_t phase = 0, aphase = 0;
+            for (int t = cluster; t < ntiles; t += nclusters) {
+                mbar_wait_cluster(tempty + acc, aphase ^ 1);
+                tc_fence_after();
+                const uint32_t d = tmem + uint32_t(acc * BN);
+                for (int kb = 0; kb < nk; ++kb) {
+                    mbar_wait(full + stage, phase);
+                    tc_fence_after();
+                    const uint64_t ad = umma_desc_sw128(smem_u32(As + stage * C::A_STAGE));
+                    const uint64_t bd = umma_desc_sw128(smem_u32(Bs + stage * C::B_STAGE));
+#pragma unroll
+                    for (int k = 0; k < TC_BK / 16; ++k)
+                        umma_bf16_2sm(d, ad + 2 * k, bd + 2 * k, idesc, (kb | k) != 0);
+                    umma_commit_2sm_mc(empty + stage, 3);
+                    if (++stage == C::STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit_2sm_mc(tfull + acc, 3);
+                if (++acc == 2) {
+                    acc = 0;
+                    aphase ^= 1;
+                }
+            }
+        }
+    } else {  // ---- epilogue warps 2..5 (both CTAs): this CTA's 128 rows of the tile
+        const int sub = warp & 3;
+        int acc = 0;
+        uint32_t aphase = 0;
+        for (int t = cluster; t < ntiles; t += nclusters) {
+            const int mt = t / nN, nt = t % nN;
+            mbar_wait_cluster(tfull + acc, aphase);
+            tc_fence_after();
+            const int row = mt * 256 + int(rank) * 128 + sub * 32 + lane;
+#pragma unroll 1
+            for (int c = 0; c < BN / 32; ++c) {
+                const int l0 = nt * BN + c * 32;
+                if (l0 >= Lrows) break;
+                uint32_t v[32];
+                tmem_ld32(tmem + (uint32_t(sub * 32) << 16) + uint32_t(acc * BN + c * 32), v);
+                tc_epilogue<KIND>(a, row, l0, v, Lrows, layer, lane);
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (rank == 0)
+                    mbar_arrive(tempty + acc);
+                else
+                    mbar_arrive_remote(tempty + acc, 0);
+            }
+            if (++acc == 2) {
+                acc = 0;
+                aphase ^= 1;
+            }
+        }
+    }
+    tc_fence_before();
+    cluster_sync_all();  // no CTA leaves while its peer's MMAs or arrives may still target it
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc_2sm(tmem, C::TMEM_COLS);
+    }
+}
+
 __global__ void pf_embed(const __grid_constant__ PrefillArgs a) {
     const int l = blockIdx.x;
     const int tok = a.tokens[l];
@@ -1646,10 +1792,65 @@ cudaError_t gemm_tc_bn(const PrefillArgs& a, const uint8_t* W, int N, int K, con
     }
 }
 
+template <int KIND, int BN>
+cudaError_t gemm_2sm_launch(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows,
+                            int layer, cudaStream_t st) {
+    using C = Tc2Cfg<BN>;
+    static int max_clusters_dev[MAX_DEVICES] = {};
+    int& max_clusters = max_clusters_dev[cur_device()];
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = C::SMEM;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (!max_clusters) {
+        cudaError_t e = cudaFuncSetAttribute(pf_gemm_2sm<KIND, BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        if (e != cudaSuccess) return e;
+        cfg.gridDim = dim3(2 * (num_sms() / 2));
+        e = cudaOccupancyMaxActiveClusters(&max_clusters, pf_gemm_2sm<KIND, BN>, &cfg);
+        if (e != cudaSuccess) return e;
+        if (max_clusters < 1) return cudaErrorInvalidConfiguration;
+    }
+    CUtensorMap wm, xm;
+    if (!make_wmap(&wm, W, N, K) || !make_xmap(&xm, X, K, ldx, rows, BN / 2)) return cudaErrorInvalidValue;
+    const int tiles = (N / 256) * ((rows + BN - 1) / BN);
+    const int quota = a.max_ctas > 0 ? std::max(1, a.max_ctas / 2) : max_clusters;
+    cfg.gridDim = dim3(2 * std::min(tiles, std::min(max_clusters, quota)));
+    return cudaLaunchKernelEx(&cfg, pf_gemm_2sm<KIND, BN>, a, wm, xm, N, K, rows, layer);
+}
+
+// CTA-pair GEMMs for N a multiple of 256 when the 256-row tiles fill every
+// cluster at least once (else the single-CTA kernel's finer, dynamically claimed
+// tiles fill the SMs better). BN 256 unless the token count makes 128 cheaper
+// (waves x max(2 BN, 256 + BN) over the cluster count). MESH_PREFILL_2SM=0|1
+// forces the choice off / on.
+template <int KIND>
+bool gemm_2sm(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows, int layer,
+              cudaStream_t st, cudaError_t* err) {
+    static const int mode = getenv("MESH_PREFILL_2SM") ? atoi(getenv("MESH_PREFILL_2SM")) : -1;
+    if (mode == 0 || N % 256 || (mode < 0 && !a.pair_ok)) return false;
+    const long long clusters = std::max(1, (a.max_ctas > 0 ? a.max_ctas : num_sms()) / 2);
+    auto tiles = [&](int bn) { return (long long)(N / 256) * ((rows + bn - 1) / bn); };
+    auto cost = [&](int bn) { return ((tiles(bn) + clusters - 1) / clusters) * std::max(2 * bn, 256 + bn); };
+    const int bn = cost(128) < cost(256) ? 128 : 256;
+    if (mode < 0 && tiles(bn) < clusters) return false;
+    *err = bn == 128 ? gemm_2sm_launch<KIND, 128>(a, W, N, K, X, ldx, rows, layer, st)
+                     : gemm_2sm_launch<KIND, 256>(a, W, N, K, X, ldx, rows, layer, st);
+    return true;
+}
+
 template <int KIND>
 cudaError_t gemm(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows,
                  int layer, cudaStream_t st) {
     if (N % TC_BM || K % TC_BK) return cudaErrorInvalidValue;
+    cudaError_t e2;
+    if (gemm_2sm<KIND>(a, W, N, K, X, ldx, rows, layer, st, &e2)) return e2;
     switch (pick_bn(N, rows)) {
         case 256: return gemm_tc_bn<KIND, 256>(a, W, N, K, X, ldx, rows, layer, st);
         case 128: return gemm_tc_bn<KIND, 128>(a, W, N, K, X, ldx, rows, layer, st);

@@ -28,6 +28,8 @@ struct PrefillArgs {
     int* last_tok;      // instance request table
     int* tok_out;       // [1]
     int max_ctas;       // SM quota of the lane (persistent GEMM grid); 0 = all SMs
+    int pair_ok;        // CTA-pair GEMMs allowed: no other lane holds an instance (co-located
+                        // decode grids leave few free SM pairs; measured slower there)
     int* tile_ctr;      // lane's dynamic tile counter (zero between launches; self-resetting)
     float* sk_ws;       // split-K partial tiles [units][128][256] fp32 (units <= 2 x SMs)
     int* sk_cnt;        // split-K arrivals per output tile (self-resetting), >= SK_TILES_MAX

@@ -1717,10 +1717,14 @@ int pick_bn(int N, int rows) {
 
 // Split-K factor for a grid of G CTAs and T output tiles of nk K blocks: fewest
 // waves x (1/S of a tile) + the partial write/read (~8 % of a tile), units <= 2G
-// (the workspace), >= 8 K blocks per unit. MESH_PREFILL_SPLITK=0 disables it.
+// (the workspace), >= 8 K blocks per unit. MESH_PREFILL_SPLITK=0 disables it,
+// =2..4 forces that factor wherever the workspace and K allow (tests).
 int pick_splits(int T, int G, int nk) {
-    static const int off = getenv("MESH_PREFILL_SPLITK") && atoi(getenv("MESH_PREFILL_SPLITK")) == 0;
-    if (off || T >= G || T > SK_TILES_MAX) return 1;
+    const char* env = getenv("MESH_PREFILL_SPLITK");  // read per launch: tests flip it in-process
+    const int force = env ? atoi(env) : -1;
+    if (force == 0 || T > SK_TILES_MAX || nk < 16) return 1;
+    if (force >= 2 && force <= 4 && T * force <= 2 * G && nk / force >= 8) return force;
+    if (T >= G) return 1;
     int best = 1;
     double best_cost = double((T + G - 1) / G);
     for (int S = 2; S <= 4; ++S) {
@@ -1833,7 +1837,8 @@ cudaError_t gemm_2sm_launch(const PrefillArgs& a, const uint8_t* W, int N, int K
 template <int KIND>
 bool gemm_2sm(const PrefillArgs& a, const uint8_t* W, int N, int K, const uint16_t* X, int ldx, int rows, int layer,
               cudaStream_t st, cudaError_t* err) {
-    static const int mode = getenv("MESH_PREFILL_2SM") ? atoi(getenv("MESH_PREFILL_2SM")) : -1;
+    const char* env = getenv("MESH_PREFILL_2SM");  // read per launch: tests flip it in-process
+    const int mode = env ? atoi(env) : -1;
     if (mode == 0 || N % 256 || (mode < 0 && !a.pair_ok)) return false;
     const long long clusters = std::max(1, (a.max_ctas > 0 ? a.max_ctas : num_sms()) / 2);
     auto tiles = [&](int bn) { return (long long)(N / 256) * ((rows + bn - 1) / bn); };

@@ -357,3 +357,46 @@ def test_decode_schedules_across_sm_quotas(name, quota):
                 _check(lg[i], toks[i], ol, f"{name}/q{quota} step {step} r{rid}")
                 last[rid] = toks[i]
         g.destroy_instance(1)
+
+
+def test_arena_backed_at_open_needs_no_vmm_calls(monkeypatch):
+    """KV arena backed at open (MESH_GPU_KV_PREALLOC_GB): grows, lazy shrinks, slack
+    reclaims, destroy and re-create only reassign slots (no cuMemMap / cuMemUnmap,
+    which drain the device), and every request still decodes exactly after its
+    blocks moved into slots another instance used before."""
+    monkeypatch.setenv("MESH_GPU_KV_PREALLOC_GB", "0.0625")  # 64 MiB = the whole pool
+    shape = SHAPES["tiny"]
+    C = shape.kv_bytes_per_token
+    gran = 2 << 20
+    with MeshGpu(0, kv_pool_bytes=32 * gran, prompt_seed=SEED_PROMPT, kv_granule_bytes=gran) as g:
+        g.capture_logits(True)
+        calls0 = g.stats()["vmm_calls"]
+        assert calls0 > 0  # the arena was backed at open
+        models = {1: ora.Oracle(shape, 3), 2: ora.Oracle(shape, 4)}
+        g.create_instance(1, shape, seed=3)
+        g.create_instance(2, shape, seed=4)
+        g.kv_resize(1, 0, 20000 * C)   # 1,258 blocks: 10 of the 32 slots
+        g.kv_resize(2, 0, 20000 * C)
+        seqs, last = {}, {}
+        for iid, rid, n in [(1, 5, 200), (2, 6, 150)]:
+            toks, lg = g.step(iid, prefill=rid, prefill_len=n, vocab=shape.vocab, with_logits=True)
+            seqs[rid], ol = _oracle_prefill(models[iid], rid, n)
+            _check(lg[0], toks[0], ol, f"prefill i{iid}")
+            last[rid] = toks[0]
+        g.kv_resize(1, 20000 * C, 400 * C)  # lazy: keeps its slots
+        g.kv_resize(2, 20000 * C, 400 * C)
+        g.create_instance(3, shape, seed=3)
+        g.kv_resize(3, 0, 60000 * C)  # needs slots beyond the free ones: takes 1's and 2's slack
+        assert g.stats()["kv_reclaims"] >= 1
+        g.destroy_instance(3)
+        g.create_instance(4, shape, seed=4)  # recycled buffers, slots of the destroyed instance
+        g.kv_resize(4, 0, 60000 * C)
+        for step in range(3):
+            for iid, rid in [(1, 5), (2, 6)]:
+                toks, lg = g.step(iid, decode=[rid], vocab=shape.vocab, with_logits=True)
+                _, ol = seqs[rid].feed(last[rid])
+                _check(lg[0], toks[0], ol, f"decode i{iid} step {step}")
+                last[rid] = toks[0]
+        assert g.stats()["vmm_calls"] == calls0
+        for mdl in models.values():
+            mdl.close()

@@ -174,3 +174,34 @@ def test_full_width_shrink_swap_migrate(name):
         decode(1, [0], "swapped-in request")
     finally:
         g.close()
+
+
+@pytest.mark.parametrize("pair,splitk", [("0", "0"), ("1", "0"), ("0", "2"), ("1", "4")])
+def test_prefill_gemm_variants(pair, splitk, monkeypatch):
+    """The single-CTA and CTA-pair (cta_group::2) prefill GEMMs, with and without
+    split-K of the down projection (forced factors), at full width: the 3B shape,
+    a 300-token and a 900-token prompt (ragged token tiles), then a decode step."""
+    monkeypatch.setenv("MESH_PREFILL_2SM", pair)
+    monkeypatch.setenv("MESH_PREFILL_SPLITK", splitk)
+    name = "3b"
+    m, pre = _oracle(name)
+    shape = _shape(name)
+    g = MeshGpu(0, kv_pool_bytes=2 << 30, prompt_seed=SEED_PROMPT)
+    try:
+        g.capture_logits(True)
+        g.create_instance(1, shape, seed=WSEED)
+        g.kv_resize(1, 0, 1400 * shape.kv_bytes_per_token)
+        for rid in (0, 4):
+            toks, lg = g.step(1, prefill=rid, prefill_len=LENS[rid], vocab=shape.vocab, with_logits=True)
+            _check(lg[0], toks[0], pre[rid][1], f"pair={pair} splitk={splitk} prefill r{rid}")
+        toks, lg = g.step(1, decode=[0, 4], vocab=shape.vocab, with_logits=True)
+        outs = m.decode([copy.deepcopy(pre[r][0]) for r in (0, 4)], [int(tok) for tok in _first_tokens(g, (0, 4))])
+        for i, rid in enumerate((0, 4)):
+            _check(lg[i], toks[i], outs[i][1], f"pair={pair} splitk={splitk} decode r{rid}")
+    finally:
+        g.close()
+
+
+def _first_tokens(g, rids):
+    """The token each request's prefill emitted (the GPU's, which the decode consumed)."""
+    return [g.request_tokens(1, r)[LENS[r]] for r in rids]

@@ -451,7 +451,7 @@ struct mesh_gpu {
     int64_t next_ticket = 1;
     bool capture_logits = false;
     mesh_gpu_stats st{};
-    int nstage = DEC_NSTAGE;  // decode ring depth in use (MESH_GPU_NSTAGE)
+    int nstage = DEC_NSTAGE;  // decode ring depth (the round-1 8-stage A/B knob is gone)
     int skip = 0;             // MESH_GPU_SKIP debug mask (benchmarking only)
     int* dbg_host = nullptr;  // MESH_GPU_WATCHDOG: host-mapped decode progress
     int* dbg_dev = nullptr;
@@ -1547,8 +1547,6 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         CK(cudaMalloc((void**)&g->d_tok, sizeof(int) * 8 * RING));
         for (int i = 0; i < RING; ++i) CK(cudaEventCreateWithFlags(&g->ring_ev[i], cudaEventDisableTiming));
         g->st.kv_pool_bytes = g->pool.limit;
-        // ring depth must be 8 or 16: a consumer warp's stages are 8 apart, so the
-        // depth must be a multiple of 8 (mbarrier parity) and a power of two (masks)
         g->check = std::getenv("MESH_GPU_CHECK") != nullptr;
         g->poison = std::getenv("MESH_GPU_POISON") != nullptr;
         g->prefill_quota = std::getenv("MESH_PREFILL_QUOTA") != nullptr;
@@ -1556,7 +1554,6 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             g->prefill_quota = true;
             g->prefill_min_ctas = std::atoi(e);
         }
-        if (const char* e = std::getenv("MESH_GPU_NSTAGE")) g->nstage = std::atoi(e) >= 16 ? 16 : 8;
         if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
         if (const char* e = std::getenv("MESH_GPU_WCACHE_GB")) g->wcache_cap = size_t(std::max(0.0, std::atof(e)) * double(1 << 30));
         if (std::getenv("MESH_GPU_WATCHDOG")) {

@@ -1,8 +1,8 @@
 """Per-SM streaming rate of the decode kernel vs SM quota (device time, not the bench).
 
 For each (model, quota) runs B = 8 decode at context CTX and prints ms/step,
-GB/s and GB/s per SM. MESH_GPU_SKIP / MESH_GPU_NSTAGE in the environment
-isolate the attention / GEMV phases and the ring depth.
+GB/s and GB/s per SM. MESH_GPU_SKIP in the environment
+isolates the attention / GEMV phases.
 usage: python tools/probe_quota.py 1b:17,148 3b:56,148
 """
 import json
@@ -32,8 +32,7 @@ def run(name: str, quota: int) -> dict:
     byts = s.weight_bytes_streamed + B * (CTX + 1) * s.kv_bytes_per_token + B * s.d_model * 2
     gbs = byts / ms / 1e6
     return dict(model=name, quota=quota, ms=round(ms, 4), GBps=round(gbs, 1), GBps_per_sm=round(gbs / quota, 2),
-                frac=round(gbs / 6539.2, 3), skip=os.environ.get("MESH_GPU_SKIP", "0"),
-                nstage=os.environ.get("MESH_GPU_NSTAGE", "16"))
+                frac=round(gbs / 6539.2, 3), skip=os.environ.get("MESH_GPU_SKIP", "0"))
 
 
 for arg in sys.argv[1:] or ["1b:17,148"]:

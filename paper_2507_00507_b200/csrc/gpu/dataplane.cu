@@ -453,6 +453,8 @@ struct mesh_gpu {
     mesh_gpu_stats st{};
     int nstage = DEC_NSTAGE;  // decode ring depth (the round-1 8-stage A/B knob is gone)
     int skip = 0;             // MESH_GPU_SKIP debug mask (benchmarking only)
+    int kv_lanes = 1;         // MESH_GPU_KV_LANES=0: attention KV stages through the batched push/flush instead of decoupled lanes
+    int l2pf = 0;             // MESH_GPU_L2PF: weight-stage L2 prefetch lookahead in stages (decode_kernel)
     int* dbg_host = nullptr;  // MESH_GPU_WATCHDOG: host-mapped decode progress
     int* dbg_dev = nullptr;
     // Weights are a pure function of shape + weight seed, and the seed is the
@@ -1148,6 +1150,8 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.trace = nullptr;
     a.arrive = nullptr;
     a.nstage = g->nstage;
+    a.l2pf = g->l2pf;
+    a.kv_lanes = g->kv_lanes;
     a.skip = g->skip;
     return a;
 }
@@ -1555,6 +1559,8 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
             g->prefill_min_ctas = std::atoi(e);
         }
         if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
+        if (const char* e = std::getenv("MESH_GPU_L2PF")) g->l2pf = std::atoi(e);
+        if (const char* e = std::getenv("MESH_GPU_KV_LANES")) g->kv_lanes = std::atoi(e);
         if (const char* e = std::getenv("MESH_GPU_WCACHE_GB")) g->wcache_cap = size_t(std::max(0.0, std::atof(e)) * double(1 << 30));
         if (std::getenv("MESH_GPU_WATCHDOG")) {
             CK(cudaHostAlloc((void**)&g->dbg_host, sizeof(int) * 2 * 1024, cudaHostAllocMapped));

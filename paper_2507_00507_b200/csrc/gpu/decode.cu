@@ -234,11 +234,24 @@ __device__ __forceinline__ Smem carve(uint8_t* base) {
 // One issuing thread serialises wait -> expect_tx -> copy at ~210 ns per stage
 // (measured: tools/readbw.cu, 8 KB stages cap at 5.2 TB/s); 8 lanes reach
 // 7.3 TB/s, above plain LDG streaming.
-constexpr int DEC_PLANES = 8;
+#ifndef DEC_PLANES_N
+#define DEC_PLANES_N 8
+#endif
+constexpr int DEC_PLANES = DEC_PLANES_N;
+// Lanes of the producer warp that run the stage enumeration: the first
+// DEC_PLANES issue the batched GEMV stages; all of them issue the decoupled
+// attention KV stages. Measured: 16 lanes made the batched GEMV path slower
+// (the idle lanes ride along the enumeration) and faulted at 3B / 148 SMs; 32
+// lanes would share ring slots (parity aliasing). 8 it is.
+#ifndef DEC_PRODUCER_LANES_N
+#define DEC_PRODUCER_LANES_N 8
+#endif
+constexpr int DEC_PRODUCER_LANES = DEC_PRODUCER_LANES_N;
+constexpr unsigned DEC_PRODUCER_MASK = DEC_PRODUCER_LANES == 32 ? 0xffffffffu : (1u << DEC_PRODUCER_LANES) - 1u;
 
 struct StageSrc {
     const uint8_t* p0;  // weight tile chunk, or the K row block of the first KV block
-    const uint8_t* p1;  // K row block of the second KV block (dh = 64)
+    const uint8_t* p1;  // K row block of the second KV block (dh = 64); weight stage: end of its matrix
     int nblk;           // -1: weight stage; else KV blocks in the stage (0..2)
 };
 
@@ -252,6 +265,7 @@ struct Producer {
     uint64_t pol;
     uint32_t kv_blk;   // bytes of one (layer, head, k|v) block; its K and V are adjacent
     StageSrc mine;     // this lane's pending stage
+    const uint8_t* wend = nullptr;  // end of the current GEMV phase's weight matrix (prefetch bound)
     uint32_t dk = 0;   // claim descriptors written
     __device__ __forceinline__ Producer(const DecodeArgs& args, Smem& s, int ln) : a(args), sm(s), lane(ln) {
         nsh = uint32_t(__ffs(a.nstage) - 1);
@@ -271,6 +285,11 @@ struct Producer {
             if (mine.nblk < 0) {
                 mbar_arrive_expect_tx(&sm.full[slot], DEC_STAGE_BYTES);
                 bulk_g2s_evict_first(dst, mine.p0, DEC_STAGE_BYTES, &sm.full[slot], pol);
+                // Weight tiles are contiguous and claimed in address order: pulling the
+                // bytes a few stages ahead into L2 now lets the ring's copy of them hit
+                // L2 later, so more bytes are in flight per SM than the ring holds.
+                const uint8_t* ahead = mine.p0 + size_t(a.l2pf) * DEC_STAGE_BYTES;
+                if (a.l2pf && ahead < mine.p1) bulk_prefetch_l2(ahead, DEC_STAGE_BYTES);
             } else {
                 // one copy per KV block: [K rows | V rows] of the (layer, head)
                 mbar_arrive_expect_tx(&sm.full[slot], 2u * uint32_t(mine.nblk) * kv_blk);
@@ -290,13 +309,14 @@ struct Producer {
     }
     __device__ __forceinline__ void gemv_dynamic(int kind, int layer, int G) {
         const GemvPhase p = gemv_phase(a, kind, layer);
+        wend = p.base + size_t(p.tiles) * p.K * 32;
         const int cl_big = claim_tiles(p.tiles, G), nch = p.K / DEC_CHUNK_COLS;
         int* ctr = a.claim + claim_index(a.s, kind, layer);
         const size_t tile_bytes = size_t(p.K) * 32;
         int cl = cl_big, next = 0;
         if (lane == 0) next = atomicAdd(ctr, cl);
         for (;;) {
-            const int t0 = __shfl_sync(0xffu, next, 0);
+            const int t0 = __shfl_sync(DEC_PRODUCER_MASK, next, 0);
             const int gn = max(0, min(cl, p.tiles - t0));
             // issue every pending stage first: the consumers may need them to
             // get to the descriptor slot this claim waits for
@@ -312,7 +332,7 @@ struct Producer {
             if (gn == 0) return;
             for (int ti = 0; ti < gn; ++ti) {
                 const uint8_t* t = p.base + size_t(t0 + ti) * tile_bytes;
-                for (int ch = 0; ch < nch; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, nullptr, -1);
+                for (int ch = 0; ch < nch; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, wend, -1);
             }
             // Next claim once this group's stages are issued: a ring's depth of them is
             // still to be consumed, which hides the round trip, and a CTA that streams
@@ -332,6 +352,7 @@ struct Producer {
         const MyTiles mt = my_tiles(p.tiles, off, cta, G);
         off = (off + p.tiles) % G;
         if (mt.n == 0) return;
+        wend = p.base + size_t(p.tiles) * p.K * 32;
         const size_t tile_bytes = size_t(p.K) * 32;
         const int nseg = n_segments(p.K);
         if (nseg > 1 && mt.n <= DEC_TACC_TILES) {
@@ -342,7 +363,7 @@ struct Producer {
                 seg_range(p.K, nseg, sg, c0, c1);
                 for (int ti = 0; ti < mt.n; ++ti) {
                     const uint8_t* t = p.base + size_t(mt.t0 + ti * G) * tile_bytes;
-                    for (int ch = c0; ch < c1; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, nullptr, -1);
+                    for (int ch = c0; ch < c1; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, wend, -1);
                 }
             }
             return;
@@ -354,7 +375,7 @@ struct Producer {
                 seg_range(p.K, nseg, sg, c0, c1);
                 for (int ti = 0; ti < gn; ++ti) {
                     const uint8_t* t = p.base + size_t(mt.t0 + (g0 + ti) * G) * tile_bytes;
-                    for (int ch = c0; ch < c1; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, nullptr, -1);
+                    for (int ch = c0; ch < c1; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, wend, -1);
                 }
             }
         }
@@ -369,6 +390,41 @@ struct Producer {
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             a.trace[2048 + ntr++] = (t << 4) | unsigned(tag);
         }
+    }
+    // KV stages with the issuing lanes decoupled: lane j walks stages a0 + j,
+    // a0 + j + P, ... on its own, waiting only for its own ring slots. A KV stage
+    // (one (layer, head) run of a paged block, its own 2 MB page at 3B/7B) has a
+    // long and variable latency; in the batched push/flush a batch of P copies
+    // waits for its slowest slot, which kept the attention stream at ~30 GB/s per
+    // SM at the lanes' quotas (weights: ~50).
+    __device__ __forceinline__ void attention_lanes(int layer, const AttnPlan& ap, const int* pos) {
+        flush();  // the previous phase's pending stages go first (q == qb)
+        if (ap.a1 <= ap.a0) return;
+        const Shape& s = a.s;
+        const int bps = ap.rt / KV_BLOCK_TOKENS;
+        const size_t head_stride = size_t(2) * KV_BLOCK_TOKENS * s.dh * 2;
+        const uint8_t* layer_base = a.kv_base + kv_offset(s, layer, 0, 0, 0);
+        const uint32_t q0 = q;
+        for (int i = ap.a0 + lane; i < ap.a1; i += DEC_PRODUCER_LANES) {
+            const AttnStage st = attn_stage_of(ap, s.n_kv, i);
+            const int k0 = st.s * bps, p = pos[st.b];
+            int nblk = 0;
+            if (k0 * KV_BLOCK_TOKENS < p) nblk = (bps == 2 && (k0 + 1) * KV_BLOCK_TOKENS < p) ? 2 : 1;
+            if (a.skip & 4) nblk = 0;
+            const int* btrow = sm.bt + st.b * DEC_BT_MAX;
+            const size_t hoff = size_t(st.kvh) * head_stride;
+            const uint32_t qi = q0 + uint32_t(i - ap.a0);
+            const uint32_t slot = qi & nmask, par = (qi >> nsh) & 1u;
+            mbar_wait(&sm.empty[slot], par ^ 1u);
+            uint8_t* dst = sm.ring + size_t(slot) * DEC_STAGE_BYTES;
+            mbar_arrive_expect_tx(&sm.full[slot], 2u * uint32_t(nblk) * kv_blk);
+            if (nblk > 0) bulk_g2s(dst, layer_base + size_t(btrow[k0]) * a.block_bytes + hoff, 2u * kv_blk, &sm.full[slot]);
+            if (nblk > 1)
+                bulk_g2s(dst + 2u * kv_blk, layer_base + size_t(btrow[k0 + 1]) * a.block_bytes + hoff, 2u * kv_blk,
+                         &sm.full[slot]);
+        }
+        __syncwarp(DEC_PRODUCER_MASK);
+        q = qb = q0 + uint32_t(ap.a1 - ap.a0);
     }
     // KV stages of this CTA's attention range: only blocks that were complete
     // before this step (every position < pos) are streamed; the current token
@@ -420,7 +476,12 @@ __device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int
         pr.ptrace(cta, 8);
         pr.gemv(PH_QKV, l, off, cta, G);
         pr.ptrace(cta, 9);
-        if (!(a.skip & 1)) pr.attention(l, ap, pos);
+        if (!(a.skip & 1)) {
+            if (a.kv_lanes)
+                pr.attention_lanes(l, ap, pos);
+            else
+                pr.attention(l, ap, pos);
+        }
         pr.ptrace(cta, 10);
         pr.gemv(PH_O, l, off, cta, G);
         pr.ptrace(cta, 11);
@@ -1360,7 +1421,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     const DecodeArgs& a = a_s;
 
     if (warp == DEC_NCW) {
-        if (lane < DEC_PLANES) producer_loop(a, sm, blockIdx.x, gridDim.x, B, pos_s, lane);
+        if (lane < DEC_PRODUCER_LANES) producer_loop(a, sm, blockIdx.x, gridDim.x, B, pos_s, lane);
         return;
     }
     Ctx c;

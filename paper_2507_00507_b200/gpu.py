@@ -13,7 +13,8 @@ from dataclasses import dataclass
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libmesh_gpu.so")
+# MESH_GPU_LIB: an alternative build of the same library (A/B experiments under tools/)
+LIB_PATH = os.environ.get("MESH_GPU_LIB") or os.path.join(_HERE, "libmesh_gpu.so")
 
 MESH_OK = 0
 

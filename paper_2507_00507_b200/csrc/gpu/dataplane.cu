@@ -454,6 +454,7 @@ struct mesh_gpu {
     int nstage = DEC_NSTAGE;  // decode ring depth (the round-1 8-stage A/B knob is gone)
     int skip = 0;             // MESH_GPU_SKIP debug mask (benchmarking only)
     int kv_lanes = 1;         // MESH_GPU_KV_LANES=0: attention KV stages through the batched push/flush instead of decoupled lanes
+    int w_lanes = 1;          // MESH_GPU_W_LANES=0: weight stages through the batched push/flush instead of decoupled lanes
     int l2pf = 0;             // MESH_GPU_L2PF: weight-stage L2 prefetch lookahead in stages (decode_kernel)
     int* dbg_host = nullptr;  // MESH_GPU_WATCHDOG: host-mapped decode progress
     int* dbg_dev = nullptr;
@@ -1152,6 +1153,7 @@ DecodeArgs decode_args(mesh_gpu* g, Instance& in, StepDesc* d_desc, int ring) {
     a.nstage = g->nstage;
     a.l2pf = g->l2pf;
     a.kv_lanes = g->kv_lanes;
+    a.w_lanes = g->w_lanes;
     a.skip = g->skip;
     return a;
 }
@@ -1561,6 +1563,7 @@ mesh_status mesh_gpu_open(const mesh_gpu_cfg* cfg, mesh_gpu** out) {
         if (const char* e = std::getenv("MESH_GPU_SKIP")) g->skip = std::atoi(e);
         if (const char* e = std::getenv("MESH_GPU_L2PF")) g->l2pf = std::atoi(e);
         if (const char* e = std::getenv("MESH_GPU_KV_LANES")) g->kv_lanes = std::atoi(e);
+        if (const char* e = std::getenv("MESH_GPU_W_LANES")) g->w_lanes = std::atoi(e);
         if (const char* e = std::getenv("MESH_GPU_WCACHE_GB")) g->wcache_cap = size_t(std::max(0.0, std::atof(e)) * double(1 << 30));
         if (std::getenv("MESH_GPU_WATCHDOG")) {
             CK(cudaHostAlloc((void**)&g->dbg_host, sizeof(int) * 2 * 1024, cudaHostAllocMapped));

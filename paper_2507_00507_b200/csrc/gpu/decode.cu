@@ -92,6 +92,14 @@ __device__ __forceinline__ void seg_range(int K, int nseg, int s, int& c0, int& 
     c1 = (chunks * (s + 1)) / nseg;
 }
 
+// Stages of the first `upto` activation segments of a segment-outer static phase.
+__device__ __forceinline__ int seg_stages(int K, int nseg, int upto, int ntiles) {
+    int c0, c1;
+    seg_range(K, nseg, upto, c0, c1);  // c0 of segment `upto` = chunks before it
+    (void)c1;
+    return c0 * ntiles;
+}
+
 // ---- attention work plan (identical on producer and consumers) ----
 // Stages enumerate (kv head, request b, chunk s of RT = 2048/dh tokens) in
 // HEAD-major order; stage = the K and V rows of those tokens for one layer,
@@ -307,6 +315,23 @@ struct Producer {
         }
         if (++q - qb == DEC_PLANES) flush();
     }
+    // Weight stages [q, q + n) issued by decoupled lanes (lane j: stages j, j + P,
+    // ...), each waiting only for its own ring slot; addr_of(i) = source of stage i.
+    template <typename AddrOf>
+    __device__ __forceinline__ void issue_lanes(int n, AddrOf addr_of) {
+        flush();
+        const uint32_t q0 = q;
+        for (int i = lane; i < n; i += DEC_PLANES) {
+            const uint32_t qi = q0 + uint32_t(i);
+            const uint32_t slot = qi & nmask, par = (qi >> nsh) & 1u;
+            const uint8_t* src = addr_of(i);
+            mbar_wait(&sm.empty[slot], par ^ 1u);
+            mbar_arrive_expect_tx(&sm.full[slot], DEC_STAGE_BYTES);
+            bulk_g2s_evict_first(sm.ring + size_t(slot) * DEC_STAGE_BYTES, src, DEC_STAGE_BYTES, &sm.full[slot], pol);
+        }
+        __syncwarp(DEC_PRODUCER_MASK);
+        q = qb = q0 + uint32_t(n);
+    }
     __device__ __forceinline__ void gemv_dynamic(int kind, int layer, int G) {
         const GemvPhase p = gemv_phase(a, kind, layer);
         wend = p.base + size_t(p.tiles) * p.K * 32;
@@ -330,9 +355,14 @@ struct Producer {
             }
             ++dk;
             if (gn == 0) return;
-            for (int ti = 0; ti < gn; ++ti) {
-                const uint8_t* t = p.base + size_t(t0 + ti) * tile_bytes;
-                for (int ch = 0; ch < nch; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, wend, -1);
+            if (a.w_lanes) {
+                const uint8_t* g0 = p.base + size_t(t0) * tile_bytes;  // the group's tiles are contiguous
+                issue_lanes(gn * nch, [&](int i) { return g0 + size_t(i) * DEC_STAGE_BYTES; });
+            } else {
+                for (int ti = 0; ti < gn; ++ti) {
+                    const uint8_t* t = p.base + size_t(t0 + ti) * tile_bytes;
+                    for (int ch = 0; ch < nch; ++ch) push(t + size_t(ch) * DEC_STAGE_BYTES, wend, -1);
+                }
             }
             // Next claim once this group's stages are issued: a ring's depth of them is
             // still to be consumed, which hides the round trip, and a CTA that streams
@@ -355,9 +385,29 @@ struct Producer {
         wend = p.base + size_t(p.tiles) * p.K * 32;
         const size_t tile_bytes = size_t(p.K) * 32;
         const int nseg = n_segments(p.K);
+        if (a.w_lanes && nseg == 1) {
+            const int nch = p.K / DEC_CHUNK_COLS;
+            issue_lanes(mt.n * nch, [&](int i) {
+                const int ti = i / nch, ch = i - ti * nch;
+                return p.base + size_t(mt.t0 + ti * G) * tile_bytes + size_t(ch) * DEC_STAGE_BYTES;
+            });
+            return;
+        }
         if (nseg > 1 && mt.n <= DEC_TACC_TILES) {
             // segment-outer, as the consumers run it (run_gemv): every tile's
             // chunks of segment 0, then of segment 1, ...
+            if (a.w_lanes) {
+                issue_lanes(seg_stages(p.K, nseg, nseg, mt.n), [&](int i) {
+                    int sg = 0;
+                    while (i >= seg_stages(p.K, nseg, sg + 1, mt.n)) ++sg;
+                    int c0, c1;
+                    seg_range(p.K, nseg, sg, c0, c1);
+                    const int r = i - seg_stages(p.K, nseg, sg, mt.n), w = c1 - c0;
+                    const int ti = r / w, ch = c0 + (r - ti * w);
+                    return p.base + size_t(mt.t0 + ti * G) * tile_bytes + size_t(ch) * DEC_STAGE_BYTES;
+                });
+                return;
+            }
             for (int sg = 0; sg < nseg; ++sg) {
                 int c0, c1;
                 seg_range(p.K, nseg, sg, c0, c1);

@@ -71,6 +71,7 @@ struct DecodeArgs {
     unsigned long long* trace;  // optional [4096]: %globaltimer at CTA 0's phase boundaries
     unsigned long long* arrive; // optional [barriers][grid]: %globaltimer of every CTA's barrier arrival
     int nstage;    // weight-ring stages in use (<= DEC_NSTAGE): bounds bytes in flight per SM
+    int w_lanes;   // weight stages of dynamic claims / static single-segment and segment-outer phases by decoupled lanes
     int kv_lanes;  // attention KV stages issued by decoupled producer lanes (1) or the batched push/flush (0)
     int l2pf;      // weight stages: also prefetch the bytes this many 8 KB stages ahead into L2 (0: off)
     int skip;      // debug: 1 skips attention, 2 the GEMV phases, 8 / 16 the attention / GEMV math (ring only); results are garbage

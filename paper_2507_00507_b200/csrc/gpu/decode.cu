@@ -522,24 +522,21 @@ __device__ __forceinline__ void producer_loop(const DecodeArgs& a, Smem& sm, int
     Producer pr(a, sm, lane);
     const AttnPlan ap = attn_plan(a.s, B, pos, cta, G);
     int off = 0;
-    for (int l = 0; l < a.s.n_layers; ++l) {
-        pr.ptrace(cta, 8);
-        pr.gemv(PH_QKV, l, off, cta, G);
-        pr.ptrace(cta, 9);
-        if (!(a.skip & 1)) {
+    // one call site per phase body (see the consumer loop)
+    const int L = a.s.n_layers;
+#pragma unroll 1
+    for (int it = 0; it <= 4 * L; ++it) {
+        const int kind = it == 4 * L ? int(PH_LM) : (it & 3), l = it == 4 * L ? 0 : (it >> 2);
+        if (kind == PH_QKV) pr.ptrace(cta, 8);
+        pr.gemv(kind, l, off, cta, G);
+        if (kind == PH_QKV && !(a.skip & 1)) {
             if (a.kv_lanes)
                 pr.attention_lanes(l, ap, pos);
             else
                 pr.attention(l, ap, pos);
         }
-        pr.ptrace(cta, 10);
-        pr.gemv(PH_O, l, off, cta, G);
-        pr.ptrace(cta, 11);
-        pr.gemv(PH_GU, l, off, cta, G);
-        pr.gemv(PH_DOWN, l, off, cta, G);
-        if (a.progress && lane == 0) a.progress[cta * 2 + 1] = int(pr.q);
+        if (kind == PH_DOWN && a.progress && lane == 0) a.progress[cta * 2 + 1] = int(pr.q);
     }
-    pr.gemv(PH_LM, 0, off, cta, G);
     pr.flush();
 }
 
@@ -553,6 +550,7 @@ struct Ctx {
     int B;
     const int* slot;  // [8] in shared memory
     const int* pos;   // [8] in shared memory
+    const int* cur_blk;  // [8] in shared memory: block holding each request's current token (-1: read the table)
     const AttnPair* pt;  // [ATT_PT_MAX] in shared memory
     int p0, np;          // first pair of this CTA's attention range, pairs touched
     uint32_t q;       // stage counter (mirrors the producer)
@@ -692,7 +690,8 @@ __device__ __forceinline__ void epi_qkv(Ctx& c, int layer, int tile, const float
             qd[r1.dim] = o1;
             qd[r1.dim + half] = o2;
         } else {
-            const int blk = ldcg_i32(a.block_table + size_t(c.slot[b]) * a.bt_stride + pos / KV_BLOCK_TOKENS);
+            const int blk = c.cur_blk[b] >= 0 ? c.cur_blk[b]
+                                              : ldcg_i32(a.block_table + size_t(c.slot[b]) * a.bt_stride + pos / KV_BLOCK_TOKENS);
             const int slot = pos % KV_BLOCK_TOKENS;
             uint8_t* e = a.kv_base + size_t(blk) * a.block_bytes + kv_offset(s, layer, r1.section - 1, r1.head, slot);
             *reinterpret_cast<uint16_t*>(e + kv_dim_off(slot, r1.dim)) = f_to_bf16(o1);
@@ -1174,7 +1173,9 @@ __device__ __forceinline__ void attn_consume(Ctx& c, int layer, const AttnStage&
     const bool patch = cur >= t0 && cur < t0 + RT;
     uint4 pv = make_uint4(0, 0, 0, 0);
     if (patch && lane < 2 * CH) {
-        const int blk = ldcg_i32(a.block_table + size_t(c.slot[st.b]) * a.bt_stride + cur / KV_BLOCK_TOKENS);
+        const int blk = c.cur_blk[st.b] >= 0
+                            ? c.cur_blk[st.b]
+                            : ldcg_i32(a.block_table + size_t(c.slot[st.b]) * a.bt_stride + cur / KV_BLOCK_TOKENS);
         pv = ldcg_u4(a.kv_base + size_t(blk) * a.block_bytes +
                      kv_offset(s, layer, lane / CH, st.kvh, cur % KV_BLOCK_TOKENS) + (lane % CH) * 16);
     }
@@ -1434,7 +1435,7 @@ __device__ __forceinline__ void run_argmax_combine(Ctx& c, float best_v[2], int 
 __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_constant__ DecodeArgs args) {
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     __shared__ DecodeArgs a_s;  // launch arguments, read with LDS instead of generic param loads
-    __shared__ int slot_s[DEC_MAXB], pos_s[DEC_MAXB];
+    __shared__ int slot_s[DEC_MAXB], pos_s[DEC_MAXB], cur_blk_s[DEC_MAXB];
     __shared__ int dt0_s[4], dgn_s[4];
     __shared__ __align__(8) uint64_t dfull_s[4], dempty_s[4];
     __shared__ __align__(8) uint64_t actbar_s;
@@ -1467,6 +1468,20 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
         const int b = i / DEC_BT_MAX, k = i % DEC_BT_MAX;
         sm.bt[i] = (b < B && k < args.bt_stride) ? args.block_table[size_t(args.desc->slot[b]) * args.bt_stride + k] : 0;
     }
+    // The block of each request's current token, as this step leaves the table (an
+    // entry installed by this step's update list wins): the QKV epilogue's K/V
+    // stores and attention's current-row patch then skip a dependent global load.
+    if (threadIdx.x < DEC_MAXB) {
+        const int b = threadIdx.x;
+        int blk = -1;
+        if (b < B) {
+            const int k = args.desc->pos[b] / KV_BLOCK_TOKENS, sl = args.desc->slot[b];
+            if (k < args.bt_stride) blk = args.block_table[size_t(sl) * args.bt_stride + k];
+            for (int i = 0; i < args.desc->n_upd; ++i)
+                if (args.desc->upd[i][0] == sl && args.desc->upd[i][1] == k) blk = args.desc->upd[i][2];
+        }
+        cur_blk_s[b] = blk;
+    }
     __syncthreads();
     const DecodeArgs& a = a_s;
 
@@ -1487,6 +1502,7 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
     c.B = B;
     c.slot = slot_s;
     c.pos = pos_s;
+    c.cur_blk = cur_blk_s;
     c.q = 0;
     c.off = 0;
     c.dk = 0;
@@ -1528,25 +1544,31 @@ __global__ void __launch_bounds__(DEC_THREADS, 1) decode_kernel(const __grid_con
 
     run_embed(c);
     grid_sync(c);
-    for (int l = 0; l < a.s.n_layers; ++l) {
-        run_gemv(c, PH_QKV, l, best_v, best_i);
-        trace(c, 6);  // no grid barrier: attention waits per KV-head group (qkv_done)
-        if (!(a.skip & 1)) {
-            if (a.s.dh == 64)
-                run_attention_t<64>(c, l, ap);
-            else
-                run_attention_t<128>(c, l, ap);
+    // One call site per phase body: the phase kind is a runtime value, so the
+    // GEMV code (schedules + epilogues) exists once instead of once per kind.
+    // The kernel shrank from 33.9k to 21.3k SASS instructions and every phase's
+    // fixed cost with it: code that runs once per layer (epilogues, combines)
+    // was missing the instruction cache under the weight stream (same-box A/B:
+    // 1.1B at 148 SMs 1.162 -> 1.068 ms, 7B 4.32 -> 3.92-3.98, 7B at 36 SMs
+    // 9.43 -> 8.69-8.84). An out-of-line attn_combine (17.8k) measured slower.
+    const int L = a.s.n_layers;
+#pragma unroll 1
+    for (int it = 0; it <= 4 * L; ++it) {
+        const int kind = it == 4 * L ? int(PH_LM) : (it & 3), l = it == 4 * L ? 0 : (it >> 2);
+        run_gemv(c, kind, l, best_v, best_i);
+        if (kind == PH_LM) break;
+        if (kind == PH_QKV) {
+            trace(c, 6);
+            if (!(a.skip & 1)) {
+                if (a.s.dh == 64)
+                    run_attention_t<64>(c, l, ap);
+                else
+                    run_attention_t<128>(c, l, ap);
+            }
+            trace(c, 7);
         }
-        trace(c, 7);
-        grid_sync(c);
-        run_gemv(c, PH_O, l, best_v, best_i);
-        grid_sync(c);
-        run_gemv(c, PH_GU, l, best_v, best_i);
-        grid_sync(c);
-        run_gemv(c, PH_DOWN, l, best_v, best_i);
         grid_sync(c);
     }
-    run_gemv(c, PH_LM, 0, best_v, best_i);
     run_argmax_combine(c, best_v, best_i);
 }
 

@@ -455,8 +455,9 @@ struct Producer {
         const size_t head_stride = size_t(2) * KV_BLOCK_TOKENS * s.dh * 2;
         const uint8_t* layer_base = a.kv_base + kv_offset(s, layer, 0, 0, 0);
         const uint32_t q0 = q;
+        // lane's first stage decoded once, then walked DEC_PRODUCER_LANES stages at a time
+        AttnStage st = attn_stage_of(ap, s.n_kv, min(ap.a0 + lane, ap.a1 - 1));
         for (int i = ap.a0 + lane; i < ap.a1; i += DEC_PRODUCER_LANES) {
-            const AttnStage st = attn_stage_of(ap, s.n_kv, i);
             const int k0 = st.s * bps, p = pos[st.b];
             int nblk = 0;
             if (k0 * KV_BLOCK_TOKENS < p) nblk = (bps == 2 && (k0 + 1) * KV_BLOCK_TOKENS < p) ? 2 : 1;
@@ -472,6 +473,15 @@ struct Producer {
             if (nblk > 1)
                 bulk_g2s(dst + 2u * kv_blk, layer_base + size_t(btrow[k0 + 1]) * a.block_bytes + hoff, 2u * kv_blk,
                          &sm.full[slot]);
+            st.s += DEC_PRODUCER_LANES;  // next stage of this lane: requests inner, kv heads outer
+            while (st.s >= ap.nst[st.b]) {
+                st.s -= ap.nst[st.b];
+                if (++st.b == ap.nb) {
+                    st.b = 0;
+                    ++st.kvh;
+                }
+                if (st.kvh >= s.n_kv) break;  // past the last stage (the loop ends)
+            }
         }
         __syncwarp(DEC_PRODUCER_MASK);
         q = qb = q0 + uint32_t(ap.a1 - ap.a0);
@@ -774,13 +784,19 @@ __device__ __forceinline__ void consume_group(Ctx& c, int gn, int sg, int nch) {
 #pragma unroll
         for (int e = 0; e < 4; ++e) d0[e] = d1[e] = 0.f;
     };
+    // (tile, chunk) of stage i walked incrementally (no per-stage integer division)
+    int ti = c.warp / nch, ch = c.warp - (c.warp / nch) * nch;
     for (int i = c.warp; i < n; i += DEC_NCW) {
-        const int ti = i / nch, ch = i - ti * nch;
         if (ti != cur) {
             if (cur >= 0) flush(cur);
             cur = ti;
         }
         consume_stage(c, c.q + i, ch * DEC_CHUNK_COLS, act_stride, d0, d1);
+        ch += DEC_NCW;
+        while (ch >= nch) {
+            ch -= nch;
+            ++ti;
+        }
     }
     if (cur >= 0) flush(cur);
     c.q += n;

@@ -676,8 +676,60 @@ __device__ __forceinline__ void consume_stage(Ctx& c, uint32_t qi, int act_col, 
     release_stage(c, slot);
 }
 
+// Epilogue operands that do not depend on the tile's sums (the residual rows
+// and the next norm's gamma for O / down, the RoPE (cos, sin) for QKV), loaded
+// by the warp that will run the tile's epilogue BEFORE it consumes the stages:
+// the loads' L2 round trip overlaps the stage loop instead of sitting on the
+// phase's critical path (the epilogue of a single tile took ~2 us at 148 SMs).
+struct EpiPre {
+    int tile;     // -1: nothing prefetched
+    float x[6];   // O / down: h[4] = x[0..3], gamma[2] = x[4..5]; QKV: (cos, sin)[2] = x[0..3]
+};
+__device__ __forceinline__ const float* gamma_after(const DecodeArgs& a, int kind, int layer) {
+    if (kind == PH_O) return a.w.g_mlp + size_t(layer) * a.s.d;
+    return (layer + 1 < a.s.n_layers) ? a.w.g_attn + size_t(layer + 1) * a.s.d : a.w.g_final;
+}
+__device__ __forceinline__ EpiPre epi_prefetch(const Ctx& c, int kind, int layer, int tile) {
+    const DecodeArgs& a = *c.a;
+    const Shape& s = a.s;
+    EpiPre e;
+    e.tile = tile;
+    const int g = c.lane >> 2, t = c.lane & 3;
+#pragma unroll
+    for (int k = 0; k < 6; ++k) e.x[k] = 0.f;
+    if (tile < 0) return e;
+    if (kind == PH_O || kind == PH_DOWN) {
+        const float* gam = gamma_after(a, kind, layer);
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+            const int row = tile * 16 + g + 8 * rr;
+            e.x[4 + rr] = gam[row];
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int b = 2 * t + j;
+                if (b < c.B) e.x[2 * rr + j] = ldcg_f32(a.h + size_t(b) * s.d + row);
+            }
+        }
+    } else if (kind == PH_QKV) {
+        const QkvRow r1 = qkv_row(s, tile * 16 + g);
+        if (r1.section < 2) {
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const int b = 2 * t + j;
+                if (b < c.B) {
+                    const float2 cs = a.w.rope[size_t(c.pos[b]) * (s.dh / 2) + r1.dim];
+                    e.x[2 * j] = cs.x;
+                    e.x[2 * j + 1] = cs.y;
+                }
+            }
+        }
+    }
+    return e;
+}
+
 // ---- GEMV epilogues: lane holds rows (g, g+8) x batch columns (2t, 2t+1) of `tile`.
-__device__ __forceinline__ void epi_qkv(Ctx& c, int layer, int tile, const float v[4], const float* rs) {
+__device__ __forceinline__ void epi_qkv(Ctx& c, int layer, int tile, const float v[4], const float* rs,
+                                        const EpiPre& pre) {
     const DecodeArgs& a = *c.a;
     const Shape& s = a.s;
     const int g = c.lane >> 2, t = c.lane & 3;
@@ -691,7 +743,8 @@ __device__ __forceinline__ void epi_qkv(Ctx& c, int layer, int tile, const float
         const int pos = c.pos[b];
         float o1 = x1, o2 = x2;
         if (r1.section < 2) {
-            const float2 cs = a.w.rope[size_t(pos) * half + r1.dim];
+            const float2 cs = pre.tile == tile ? make_float2(pre.x[2 * j], pre.x[2 * j + 1])
+                                               : a.w.rope[size_t(pos) * half + r1.dim];
             o1 = x1 * cs.x - x2 * cs.y;
             o2 = x2 * cs.x + x1 * cs.y;
         }
@@ -726,7 +779,8 @@ __device__ __forceinline__ void epi_gu(Ctx& c, int tile, const float v[4], const
 // Residual add for the rows this tile owns, the next RMSNorm's numerator and
 // the per-tile sum of squares.
 __device__ __forceinline__ void epi_residual(Ctx& c, int tile, const float v[4], const float* gamma_next,
-                                             float* ss_out) {
+                                             float* ss_out, const EpiPre& pre) {
+    const bool have = pre.tile == tile;
     const DecodeArgs& a = *c.a;
     const int d = a.s.d;
     const int g = c.lane >> 2, t = c.lane & 3;
@@ -734,13 +788,13 @@ __device__ __forceinline__ void epi_residual(Ctx& c, int tile, const float v[4],
 #pragma unroll
     for (int rr = 0; rr < 2; ++rr) {
         const int row = tile * 16 + g + 8 * rr;
-        const float gm = gamma_next[row];
+        const float gm = have ? pre.x[4 + rr] : gamma_next[row];
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const int b = 2 * t + j;
             if (b >= c.B) continue;
             float* hp = a.h + size_t(b) * d + row;
-            const float hv = ldcg_f32(hp) + v[2 * rr + j];
+            const float hv = (have ? pre.x[2 * rr + j] : ldcg_f32(hp)) + v[2 * rr + j];
             *hp = hv;
             a.act[size_t(b) * d + row] = f_to_bf16(hv * gm);
             sq[j] += hv * hv;
@@ -821,7 +875,7 @@ __device__ __forceinline__ float4 warp_sum(const Ctx& c, int ti) {
 // tacc_base >= 0: the tile sums were accumulated across segments in tacc[tacc_base + ti]
 template <typename TileOf>
 __device__ __forceinline__ void epilogue_group(Ctx& c, int kind, int layer, int gn, TileOf tile_of, const float* rs,
-                                               float* best_v, int* best_i, int tacc_base = -1) {
+                                               float* best_v, int* best_i, const EpiPre& pre, int tacc_base = -1) {
     const DecodeArgs& a = *c.a;
     for (int ti = c.warp; ti < gn; ti += DEC_NCW) {
         const int tile = tile_of(ti);
@@ -830,7 +884,7 @@ __device__ __forceinline__ void epilogue_group(Ctx& c, int kind, int layer, int 
         float v[4] = {sv.x, sv.y, sv.z, sv.w};
         switch (kind) {
             case PH_QKV:
-                epi_qkv(c, layer, tile, v, rs);
+                epi_qkv(c, layer, tile, v, rs, pre);
                 // publish the tile to the attention of its KV-head group (no grid barrier
                 // between QKV and attention): stores visible, then one count per tile
                 __threadfence();
@@ -840,12 +894,8 @@ __device__ __forceinline__ void epilogue_group(Ctx& c, int kind, int layer, int 
                                  : "memory");
                 break;
             case PH_GU: epi_gu(c, tile, v, rs); break;
-            case PH_O: epi_residual(c, tile, v, a.w.g_mlp + size_t(layer) * a.s.d, a.ssB); break;
-            case PH_DOWN: {
-                const float* gnext = (layer + 1 < a.s.n_layers) ? a.w.g_attn + size_t(layer + 1) * a.s.d : a.w.g_final;
-                epi_residual(c, tile, v, gnext, a.ssA);
-                break;
-            }
+            case PH_O: epi_residual(c, tile, v, gamma_after(a, PH_O, layer), a.ssB, pre); break;
+            case PH_DOWN: epi_residual(c, tile, v, gamma_after(a, PH_DOWN, layer), a.ssA, pre); break;
             default: {  // lm_head
                 const int g = c.lane >> 2, t = c.lane & 3;
 #pragma unroll
@@ -901,11 +951,12 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
                 if (c.tid == 0) mbar_arrive(&c.sm.dempty[ds]);
                 return;
             }
+            const EpiPre pre = epi_prefetch(c, kind, layer, c.warp < gn ? t0 + c.warp : -1);
             consume_group(c, gn, 0, nch);
             csync();
             if (c.tid == 0) mbar_arrive(&c.sm.dempty[ds]);  // every consumer read it before the csync
             trace(c, 3);
-            epilogue_group(c, kind, layer, gn, [&](int ti) { return t0 + ti; }, rs, best_v, best_i);
+            epilogue_group(c, kind, layer, gn, [&](int ti) { return t0 + ti; }, rs, best_v, best_i, pre);
             csync();  // partials are rewritten by the next group
             trace(c, 4);
         }
@@ -921,6 +972,7 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
         // Segment-outer: each activation segment is loaded once for all of the
         // CTA's tiles (group-outer reloads it per group of 4 tiles); per-tile
         // sums carry across segments in tacc.
+        const EpiPre pre = epi_prefetch(c, kind, layer, c.warp < mt.n ? mt.t0 + c.warp * c.G : -1);
         for (int sg = 0; sg < nseg; ++sg) {
             int c0, c1;
             seg_range(p.K, nseg, sg, c0, c1);
@@ -949,13 +1001,14 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
             }
         }
         trace(c, 3);
-        epilogue_group(c, kind, layer, mt.n, [&](int ti) { return mt.t0 + ti * c.G; }, rs, best_v, best_i, 0);
+        epilogue_group(c, kind, layer, mt.n, [&](int ti) { return mt.t0 + ti * c.G; }, rs, best_v, best_i, pre, 0);
         csync();
         trace(c, 4);
         return;
     }
     for (int g0 = 0; g0 < mt.n; g0 += DEC_MAXT) {
         const int gn = min(DEC_MAXT, mt.n - g0);
+        const EpiPre pre = epi_prefetch(c, kind, layer, c.warp < gn ? mt.t0 + (g0 + c.warp) * c.G : -1);
         for (int sg = 0; sg < nseg; ++sg) {
             int c0, c1;
             seg_range(p.K, nseg, sg, c0, c1);
@@ -972,7 +1025,7 @@ __device__ __forceinline__ void run_gemv(Ctx& c, int kind, int layer, float* bes
         }
         csync();
         trace(c, 3);
-        epilogue_group(c, kind, layer, gn, [&](int ti) { return mt.t0 + (g0 + ti) * c.G; }, rs, best_v, best_i);
+        epilogue_group(c, kind, layer, gn, [&](int ti) { return mt.t0 + (g0 + ti) * c.G; }, rs, best_v, best_i, pre);
         csync();  // partials are rewritten by the next group
         trace(c, 4);
     }

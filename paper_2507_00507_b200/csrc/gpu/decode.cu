@@ -1356,10 +1356,15 @@ __device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPla
         csync();
         return;
     }
-    for (int i = c.warp; i < n; i += DEC_NCW) {
-        const AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0 + i);
-        if (st.pair != cur_pair) {
+    // The warp's stages walked incrementally (DEC_NCW at a time), and ONE flush
+    // site (the pass after the last stage flushes the open pair): attn_flush
+    // inlines two partial-combine variants, so a second call site doubled them.
+    AttnStage st = attn_stage_of(ap, s.n_kv, ap.a0 + min(c.warp, max(n - 1, 0)));
+    for (int i = c.warp;; i += DEC_NCW) {
+        const bool end = i >= n;
+        if (end || st.pair != cur_pair) {
             if (cur_pair >= 0) attn_flush<DH>(c, ap, cur_b, cur_kvh, cur_lo, cur_n, stt);
+            if (end) break;
             // this layer's q / current K,V of the group are written by the QKV phase's
             // tiles of group kvh (any CTA): wait for the group's count, not for the grid
             if (c.lane == 0) {
@@ -1396,13 +1401,23 @@ __device__ __forceinline__ void run_attention_t(Ctx& c, int layer, const AttnPla
             uint32_t slot;
             wait_stage(c, c.q + i, slot);
             release_stage(c, slot);
-            continue;
+        } else {
+            attn_consume<DH>(c, layer, st, c.q + i, stt);
         }
-        attn_consume<DH>(c, layer, st, c.q + i, stt);
         if (i == c.warp) trace(c, 12);
+        st.s += DEC_NCW;  // next stage of this warp: requests inner, kv heads outer
+        while (st.s >= ap.nst[st.b]) {
+            st.s -= ap.nst[st.b];
+            st.pair_lo += ap.nst[st.b];
+            if (++st.b == ap.nb) {
+                st.b = 0;
+                ++st.kvh;
+            }
+            st.pair = st.kvh * ap.nb + st.b;
+            if (st.kvh >= s.n_kv) break;  // past the range (the loop ends)
+        }
     }
     trace(c, 13);
-    if (cur_pair >= 0) attn_flush<DH>(c, ap, cur_b, cur_kvh, cur_lo, cur_n, stt);
     c.q += n;
     trace(c, 14);
     csync();  // warp partials of pre-combined pairs are in shared memory

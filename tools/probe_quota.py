@@ -13,6 +13,10 @@ sys.path.insert(0, ".")
 from paper_2507_00507_b200.gpu import SHAPES, MeshGpu  # noqa: E402
 
 CTX = int(os.environ.get("PROBE_CTX", "1024"))
+try:  # the driver-written measured copy peak of this pool
+    PEAK = float(json.load(open(os.path.join(os.path.dirname(__file__), "..", "MEASURED_PEAKS.json")))["hbm_gbs"])
+except (OSError, KeyError, ValueError):
+    PEAK = 6549.1
 ITERS = int(os.environ.get("PROBE_ITERS", "20"))
 B = 8
 
@@ -32,7 +36,7 @@ def run(name: str, quota: int) -> dict:
     byts = s.weight_bytes_streamed + B * (CTX + 1) * s.kv_bytes_per_token + B * s.d_model * 2
     gbs = byts / ms / 1e6
     return dict(model=name, quota=quota, ms=round(ms, 4), GBps=round(gbs, 1), GBps_per_sm=round(gbs / quota, 2),
-                frac=round(gbs / 6539.2, 3), skip=os.environ.get("MESH_GPU_SKIP", "0"))
+                frac=round(gbs / PEAK, 3), skip=os.environ.get("MESH_GPU_SKIP", "0"))
 
 
 for arg in sys.argv[1:] or ["1b:17,148"]:

@@ -886,8 +886,10 @@ __device__ __forceinline__ void epilogue_group(Ctx& c, int kind, int layer, int 
             case PH_QKV:
                 epi_qkv(c, layer, tile, v, rs, pre);
                 // publish the tile to the attention of its KV-head group (no grid barrier
-                // between QKV and attention): stores visible, then one count per tile
-                __threadfence();
+                // between QKV and attention): one count per tile. The lanes' stores are
+                // ordered before lane 0's release by the warp barrier and the release's
+                // cumulativity (the attention partials use the same pattern); a
+                // __threadfence here made every lane wait for its stores to reach L2.
                 __syncwarp();
                 if (c.lane == 0)
                     asm volatile("red.release.gpu.global.add.s32 [%0], 1;\n" ::"l"(a.qkv_done + tile / qkv_group_tiles(a.s))
